@@ -1,0 +1,229 @@
+"""CPU oracle for the laplacianFoam hot path — TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` (its
+``cpu_baseline`` leg and the ``--impl reference`` arm) may import this
+package.  The product (``paper_2507_18268_b200``) never imports it and
+shares no code with it; ``oracle/lfoam_oracle.c`` is compiled on its own
+(gcc -O2 -ffp-contract=off) into ``oracle/liboracle.so``.
+
+Functions follow SURVEY.md §8(c.1) / PAPER.md Listing 1, §5.2
+ and §6; see the C file header for per-function
+citations.  ``geometry`` recomputes mesh geometry from points/faces.
+Parity pins: tests/test_oracle_*.py.  Unpinned beyond oracle agreement
+("parity unpinned"): PCG iteration counts and residual values after step 0
+(no closed form exists).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from typing import Callable, List, Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "lfoam_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_TYPES = {"fixedValue": 0, "zeroGradient": 1, "processor": 2}
+
+
+def build(force: bool = False) -> str:
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-std=c99", "-O2", "-ffp-contract=off", "-fno-fast-math",
+                               "-fPIC", "-shared", "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+class _Mesh(C.Structure):
+    _fields_ = [("n_cells", C.c_int32), ("n_faces", C.c_int32), ("n_patches", C.c_int32),
+                ("n_bfaces", C.c_int32), ("owner", C.c_void_p), ("neighbour", C.c_void_p),
+                ("mag_sf", C.c_void_p), ("delta", C.c_void_p), ("V", C.c_void_p),
+                ("patch_type", C.c_void_p), ("patch_start", C.c_void_p), ("b_cells", C.c_void_p),
+                ("b_mag_sf", C.c_void_p), ("b_delta", C.c_void_p)]
+
+
+class Perf(C.Structure):
+    _fields_ = [("initial_residual", C.c_double), ("final_residual", C.c_double),
+                ("n_iterations", C.c_int32), ("converged", C.c_int32),
+                ("singular", C.c_int32), ("pad", C.c_int32)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k in ("initial_residual", "final_residual",
+                                              "n_iterations", "converged", "singular")}
+
+
+GSUM = C.CFUNCTYPE(None, C.c_void_p, C.POINTER(C.c_double), C.c_int32)
+HALO = C.CFUNCTYPE(None, C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double))
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = C.CDLL(build())
+        vp = C.c_void_p
+        _lib.orc_group.argtypes = [vp, C.c_int64, C.c_int32, vp, vp]
+        _lib.orc_assemble.argtypes = [C.POINTER(_Mesh), C.c_double, C.c_double, vp, vp, vp, vp, vp, vp, vp]
+        _lib.orc_amul.argtypes = [C.POINTER(_Mesh), vp, vp, vp, vp, vp, vp]
+        _lib.orc_sumA.argtypes = [C.POINTER(_Mesh), vp, vp, vp, vp]
+        _lib.orc_pcg.argtypes = [C.POINTER(_Mesh), vp, vp, vp, vp, vp, C.c_double, C.c_double,
+                                 C.c_int32, C.c_int32, GSUM, HALO, vp, C.POINTER(Perf)]
+        _lib.orc_laplacian_foam.argtypes = [C.POINTER(_Mesh), C.c_double, C.c_double, vp, vp,
+                                            C.c_int32, C.c_double, C.c_double, C.c_int32,
+                                            C.c_int32, GSUM, HALO, vp, C.POINTER(Perf)]
+        _lib.orc_patch_values.argtypes = [C.POINTER(_Mesh), vp, vp]
+    return _lib
+
+
+def _p(a):
+    return a.ctypes.data if a is not None and a.size else None
+
+
+class OMesh:
+    """Flattened view of a meshgen.Mesh (keeps the numpy buffers alive)."""
+
+    def __init__(self, mesh):
+        self.src = mesh
+        self.owner = np.ascontiguousarray(mesh.owner, dtype=np.int32)
+        self.neighbour = np.ascontiguousarray(mesh.neighbour, dtype=np.int32)
+        self.mag_sf = np.ascontiguousarray(mesh.mag_sf, dtype=np.float64)
+        self.delta = np.ascontiguousarray(mesh.delta, dtype=np.float64)
+        self.V = np.ascontiguousarray(mesh.V, dtype=np.float64)
+        self.patch_type = np.array([_TYPES[p.type] for p in mesh.patches], dtype=np.int32)
+        sizes = [p.n_faces for p in mesh.patches]
+        self.patch_start = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int32)
+        cat = lambda name, dt: (np.concatenate([getattr(p, name) for p in mesh.patches]).astype(dt)
+                                if mesh.patches else np.zeros(0, dt))
+        self.b_cells = cat("face_cells", np.int32)
+        self.b_mag_sf = cat("mag_sf", np.float64)
+        self.b_delta = cat("delta", np.float64)
+        self.b_value = cat("value", np.float64)
+        self.n_cells, self.n_faces = int(mesh.n_cells), int(self.owner.shape[0])
+        self.n_bfaces = int(self.b_cells.shape[0])
+        self.s = _Mesh(self.n_cells, self.n_faces, len(sizes), self.n_bfaces,
+                       _p(self.owner), _p(self.neighbour), _p(self.mag_sf), _p(self.delta),
+                       _p(self.V), _p(self.patch_type), _p(self.patch_start), _p(self.b_cells),
+                       _p(self.b_mag_sf), _p(self.b_delta))
+
+    def patch_slices(self):
+        return [slice(int(self.patch_start[i]), int(self.patch_start[i + 1]))
+                for i in range(len(self.patch_start) - 1)]
+
+
+def _om(mesh):
+    return mesh if isinstance(mesh, OMesh) else OMesh(mesh)
+
+
+def group(keys: np.ndarray, n_groups: int):
+    """Stable cell->face grouping (items, starts[n_groups+1])."""
+    keys = np.ascontiguousarray(keys, dtype=np.int32)
+    items = np.zeros(keys.shape[0], np.int32)
+    starts = np.zeros(n_groups + 1, np.int32)
+    rc = lib().orc_group(_p(keys), keys.shape[0], n_groups, _p(items), starts.ctypes.data)
+    if rc:
+        raise ValueError("key out of range")
+    return items, starts
+
+
+def assemble(mesh, DT: float, dt: float, T0: np.ndarray, b_value: Optional[np.ndarray] = None):
+    """Returns dict(diag, upper, source, internal_coeffs, boundary_coeffs)."""
+    om = _om(mesh)
+    T0 = np.ascontiguousarray(T0, dtype=np.float64)
+    bv = om.b_value if b_value is None else np.ascontiguousarray(b_value, np.float64)
+    out = dict(diag=np.zeros(om.n_cells), upper=np.zeros(om.n_faces), source=np.zeros(om.n_cells),
+               internal_coeffs=np.zeros(om.n_bfaces), boundary_coeffs=np.zeros(om.n_bfaces))
+    rc = lib().orc_assemble(C.byref(om.s), DT, dt, _p(T0), _p(bv), _p(out["diag"]),
+                            _p(out["upper"]), _p(out["source"]), _p(out["internal_coeffs"]),
+                            _p(out["boundary_coeffs"]))
+    if rc:
+        raise MemoryError
+    return out
+
+
+def amul(mesh, diag, upper, x, boundary_coeffs=None, x_remote=None):
+    om = _om(mesh)
+    bc = np.zeros(om.n_bfaces) if boundary_coeffs is None else np.ascontiguousarray(boundary_coeffs, np.float64)
+    xr = np.zeros(om.n_bfaces) if x_remote is None else np.ascontiguousarray(x_remote, np.float64)
+    x = np.ascontiguousarray(x, np.float64)
+    y = np.zeros(om.n_cells)
+    lib().orc_amul(C.byref(om.s), _p(np.ascontiguousarray(diag, np.float64)),
+                   _p(np.ascontiguousarray(upper, np.float64)), _p(bc), _p(x), _p(xr), _p(y))
+    return y
+
+
+def sumA(mesh, diag, upper, boundary_coeffs=None):
+    om = _om(mesh)
+    bc = np.zeros(om.n_bfaces) if boundary_coeffs is None else np.ascontiguousarray(boundary_coeffs, np.float64)
+    out = np.zeros(om.n_cells)
+    lib().orc_sumA(C.byref(om.s), _p(np.ascontiguousarray(diag, np.float64)),
+                   _p(np.ascontiguousarray(upper, np.float64)), _p(bc), _p(out))
+    return out
+
+
+def _callbacks(gsum: Optional[Callable], halo: Optional[Callable], n_cells: int, n_bfaces: int):
+    g = GSUM(0)
+    h = HALO(0)
+    if gsum is not None:
+        def _g(ctx, vals, k):
+            arr = np.ctypeslib.as_array(vals, shape=(k,))
+            arr[:] = gsum(arr.copy())
+        g = GSUM(_g)
+    if halo is not None:
+        def _h(ctx, x, xr):
+            xa = np.ctypeslib.as_array(x, shape=(max(n_cells, 1),))[:n_cells].copy()
+            xra = np.ctypeslib.as_array(xr, shape=(max(n_bfaces, 1),))
+            halo(xa, xra[:n_bfaces])
+        h = HALO(_h)
+    return g, h
+
+
+def pcg(mesh, sys: dict, psi: np.ndarray, tol=1e-10, rel_tol=0.0, max_iter=1000, min_iter=0,
+        gsum=None, halo=None):
+    """OpenFOAM PCG (diagonal preconditioner). Returns (psi, perf dict)."""
+    om = _om(mesh)
+    psi = np.array(psi, dtype=np.float64, copy=True)
+    perf = Perf()
+    g, h = _callbacks(gsum, halo, om.n_cells, om.n_bfaces)
+    bc = sys.get("boundary_coeffs")
+    bc = np.zeros(om.n_bfaces) if bc is None else np.ascontiguousarray(bc, np.float64)
+    rc = lib().orc_pcg(C.byref(om.s), _p(np.ascontiguousarray(sys["diag"], np.float64)),
+                       _p(np.ascontiguousarray(sys["upper"], np.float64)), _p(bc),
+                       _p(np.ascontiguousarray(sys["source"], np.float64)), _p(psi),
+                       tol, rel_tol, max_iter, min_iter, g, h, None, C.byref(perf))
+    if rc:
+        raise MemoryError
+    return psi, perf.as_dict()
+
+
+def laplacian_foam(mesh, T0, n_steps, DT=1.0, dt=0.2, tol=1e-10, rel_tol=0.0, max_iter=1000,
+                   min_iter=0, gsum=None, halo=None, b_value=None):
+    """Listing 1 time loop. Returns (T, b_value, [perf dicts])."""
+    om = _om(mesh)
+    T = np.array(T0, dtype=np.float64, copy=True)
+    bv = np.array(om.b_value if b_value is None else b_value, dtype=np.float64, copy=True)
+    perfs = (Perf * max(n_steps, 1))()
+    g, h = _callbacks(gsum, halo, om.n_cells, om.n_bfaces)
+    rc = lib().orc_laplacian_foam(C.byref(om.s), DT, dt, _p(T), _p(bv), n_steps, tol, rel_tol,
+                                  max_iter, min_iter, g, h, None, perfs)
+    if rc:
+        raise MemoryError
+    return T, bv, [perfs[i].as_dict() for i in range(n_steps)]
+
+
+def self_halo(mesh):
+    """Halo callback for a mesh whose processor patches couple to the same
+    rank (pairs of consecutive self-processor patches, matched face by face)."""
+    om = _om(mesh)
+    sl = om.patch_slices()
+    procs = [i for i, p in enumerate(mesh.patches) if p.type == "processor"]
+    pairs = [(procs[i], procs[i + 1]) for i in range(0, len(procs), 2)]
+
+    def halo(x, xr):
+        for a, b in pairs:
+            xr[sl[a]] = x[om.b_cells[sl[b]]]
+            xr[sl[b]] = x[om.b_cells[sl[a]]]
+    return halo

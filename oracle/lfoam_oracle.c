@@ -1,0 +1,326 @@
+/*
+ * lfoam_oracle.c — CPU ORACLE for the laplacianFoam hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py (its cpu_baseline leg and --impl reference arm) may load this
+ * library.  The product (paper_2507_18268_b200, liblfoam.so) never links,
+ * loads or calls it, and shares no code, header or table with it.
+ *
+ * Plain C99, IEEE double, single-threaded, built with -O2 -ffp-contract=off
+ * (no FMA contraction), loops in the order the definitions state them.
+ *
+ * What it computes (PAPER.md = P):
+ *   - laplacianFoam step, P:233-261 (Listing 1): TEqn = fvm::ddt(T) -
+ *     fvm::laplacian(DT,T) == fvOptions(T) (= 0, reading A2); TEqn.solve().
+ *   - Euler ddt (reading A3): diag += rDeltaT*V, source += (rDeltaT*T0)*V.
+ *   - Gauss laplacian, orthogonal two-point flux (reading A4):
+ *     u_f = deltaCoeffs_f*(DT*magSf_f); upper = -u; negSumDiag.
+ *   - boundary coefficients (reading A5; OpenFOAM fvMatrix addBoundaryDiag /
+ *     addBoundarySource): fixedValue diag += a, source += (DT*magSf)*(delta*Tb);
+ *     zeroGradient nothing; processor diag += a, interface coeff = a.
+ *   - lduMatrix::Amul with processor interfaces (y -= bc*x_remote).
+ *   - OpenFOAM PCG + diagonal preconditioner (§5.1, §6): L1
+ *     residual / normFactor, strict '<' (reading A9), singularity 1e-300.
+ *   - CSR cell->face grouping (§5.2): the plain definition — a
+ *     stable counting sort (items grouped by key, ties in input order,
+ *     starts = exclusive scan of counts with the total appended, A13/A14).
+ *
+ * Parity pins for every function live in tests/test_oracle_*.py (closed
+ * forms, SPEC worked examples, dense brute force, invariants).  The PCG
+ * iteration count, normFactor and residuals after step 0 have no closed
+ * form: "parity unpinned" beyond the pins listed in DESIGN.md §Parity.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define ORC_FIXED_VALUE 0
+#define ORC_ZERO_GRADIENT 1
+#define ORC_PROCESSOR 2
+
+typedef struct {
+    int32_t n_cells, n_faces, n_patches, n_bfaces;
+    const int32_t *owner, *neighbour;      /* [n_faces] */
+    const double *mag_sf, *delta, *V;      /* [n_faces], [n_faces], [n_cells] */
+    const int32_t *patch_type;             /* [n_patches] */
+    const int32_t *patch_start;            /* [n_patches+1] into the flat boundary arrays */
+    const int32_t *b_cells;                /* [n_bfaces] faceCells */
+    const double *b_mag_sf, *b_delta;      /* [n_bfaces] */
+} orc_mesh;
+
+typedef struct {
+    double initial_residual, final_residual;
+    int32_t n_iterations, converged, singular, pad;
+} orc_perf;
+
+/* gsum: in-place global sum of k doubles over all ranks (NULL = one rank).
+ * halo: x_remote[i] := value of x across processor boundary face i
+ *       (flat boundary index; non-processor entries untouched). */
+typedef void (*orc_gsum_fn)(void *ctx, double *vals, int32_t k);
+typedef void (*orc_halo_fn)(void *ctx, const double *x, double *x_remote);
+
+/* ------------------------------------------------------------------ CSR */
+/* P:401-429 (§5.2, "List of List", "Sorting owner list", "Starting index"):
+ * group face ids by key.  Definition: starts[g] = #keys < g (n_groups+1
+ * entries, A14); items lists, for each group in ascending order, the input
+ * positions with that key in input order (stable, A13). */
+int orc_group(const int32_t *keys, int64_t m, int32_t n_groups,
+              int32_t *items, int32_t *starts)
+{
+    int64_t i;
+    int32_t g;
+    int32_t *fill;
+    for (g = 0; g <= n_groups; g++) starts[g] = 0;
+    for (i = 0; i < m; i++) {
+        if (keys[i] < 0 || keys[i] >= n_groups) return 1;
+        starts[keys[i] + 1] += 1;
+    }
+    for (g = 0; g < n_groups; g++) starts[g + 1] += starts[g];
+    fill = (int32_t *)malloc(sizeof(int32_t) * (size_t)(n_groups > 0 ? n_groups : 1));
+    if (!fill) return 2;
+    for (g = 0; g < n_groups; g++) fill[g] = starts[g];
+    for (i = 0; i < m; i++) items[fill[keys[i]]++] = (int32_t)i;
+    free(fill);
+    return 0;
+}
+
+/* ------------------------------------------------------------- assembly */
+/* SURVEY §8(c.1) lines 1-4 (OpenFOAM EulerDdtScheme::fvmDdt,
+ * gaussLaplacianScheme::fvmLaplacianUncorrected + negSumDiag, fvMatrix
+ * operator-, addBoundaryDiag/addBoundarySource).
+ *   b_int[i]  = internalCoeffs of boundary face i (a; 0 for zeroGradient)
+ *   b_bnd[i]  = boundaryCoeffs of boundary face i ((DT*magSf)*(delta*Tb)
+ *               for fixedValue, a for processor (interfaceBouCoeffs), 0 zeroGradient)
+ */
+int orc_assemble(const orc_mesh *m, double DT, double dt, const double *T0,
+                 const double *b_value, double *diag, double *upper,
+                 double *source, double *b_int, double *b_bnd)
+{
+    int32_t c, f, p, i;
+    double rDeltaT = 1.0 / dt;
+    double *L = (double *)calloc((size_t)(m->n_cells > 0 ? m->n_cells : 1), sizeof(double));
+    if (!L) return 2;
+    for (c = 0; c < m->n_cells; c++) {
+        diag[c] = rDeltaT * m->V[c];                    /* D[c] */
+        source[c] = (rDeltaT * T0[c]) * m->V[c];        /* S[c] */
+    }
+    for (f = 0; f < m->n_faces; f++) {                 /* file order */
+        double u = m->delta[f] * (DT * m->mag_sf[f]);
+        upper[f] = -u;
+        L[m->owner[f]] -= u;
+        L[m->neighbour[f]] -= u;
+    }
+    for (c = 0; c < m->n_cells; c++) diag[c] = diag[c] - L[c];
+    free(L);
+    for (p = 0; p < m->n_patches; p++) {
+        int32_t t = m->patch_type[p];
+        for (i = m->patch_start[p]; i < m->patch_start[p + 1]; i++) {
+            int32_t cc = m->b_cells[i];
+            double gms = DT * m->b_mag_sf[i];
+            double a = gms * m->b_delta[i];
+            if (t == ORC_FIXED_VALUE) {
+                double bc = gms * (m->b_delta[i] * b_value[i]);
+                diag[cc] += a;
+                source[cc] += bc;
+                b_int[i] = a;
+                b_bnd[i] = bc;
+            } else if (t == ORC_PROCESSOR) {
+                diag[cc] += a;
+                b_int[i] = a;
+                b_bnd[i] = a;
+            } else {
+                b_int[i] = 0.0;
+                b_bnd[i] = 0.0;
+            }
+        }
+    }
+    return 0;
+}
+
+/* ----------------------------------------------------------------- Amul */
+/* lduMatrix::Amul (SURVEY §8(c.1) "Amul(x)"): y = diag*x; face loop in
+ * file order; then processor interfaces y[c] -= bc*x_remote. */
+void orc_amul(const orc_mesh *m, const double *diag, const double *upper,
+              const double *b_bnd, const double *x, const double *x_remote,
+              double *y)
+{
+    int32_t c, f, p, i;
+    for (c = 0; c < m->n_cells; c++) y[c] = diag[c] * x[c];
+    for (f = 0; f < m->n_faces; f++) {
+        y[m->neighbour[f]] += upper[f] * x[m->owner[f]];
+        y[m->owner[f]] += upper[f] * x[m->neighbour[f]];
+    }
+    for (p = 0; p < m->n_patches; p++) {
+        if (m->patch_type[p] != ORC_PROCESSOR) continue;
+        for (i = m->patch_start[p]; i < m->patch_start[p + 1]; i++)
+            y[m->b_cells[i]] -= b_bnd[i] * x_remote[i];
+    }
+}
+
+/* lduMatrix::sumA: row sums incl. interface boundary coeffs. */
+void orc_sumA(const orc_mesh *m, const double *diag, const double *upper,
+              const double *b_bnd, double *sumA)
+{
+    int32_t c, f, p, i;
+    for (c = 0; c < m->n_cells; c++) sumA[c] = diag[c];
+    for (f = 0; f < m->n_faces; f++) {
+        sumA[m->neighbour[f]] += upper[f];
+        sumA[m->owner[f]] += upper[f];
+    }
+    for (p = 0; p < m->n_patches; p++) {
+        if (m->patch_type[p] != ORC_PROCESSOR) continue;
+        for (i = m->patch_start[p]; i < m->patch_start[p + 1]; i++)
+            sumA[m->b_cells[i]] -= b_bnd[i];
+    }
+}
+
+static void gsum(orc_gsum_fn fn, void *ctx, double *v, int32_t k)
+{
+    if (fn) fn(ctx, v, k);
+}
+
+static void amul_halo(const orc_mesh *m, const double *diag, const double *upper,
+                      const double *b_bnd, const double *x, double *xr, double *y,
+                      orc_halo_fn halo, void *ctx)
+{
+    if (halo) halo(ctx, x, xr);
+    orc_amul(m, diag, upper, b_bnd, x, xr, y);
+}
+
+static int converged(double res, double init, double tol, double rel_tol)
+{
+    return res < tol || (rel_tol > 0.0 && res < rel_tol * init);
+}
+
+/* ------------------------------------------------------------------ PCG */
+/* OpenFOAM PCG::scalarSolve with diagonalPreconditioner, SURVEY §8(c.1)
+ * "PCG" block, step by step in its order. */
+int orc_pcg(const orc_mesh *m, const double *diag, const double *upper,
+            const double *b_bnd, const double *source, double *psi,
+            double tol, double rel_tol, int32_t max_iter, int32_t min_iter,
+            orc_gsum_fn gsum_fn, orc_halo_fn halo_fn, void *ctx, orc_perf *perf)
+{
+    int32_t n = m->n_cells, c;
+    size_t nn = (size_t)(n > 0 ? n : 1), nb = (size_t)(m->n_bfaces > 0 ? m->n_bfaces : 1);
+    double *wA = (double *)calloc(nn, sizeof(double));
+    double *rA = (double *)calloc(nn, sizeof(double));
+    double *pA = (double *)calloc(nn, sizeof(double));
+    double *rD = (double *)calloc(nn, sizeof(double));
+    double *tmp = (double *)calloc(nn, sizeof(double));
+    double *xr = (double *)calloc(nb, sizeof(double));
+    double s[2], normFactor, psibar, wArA, wArAold, wApA, alpha, beta;
+    int32_t it = 0;
+    if (!wA || !rA || !pA || !rD || !tmp || !xr) return 2;
+
+    memset(perf, 0, sizeof(*perf));
+    /* wA = A psi ; rA = source - wA */
+    amul_halo(m, diag, upper, b_bnd, psi, xr, wA, halo_fn, ctx);
+    for (c = 0; c < n; c++) rA[c] = source[c] - wA[c];
+
+    /* normFactor: psibar = gAverage(psi); tmp = sumA*psibar;
+     * gSum(|wA - tmp| + |source - tmp|) + 1e-20 */
+    s[0] = 0.0;
+    for (c = 0; c < n; c++) s[0] += psi[c];
+    s[1] = (double)n;
+    gsum(gsum_fn, ctx, s, 2);
+    psibar = s[1] > 0.0 ? s[0] / s[1] : 0.0;
+    orc_sumA(m, diag, upper, b_bnd, tmp);
+    for (c = 0; c < n; c++) tmp[c] *= psibar;
+    s[0] = 0.0;
+    for (c = 0; c < n; c++) s[0] += fabs(wA[c] - tmp[c]) + fabs(source[c] - tmp[c]);
+    gsum(gsum_fn, ctx, s, 1);
+    normFactor = s[0] + 1e-20;
+
+    s[0] = 0.0;
+    for (c = 0; c < n; c++) s[0] += fabs(rA[c]);
+    gsum(gsum_fn, ctx, s, 1);
+    perf->initial_residual = s[0] / normFactor;
+    perf->final_residual = perf->initial_residual;
+
+    if (min_iter > 0 || !converged(perf->final_residual, perf->initial_residual, tol, rel_tol)) {
+        for (c = 0; c < n; c++) rD[c] = 1.0 / diag[c];
+        wArA = 1e20; /* OpenFOAM solverPerformance::great_ */
+        do {
+            wArAold = wArA;
+            for (c = 0; c < n; c++) wA[c] = rD[c] * rA[c];          /* precondition */
+            s[0] = 0.0;
+            for (c = 0; c < n; c++) s[0] += wA[c] * rA[c];
+            gsum(gsum_fn, ctx, s, 1);
+            wArA = s[0];
+            if (it == 0) {
+                for (c = 0; c < n; c++) pA[c] = wA[c];
+            } else {
+                beta = wArA / wArAold;
+                for (c = 0; c < n; c++) pA[c] = wA[c] + beta * pA[c];
+            }
+            amul_halo(m, diag, upper, b_bnd, pA, xr, wA, halo_fn, ctx);
+            s[0] = 0.0;
+            for (c = 0; c < n; c++) s[0] += wA[c] * pA[c];
+            gsum(gsum_fn, ctx, s, 1);
+            wApA = s[0];
+            if (fabs(wApA) / normFactor < 1e-300) {              /* checkSingularity */
+                perf->singular = 1;
+                break;
+            }
+            alpha = wArA / wApA;
+            for (c = 0; c < n; c++) {
+                psi[c] += alpha * pA[c];
+                rA[c] -= alpha * wA[c];
+            }
+            s[0] = 0.0;
+            for (c = 0; c < n; c++) s[0] += fabs(rA[c]);
+            gsum(gsum_fn, ctx, s, 1);
+            perf->final_residual = s[0] / normFactor;
+        } while ((++it < max_iter &&
+                  !converged(perf->final_residual, perf->initial_residual, tol, rel_tol)) ||
+                 it < min_iter);
+    }
+    perf->n_iterations = it;
+    perf->converged = converged(perf->final_residual, perf->initial_residual, tol, rel_tol);
+    free(wA); free(rA); free(pA); free(rD); free(tmp); free(xr);
+    return 0;
+}
+
+/* correctBoundaryConditions for the patch values (a6): zeroGradient
+ * Tb = T[faceCells]; fixedValue unchanged. */
+void orc_patch_values(const orc_mesh *m, const double *T, double *b_value)
+{
+    int32_t p, i;
+    for (p = 0; p < m->n_patches; p++) {
+        if (m->patch_type[p] != ORC_ZERO_GRADIENT) continue;
+        for (i = m->patch_start[p]; i < m->patch_start[p + 1]; i++)
+            b_value[i] = T[m->b_cells[i]];
+    }
+}
+
+/* ------------------------------------------------------- laplacianFoam */
+/* Listing 1: for each step: assemble TEqn from T0 = T, solve
+ * with psi = T (initial guess = old T), correct boundary values. */
+int orc_laplacian_foam(const orc_mesh *m, double DT, double dt, double *T,
+                       double *b_value, int32_t n_steps, double tol,
+                       double rel_tol, int32_t max_iter, int32_t min_iter,
+                       orc_gsum_fn gsum_fn, orc_halo_fn halo_fn, void *ctx,
+                       orc_perf *perf)
+{
+    size_t nn = (size_t)(m->n_cells > 0 ? m->n_cells : 1);
+    size_t nf = (size_t)(m->n_faces > 0 ? m->n_faces : 1);
+    size_t nb = (size_t)(m->n_bfaces > 0 ? m->n_bfaces : 1);
+    double *diag = (double *)malloc(nn * sizeof(double));
+    double *source = (double *)malloc(nn * sizeof(double));
+    double *upper = (double *)malloc(nf * sizeof(double));
+    double *b_int = (double *)malloc(nb * sizeof(double));
+    double *b_bnd = (double *)malloc(nb * sizeof(double));
+    int32_t s;
+    int rc = 0;
+    if (!diag || !source || !upper || !b_int || !b_bnd) return 2;
+    for (s = 0; s < n_steps && rc == 0; s++) {
+        rc = orc_assemble(m, DT, dt, T, b_value, diag, upper, source, b_int, b_bnd);
+        if (rc == 0)
+            rc = orc_pcg(m, diag, upper, b_bnd, source, T, tol, rel_tol, max_iter,
+                         min_iter, gsum_fn, halo_fn, ctx, &perf[s]);
+        orc_patch_values(m, T, b_value);
+    }
+    free(diag); free(source); free(upper); free(b_int); free(b_bnd);
+    return rc;
+}
