@@ -1,0 +1,320 @@
+#!/usr/bin/env python
+"""laplacianFoam hot-path benchmark (driver contract).
+
+One bench step = one laplacianFoam time step (fvm::ddt + fvm::laplacian
+assembly fused with the PCG setup, then the diagonal-PCG solve to tol 1e-10)
+on the BASELINE config (default: config 2, 100^3 cube, 1M cells).  Metric:
+cell-updates/s = n_cells * steps / device time.  Inputs are resident in HBM;
+L2 is flushed (256 MiB write) between timed steps, outside the events.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+N>1: launch under torchrun; the mesh is decomposed into N contiguous cell
+blocks (z-slabs) with processor patches; value = all cells * K / max-rank time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import meshgen  # noqa: E402
+
+METRIC = "cell-updates/sec per laplacianFoam step"
+UNIT = "cell-updates/s"
+DT, DELTA_T, TOL = 1.0, 0.2, 1e-10
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-steps", type=int, default=0, help="oracle steps for cpu_baseline (0 = auto)")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def workload_name(cfg):
+    c = meshgen.CONFIGS[cfg]
+    return f"cube{c['N']}^3{'-permuted' if c['permuted'] else ''}"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].strip() == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic(cfg, kernel):
+    """Per-launch DRAM bytes of `kernel` from the committed ncu summary, or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(f"config{cfg}", {}).get(kernel)
+    except Exception:
+        return None
+
+
+# --------------------------------------------------------------- oracle arm
+def oracle_rate(mesh, T0, steps):
+    import oracle
+    om = oracle.OMesh(mesh)
+    t0 = time.perf_counter()
+    _, _, perfs = oracle.laplacian_foam(om, T0, steps, DT=DT, dt=DELTA_T, tol=TOL)
+    dt = time.perf_counter() - t0
+    return mesh.n_cells * steps / dt, dt, perfs
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    cfg = args.config
+    mesh = meshgen.config_mesh(cfg)
+    T0 = meshgen.canonical_field(mesh)
+    K = min(args.steps, 20)
+    W = min(args.warmup, 1)
+    if W:
+        oracle_rate(mesh, T0, W)
+    rate, secs, perfs = oracle_rate(mesh, T0, K)
+    its = [p["n_iterations"] for p in perfs]
+    sample = (f"first {K} laplacianFoam steps of {workload_name(cfg)} (of --steps {args.steps}); "
+              f"single-threaded C oracle, PCG iterations/step {min(its)}-{max(its)}")
+    line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": K, "warmup": W, "ms_per_step": secs / K * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_name(cfg), "n_cells": mesh.n_cells, "global_batch": 1,
+                       "seq_len": 0, "parallelism": "cpu-1core"},
+            "cpu_baseline": {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- GPU arm
+def run_ours(args):
+    import torch
+    import paper_2507_18268_b200 as P
+
+    ws, rank, local = dist_env()
+    assert ws == args.gpus or ws == 1, "launch N>1 under torchrun with --gpus N"
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    ctx = P.Context(local, stream=stream)
+
+    cfg = args.config
+    gmesh = meshgen.config_mesh(cfg)
+    n_global = gmesh.n_cells
+    T0g = meshgen.canonical_field(gmesh)
+    if ws > 1:
+        from paper_2507_18268_b200 import decompose
+        uid = [P.Context.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx.comm_init(uid[0], ws, rank)
+        part = decompose.slab_partition(gmesh, ws)
+        m, cells = decompose.local_mesh(gmesh, part, rank)
+        T0 = T0g[cells]
+    else:
+        m, T0 = gmesh, T0g
+    del gmesh
+    mesh = P.Mesh(ctx, m)
+    n_local = m.n_cells
+    F_local = m.n_faces
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+
+    # warm-up (W >= 3 steps), then reset to step 0 of the case
+    mesh.set_T(T0)
+    mesh.step(max(args.warmup, 3), DT, DELTA_T, tol=TOL)
+
+    def timed_pass(instrument=False):
+        mesh.set_T(T0)
+        ctx.set_instrumentation(instrument)  # also resets the launch counters
+        perfs = []
+        barrier()
+        torch.cuda.synchronize()
+        for k in range(args.steps):
+            flush.fill_(float(k))          # L2 flush, outside the events
+            a, b = ev[k]
+            a.record(stream)
+            perfs += mesh.step(1, DT, DELTA_T, tol=TOL)
+            b.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ms = sum(a.elapsed_time(b) for a, b in ev)
+        return ms, perfs
+
+    with ClockSampler(local) as clk:
+        total_ms, perfs = timed_pass(False)
+    launches = ctx.launch_count()
+    if dist is not None:
+        t = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = n_global * args.steps / (total_ms / 1e3)
+
+    # instrumented replay of the same K steps: per-kernel CUDA-event durations
+    inst_ms, perfs_i = timed_pass(True)
+    n_p1, ms_p1 = ctx.kernel_stats("phase1")
+    n_p2, ms_p2 = ctx.kernel_stats("phase2")
+    n_as, ms_as = ctx.kernel_stats("assemble")
+    iters = sum(p["n_iterations"] for p in perfs_i)
+    bytes_p1 = 56 * n_local + 16 * F_local          # per full phase-1 launch
+    bytes_p2 = 40 * n_local
+    peak, peak_kind = measured_peak()
+    achieved = bytes_p1 * iters / (ms_p1 / 1e3) / 1e9 if ms_p1 > 0 else None
+    traffic = ncu_traffic(cfg, "k_phase1") if ws == 1 else None
+
+    # e2e through the public API with host buffers (pinned), copies inside the region
+    T0h = torch.from_numpy(np.ascontiguousarray(T0)).pin_memory()
+    Th = torch.empty(n_local, dtype=torch.float64).pin_memory()
+    mesh.set_T(T0)
+    barrier()
+    torch.cuda.synchronize()
+    e2e_ms = 0.0
+    for k in range(args.steps):
+        flush.fill_(float(k))
+        a, b = ev[k]
+        a.record(stream)
+        mesh.set_T(T0h.numpy() if k == 0 else Th.numpy())   # H2D of this step's input state
+        mesh.step(1, DT, DELTA_T, tol=TOL)
+        mesh.get_T(Th.numpy())                              # D2H of this step's result
+        b.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = sum(a.elapsed_time(b) for a, b in ev)
+    if dist is not None:
+        t = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e = n_global * args.steps / (e2e_ms / 1e3)
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        steps = args.cpu_steps or (2 if n_global <= 2_000_000 else 1)
+        full = meshgen.config_mesh(cfg)
+        rate, secs, po = oracle_rate(full, meshgen.canonical_field(full), steps)
+        cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"first {steps} laplacianFoam steps of {workload_name(cfg)} "
+                         f"({secs:.1f} s, PCG iterations {[p['n_iterations'] for p in po]})"}
+
+    its = [p["n_iterations"] for p in perfs]
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak" if ws == 1 else "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": workload_name(cfg), "n_cells": n_global, "steps_per_run": args.steps,
+                   "global_batch": 1, "seq_len": 0, "parallelism": f"dp{ws}" if ws == 1 else f"domain{ws}",
+                   "l2": "flushed between timed steps (256 MiB write)", "tol": TOL,
+                   "pcg_iterations_per_step": {"min": min(its), "max": max(its), "mean": sum(its) / len(its)}},
+        "roofline": {"bound": "hbm", "kernel": "k_phase1", "achieved": achieved, "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": (achieved / peak) if achieved else None,
+                     "traffic": traffic, "bytes_per_launch": bytes_p1, "launches": n_p1,
+                     "avg_launch_ms": ms_p1 / max(n_p1, 1),
+                     "share_of_step": ms_p1 / inst_ms if inst_ms > 0 else None,
+                     "phase2": {"achieved": bytes_p2 * iters / (ms_p2 / 1e3) / 1e9 if ms_p2 > 0 else None,
+                                "avg_launch_ms": ms_p2 / max(n_p2, 1), "share_of_step": ms_p2 / inst_ms},
+                     "assemble": {"avg_launch_ms": ms_as / max(n_as, 1), "share_of_step": ms_as / inst_ms},
+                     "instrumented_ms_per_step": inst_ms / args.steps},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * n_local,
+                "d2h_bytes_per_step": 8 * n_local},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    mesh.close()
+    ctx.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

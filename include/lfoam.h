@@ -1,0 +1,226 @@
+/*
+ * lfoam.h — C ABI of the B200 laplacianFoam hot-path library (liblfoam.so).
+ *
+ * One implicit time step of dT/dt = div(DT grad T) on a finite-volume mesh in
+ * OpenFOAM LDU face addressing (PAPER.md = P):
+ *   TEqn( fvm::ddt(T) - fvm::laplacian(DT, T) == fvOptions(T) ); TEqn.solve();
+ *   Listing 1, P:233-261 (§5.1); PCG + diagonal preconditioner.
+ * The library assembles the matrix (fvm::ddt + fvm::laplacian face loop as an
+ * atomic-free cell gather over the paper's CSR lists, §5.2), injects
+ * boundary coefficients (P:457-497 pattern), runs lduMatrix::Amul and the
+ * OpenFOAM PCG with fused reductions, on one or several B200 GPUs (processor
+ * patches + NCCL, one process per GPU, §6.2).
+ *
+ * Conventions for every call:
+ *   - Return value lf_status; LF_OK = 0.  No exceptions or aborts cross the
+ *     ABI; lf_last_error() gives a thread-local detail string.
+ *   - Labels are int32, values IEEE fp64 (reading A12).
+ *   - "host" pointers are plain CPU memory; "device" pointers are CUDA device
+ *     memory on the context's device (e.g. torch tensors' data_ptr()).
+ *   - All device work is enqueued on the context's stream (the one passed to
+ *     lf_context_create, or a private non-blocking stream if NULL).
+ *   - Calls are not thread-safe on the same context.
+ *   - After LF_ERR_CUDA / LF_ERR_NCCL a mesh is unusable: later calls on it
+ *     return LF_ERR_STATE.
+ */
+#ifndef LFOAM_H
+#define LFOAM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LF_VERSION 1
+
+#if defined(__GNUC__)
+#define LF_API __attribute__((visibility("default")))
+#else
+#define LF_API
+#endif
+
+typedef enum {
+  LF_OK = 0,
+  LF_ERR_INVALID_ARG = 1, /* bad label/size/value; argument named in lf_last_error() */
+  LF_ERR_STATE = 2,       /* object unusable or call out of order */
+  LF_ERR_OOM = 3,         /* device or host allocation failed */
+  LF_ERR_CUDA = 4,        /* CUDA runtime error */
+  LF_ERR_NCCL = 5,        /* NCCL missing or failed */
+  LF_ERR_INTERNAL = 6
+} lf_status;
+
+LF_API const char *lf_status_string(lf_status s);
+LF_API const char *lf_last_error(void);
+LF_API int lf_version(void);
+
+/* ------------------------------------------------------------- context */
+typedef struct lf_context lf_context;
+
+/* device: CUDA ordinal.  cuda_stream: a cudaStream_t (borrowed, must outlive
+ * the context) or NULL for a private non-blocking stream. */
+LF_API lf_status lf_context_create(int device, void *cuda_stream, lf_context **out);
+LF_API lf_status lf_context_destroy(lf_context *ctx);
+
+/* Multi-GPU ("1 MPI process for each GPU").
+ * lf_comm_unique_id writes a 128-byte NCCL unique id (call on rank 0 and
+ * broadcast it, e.g. through torch.distributed).  lf_comm_init joins the
+ * communicator; all later reductions and processor-patch halos of meshes
+ * created on this context are global over it.  NCCL is loaded at run time
+ * (libnccl.so.2); if absent: LF_ERR_NCCL.  nranks == 1 is valid. */
+LF_API lf_status lf_comm_unique_id(void *out_128_bytes);
+LF_API lf_status lf_comm_init(lf_context *ctx, const void *unique_id_128, int nranks, int rank);
+LF_API lf_status lf_comm_info(const lf_context *ctx, int *nranks, int *rank);
+
+/* ---------------------------------------------------------------- mesh */
+typedef enum {
+  LF_PATCH_FIXED_VALUE = 0,   /* Dirichlet T_b (fvPatchField fixedValue)       */
+  LF_PATCH_ZERO_GRADIENT = 1, /* homogeneous Neumann, contributes nothing      */
+  LF_PATCH_PROCESSOR = 2      /* coupled to cells of rank neighb_rank          */
+} lf_patch_type;
+
+typedef struct {
+  lf_patch_type type;
+  int32_t n_faces;
+  const int32_t *face_cells;   /* host [n_faces] local cell labels (faceCells)             */
+  const double *mag_sf;        /* host [n_faces] |Sf| > 0                                  */
+  const double *delta_coeffs;  /* host [n_faces] 1/|n.(Cf-C_P)| (wall), 1/|C_N-C_P| (proc)  */
+  const double *value;         /* host [n_faces] fixedValue T_b, or NULL (= 0)             */
+  int32_t neighb_rank;         /* processor only.  Faces must be in the same order on both
+                                  sides (e.g. ascending global face id).  neighb_rank ==
+                                  own rank: coupled to the NEXT processor patch that also
+                                  names the own rank (self pairs, a loopback used by tests). */
+} lf_patch_desc;
+
+typedef struct {
+  int32_t n_cells;             /* >= 1                                                      */
+  int32_t n_faces;             /* internal faces, >= 0                                      */
+  int32_t n_patches;
+  const int32_t *owner;        /* host [n_faces] 0 <= owner,neighbour < n_cells,           */
+  const int32_t *neighbour;    /* owner != neighbour; any face order, any orientation      */
+  const double *mag_sf;        /* host [n_faces] |Sf|                                       */
+  const double *delta_coeffs;  /* host [n_faces] 1/|C_N - C_P| (orthogonal meshes, A4)      */
+  const double *V;             /* host [n_cells] > 0                                        */
+  const lf_patch_desc *patches;/* host [n_patches]                                          */
+  int32_t renumber;            /* 0 keep numbering; 1 reverse Cuthill-McKee inside the
+                                  library (fields still speak the caller's numbering)      */
+} lf_mesh_desc;
+
+typedef struct lf_mesh lf_mesh;
+
+/* Copies every host array (caller keeps ownership), validates labels and
+ * values (LF_ERR_INVALID_ARG), uploads to the device and builds the
+ * atomic-free cell->face lists of P:387-429 (§5.2) on the GPU:
+ *   internal faces re-sorted upper-triangular (owner, then neighbour),
+ *   ownerStart[n+1]; losort = stable argsort of neighbour ("neighbourList"),
+ *   losortStart[n+1]; per-cell boundary-face groups (facePatchIndex/Start,
+ *   P:471-481).  Allocates every work array once (no per-step allocation,
+ *   the lesson of P:728).  T starts at 0. */
+LF_API lf_status mesh_create(lf_context *ctx, const lf_mesh_desc *desc, lf_mesh **out);
+LF_API lf_status mesh_destroy(lf_mesh *mesh);
+
+/* Sizes: n_cells, internal faces, total boundary faces, device bytes held. */
+LF_API lf_status lf_mesh_info(const lf_mesh *mesh, int32_t *n_cells, int32_t *n_faces,
+                       int32_t *n_boundary_faces, int64_t *device_bytes);
+
+/* Host copies of the addressing built by mesh_create, for tests (internal
+ * numbering and face order).  Any pointer may be NULL.
+ *   owner_start[n+1], losort[F], losort_start[n+1], face_order[F] (internal
+ *   face i = caller's face face_order[i]), cell_order[n] (internal cell i =
+ *   caller's cell cell_order[i]). */
+LF_API lf_status lf_mesh_export_addressing(const lf_mesh *mesh, int32_t *owner_start,
+                                    int32_t *losort, int32_t *losort_start,
+                                    int32_t *face_order, int32_t *cell_order);
+
+/* Device arrays between the caller's and the internal cell numbering
+ * (identity copy when renumber == 0).  to_internal: 1 caller->internal. */
+LF_API lf_status lf_permute(const lf_mesh *mesh, int to_internal, const double *in_dev, double *out_dev);
+
+/* --------------------------------------------------------------- fields */
+typedef enum {
+  LF_FIELD_T = 0,            /* cell values, n = n_cells, patch = -1            */
+  LF_FIELD_PATCH_VALUE = 1   /* boundary values of patch `patch`, n = n_faces.
+                                fixedValue: T_b (set/get).  zeroGradient: get
+                                returns T[faceCells] (correctBoundaryConditions);
+                                set is ignored.  processor: get returns 0.      */
+} lf_field;
+
+/* on_device: 1 if v is a device pointer, 0 host.  Stream-ordered; a host
+ * field_get returns after the copy is complete. */
+LF_API lf_status field_set(lf_mesh *mesh, lf_field f, int32_t patch, const double *v, int64_t n, int on_device);
+LF_API lf_status field_get(const lf_mesh *mesh, lf_field f, int32_t patch, double *v, int64_t n, int on_device);
+
+/* ---------------------------------------------------------- assembly */
+typedef struct {
+  double DT;   /* uniform diffusivity > 0 (reading A11)   */
+  double dt;   /* time step > 0 (P:608 uses 0.2 s)        */
+} lf_laplacian_params;
+
+typedef struct lf_ldu lf_ldu;   /* owned by its mesh, reused every step */
+
+/* fvm::ddt(T) - fvm::laplacian(DT,T) with T0 = current T (Listing 1
+ * line 12; readings A3-A5): per internal face u = delta*(DT*magSf),
+ * upper = -u; diag = V/dt + sum u (+ boundary internalCoeffs);
+ * source = (T0/dt)*V (+ fixedValue boundaryCoeffs).  One kernel, a per-cell
+ * gather (no float atomics); deterministic.  Errors: DT/dt <= 0 -> INVALID_ARG. */
+LF_API lf_status laplacian_assemble(lf_mesh *mesh, const lf_laplacian_params *p, lf_ldu **sys);
+
+/* Host copies in the CALLER's numbering and face order; any pointer may be
+ * NULL.  internal/boundary_coeffs: [total boundary faces] in patch order
+ * (internalCoeffs = a; boundaryCoeffs = a*T_b fixedValue, a processor). */
+LF_API lf_status lf_ldu_export(const lf_ldu *sys, double *diag, double *upper, double *source,
+                        double *internal_coeffs, double *boundary_coeffs);
+
+/* y = A x (lduMatrix::Amul incl. processor interfaces).  x_dev, y_dev:
+ * device [n_cells] in INTERNAL numbering (== caller's when renumber == 0),
+ * must not alias.  Asynchronous, stream-ordered. */
+LF_API lf_status ldu_amul(const lf_ldu *sys, const double *x_dev, double *y_dev);
+
+/* ---------------------------------------------------------------- PCG */
+typedef struct {
+  double tolerance;   /* absolute on the normalised L1 residual (1e-10)   */
+  double rel_tol;     /* 0 = off                                          */
+  int32_t max_iter;   /* 1000 (OpenFOAM default)                          */
+  int32_t min_iter;   /* 0                                                */
+} lf_solver_controls;
+
+typedef struct {
+  double initial_residual, final_residual;
+  int32_t n_iterations, converged, singular, reserved;
+} lf_solver_perf;
+
+/* OpenFOAM PCG with diagonal preconditioner:
+ * psi_dev (device [n_cells], internal numbering) is the initial guess and
+ * receives the solution.  Two fused kernels per iteration; alpha, beta and
+ * the stopping rule are evaluated on the device.  Returns once *out is on
+ * the host.  Non-convergence and singularity are LF_OK with flags set. */
+LF_API lf_status pcg_solve(lf_ldu *sys, double *psi_dev, const lf_solver_controls *c, lf_solver_perf *out);
+
+/* n_steps laplacianFoam time steps on the mesh's T field: each step
+ * assembles (fused with the PCG setup) and solves in place (Listing 1).
+ * per_step: host [n_steps] or NULL. */
+LF_API lf_status laplacianFoam_step(lf_mesh *mesh, const lf_laplacian_params *p,
+                             const lf_solver_controls *c, int32_t n_steps,
+                             lf_solver_perf *per_step);
+
+/* ------------------------------------------------------- instrumentation */
+/* Kernel kinds for lf_kernel_stats. */
+typedef enum {
+  LF_K_ASSEMBLE = 0, LF_K_SETUP = 1, LF_K_PHASE1 = 2, LF_K_PHASE2 = 3,
+  LF_K_AMUL = 4, LF_K_SUMPSI = 5, LF_K_PACK = 6, LF_K_COUNT = 7
+} lf_kernel_kind;
+
+/* enable != 0: bracket every launch of the hot kernels with CUDA events on
+ * the context stream and accumulate their durations (timings are read back
+ * at the per-solve sync).  Counters reset on enable. */
+LF_API lf_status lf_set_instrumentation(lf_context *ctx, int enable);
+/* launches and summed device milliseconds of one kernel kind since enable;
+ * also the number of kernels the library launched in total. */
+LF_API lf_status lf_kernel_stats(const lf_context *ctx, lf_kernel_kind k, int64_t *launches,
+                          double *total_ms);
+LF_API lf_status lf_launch_count(const lf_context *ctx, int64_t *kernels_launched);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LFOAM_H */

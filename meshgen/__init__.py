@@ -11,10 +11,12 @@ synthetic inputs"): unit cube [0,1]^3, cell c = i + N*j + N^2*k, internal
 faces upper-triangular, six patches xmin,xmax,ymin,ymax,zmin,zmax, DT=1,
 dt=0.2, fixedValue 0 walls, T0 = sin(pi x) sin(pi y) sin(pi z).
 """
-from .cube import (Mesh, Patch, block_mesh, permute_mesh, sine_field,
+from .cube import (Mesh, Patch, block_mesh, permute_mesh, sine_field, canonical_field,
+                   CANONICAL_AMPLITUDE,
                    cosine_field, multimode_field, random_field, hot_plate,
                    cube_counts, mesh_points_faces, CONFIGS, config_mesh)
 
-__all__ = ["Mesh", "Patch", "block_mesh", "permute_mesh", "sine_field",
+__all__ = ["Mesh", "Patch", "block_mesh", "permute_mesh", "sine_field", "canonical_field",
+           "CANONICAL_AMPLITUDE",
            "cosine_field", "multimode_field", "random_field", "hot_plate",
            "cube_counts", "mesh_points_faces", "CONFIGS", "config_mesh"]

@@ -181,6 +181,21 @@ def sine_field(mesh: Mesh, k=(1, 1, 1), amp: float = 1.0) -> np.ndarray:
     return out
 
 
+# Reading A30: the decaying sine case loses a factor g ~ 1/6.9
+# per step (g^100 ~ 1e-84 at dt = 0.2).  OpenFOAM's normFactor carries an
+# absolute floor (solverPerformance::small_ = 1e-20); once the field falls
+# to ~1e-20 the solver "converges" with ~0 iterations and the run degenerates
+# into empty steps.  The problem is linear and homogeneous (T_b = 0), so the
+# canonical bench/full-run field is the same mode scaled by 1e80: the decay is
+# identical (T^n = g^n T0) and the field ends at ~1e-4 after 100 steps, far
+# above the floor; squares stay < 1e170.
+CANONICAL_AMPLITUDE = 1e80
+
+
+def canonical_field(mesh: Mesh) -> np.ndarray:
+    return sine_field(mesh, amp=CANONICAL_AMPLITUDE)
+
+
 def cosine_field(mesh: Mesh, k=(1, 2, 0), amp: float = 1.0, offset: float = 0.0) -> np.ndarray:
     """offset + amp * prod_d cos(k_d pi x_d / L_d): the zeroGradient eigenmode."""
     C = mesh.cell_centres()

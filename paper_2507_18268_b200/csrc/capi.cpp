@@ -1,0 +1,415 @@
+// C ABI entry points (include/lfoam.h).  Every call catches everything and
+// maps it to an lf_status; nothing throws or aborts across the boundary.
+#include <cstdio>
+
+#include "host.h"
+
+using namespace lf;
+
+namespace lf {
+void mesh_create_impl(lf_context *ctx, const lf_mesh_desc *d, lf_mesh **out);
+}
+
+static thread_local std::string g_last_error;
+
+template <class F>
+static lf_status guard(F &&fn, lf_mesh *M = nullptr) {
+  try {
+    if (M && M->broken) throw Error{LF_ERR_STATE, "mesh unusable after an earlier CUDA/NCCL error"};
+    fn();
+    return LF_OK;
+  } catch (const Error &e) {
+    g_last_error = e.msg;
+    if (M && (e.st == LF_ERR_CUDA || e.st == LF_ERR_NCCL)) M->broken = true;
+    return e.st;
+  } catch (const std::bad_alloc &) {
+    g_last_error = "host allocation failed";
+    return LF_ERR_OOM;
+  } catch (const std::exception &e) {
+    g_last_error = e.what();
+    return LF_ERR_INTERNAL;
+  } catch (...) {
+    g_last_error = "unknown exception";
+    return LF_ERR_INTERNAL;
+  }
+}
+
+// ------------------------------------------------------------- context
+void lf_context::launch(int kind, const std::function<void()> &fn) {
+  if (capturing) {  // recorded into a graph; counted when the graph is launched
+    fn();
+    LF_CUDA(cudaGetLastError());
+    return;
+  }
+  if (instrument) {
+    cudaEvent_t a = event(), b = event();
+    LF_CUDA(cudaEventRecord(a, stream));
+    fn();
+    LF_CUDA(cudaGetLastError());
+    LF_CUDA(cudaEventRecord(b, stream));
+    pending.push_back({kind, a, b});
+  } else {
+    fn();
+    LF_CUDA(cudaGetLastError());
+  }
+  ++launches;
+  ++kLaunches[kind];
+}
+
+cudaEvent_t lf_context::event() {
+  if (!evFree.empty()) {
+    cudaEvent_t e = evFree.back();
+    evFree.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  LF_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
+void lf_context::harvest() {
+  for (const Pending &p : pending) {
+    float ms = 0.f;
+    LF_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
+    kMs[p.kind] += ms;
+    evFree.push_back(p.a);
+    evFree.push_back(p.b);
+  }
+  pending.clear();
+}
+
+lf_context::~lf_context() {
+  if (stream) cudaStreamSynchronize(stream);
+  for (auto &p : pending) {
+    cudaEventDestroy(p.a);
+    cudaEventDestroy(p.b);
+  }
+  for (auto e : evFree) cudaEventDestroy(e);
+  if (comm) nccl_comm_destroy(comm);
+  if (ownStream && stream) cudaStreamDestroy(stream);
+}
+
+extern "C" {
+
+const char *lf_status_string(lf_status s) {
+  switch (s) {
+    case LF_OK: return "LF_OK";
+    case LF_ERR_INVALID_ARG: return "LF_ERR_INVALID_ARG";
+    case LF_ERR_STATE: return "LF_ERR_STATE";
+    case LF_ERR_OOM: return "LF_ERR_OOM";
+    case LF_ERR_CUDA: return "LF_ERR_CUDA";
+    case LF_ERR_NCCL: return "LF_ERR_NCCL";
+    case LF_ERR_INTERNAL: return "LF_ERR_INTERNAL";
+  }
+  return "LF_ERR_UNKNOWN";
+}
+
+const char *lf_last_error(void) { return g_last_error.c_str(); }
+
+int lf_version(void) { return LF_VERSION; }
+
+lf_status lf_context_create(int device, void *cuda_stream, lf_context **out) {
+  return guard([&] {
+    LF_REQUIRE(out != nullptr, "out is NULL");
+    int ndev = 0;
+    LF_CUDA(cudaGetDeviceCount(&ndev));
+    LF_REQUIRE(device >= 0 && device < ndev, "device ordinal out of range");
+    LF_CUDA(cudaSetDevice(device));
+    std::unique_ptr<lf_context> c(new lf_context());
+    c->device = device;
+    LF_CUDA(cudaDeviceGetAttribute(&c->smCount, cudaDevAttrMultiProcessorCount, device));
+    if (cuda_stream) {
+      c->stream = static_cast<cudaStream_t>(cuda_stream);
+    } else {
+      LF_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      c->ownStream = true;
+    }
+    *out = c.release();
+  });
+}
+
+lf_status lf_context_destroy(lf_context *ctx) {
+  return guard([&] { delete ctx; });
+}
+
+lf_status lf_comm_unique_id(void *out) {
+  return guard([&] {
+    LF_REQUIRE(out != nullptr, "out is NULL");
+    nccl_unique_id(out);
+  });
+}
+
+lf_status lf_comm_init(lf_context *ctx, const void *uid, int nranks, int rank) {
+  return guard([&] {
+    LF_REQUIRE(ctx && uid, "NULL argument");
+    LF_REQUIRE(nranks >= 1 && rank >= 0 && rank < nranks, "bad nranks/rank");
+    LF_REQUIRE(ctx->comm == nullptr, "communicator already initialised");
+    ctx->comm = nccl_comm_init(uid, nranks, rank, ctx->device);
+    ctx->nranks = nranks;
+    ctx->rank = rank;
+  });
+}
+
+lf_status lf_comm_info(const lf_context *ctx, int *nranks, int *rank) {
+  return guard([&] {
+    LF_REQUIRE(ctx != nullptr, "ctx is NULL");
+    if (nranks) *nranks = ctx->nranks;
+    if (rank) *rank = ctx->rank;
+  });
+}
+
+// ---------------------------------------------------------------- mesh
+lf_status mesh_create(lf_context *ctx, const lf_mesh_desc *desc, lf_mesh **out) {
+  return guard([&] { mesh_create_impl(ctx, desc, out); });
+}
+
+lf_status mesh_destroy(lf_mesh *mesh) {
+  return guard([&] {
+    if (mesh) cudaStreamSynchronize(mesh->ctx->stream);
+    delete mesh;
+  });
+}
+
+lf_status lf_mesh_info(const lf_mesh *M, int32_t *n, int32_t *F, int32_t *B, int64_t *bytes) {
+  return guard([&] {
+    LF_REQUIRE(M != nullptr, "mesh is NULL");
+    if (n) *n = M->n;
+    if (F) *F = M->F;
+    if (B) *B = M->B;
+    if (bytes) *bytes = M->arena.bytes;
+  });
+}
+
+lf_status lf_mesh_export_addressing(const lf_mesh *M, int32_t *owner_start, int32_t *losort,
+                                    int32_t *losort_start, int32_t *face_order, int32_t *cell_order) {
+  return guard([&] {
+    LF_REQUIRE(M != nullptr, "mesh is NULL");
+    cudaStream_t s = M->ctx->stream;
+    auto cp = [&](int32_t *dst, const int32_t *src, size_t cnt) {
+      if (dst && cnt) LF_CUDA(cudaMemcpyAsync(dst, src, sizeof(int32_t) * cnt, cudaMemcpyDeviceToHost, s));
+    };
+    cp(owner_start, M->md.ownerStart, M->n + 1);
+    cp(losort, M->md.losort, M->F);
+    cp(losort_start, M->md.losortStart, M->n + 1);
+    cp(face_order, M->facePerm, M->F);
+    if (cell_order) {
+      if (M->renumbered)
+        cp(cell_order, M->cellPerm, M->n);
+      else
+        for (int32_t i = 0; i < M->n; ++i) cell_order[i] = i;
+    }
+    LF_CUDA(cudaStreamSynchronize(s));
+  }, const_cast<lf_mesh *>(M));
+}
+
+lf_status lf_permute(const lf_mesh *M, int to_internal, const double *in, double *out) {
+  return guard([&] {
+    LF_REQUIRE(M && in && out, "NULL argument");
+    LF_REQUIRE(in != out, "in and out must not alias");
+    cudaStream_t s = M->ctx->stream;
+    if (!M->renumbered) {
+      LF_CUDA(cudaMemcpyAsync(out, in, sizeof(double) * M->n, cudaMemcpyDeviceToDevice, s));
+    } else {
+      // internal[i] = caller[cellPerm[i]]  /  caller[cellPerm[i]] = internal[i]
+      launch_permute(s, M->n, M->cellPerm, in, out, !to_internal);
+      LF_CUDA(cudaGetLastError());
+    }
+  }, const_cast<lf_mesh *>(M));
+}
+
+// --------------------------------------------------------------- fields
+lf_status field_set(lf_mesh *M, lf_field f, int32_t patch, const double *v, int64_t n, int on_device) {
+  return guard([&] {
+    LF_REQUIRE(M && v, "NULL argument");
+    cudaStream_t s = M->ctx->stream;
+    const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    if (f == LF_FIELD_T) {
+      LF_REQUIRE(patch == -1, "patch must be -1 for LF_FIELD_T");
+      LF_REQUIRE(n == M->n, "n must equal n_cells");
+      if (!M->renumbered) {
+        LF_CUDA(cudaMemcpyAsync(M->T, v, sizeof(double) * n, kind, s));
+      } else {
+        LF_CUDA(cudaMemcpyAsync(M->scratch, v, sizeof(double) * n, kind, s));
+        launch_permute(s, M->n, M->cellPerm, M->scratch, M->T, false);
+      }
+      M->sumPsiValid = false;
+    } else if (f == LF_FIELD_PATCH_VALUE) {
+      LF_REQUIRE(patch >= 0 && patch < M->nPatches, "patch out of range");
+      const int32_t off = M->patchStart[patch], cnt = M->patchStart[patch + 1] - off;
+      LF_REQUIRE(n == cnt, "n must equal the patch's n_faces");
+      if (M->patchType[patch] == LF_PATCH_FIXED_VALUE)
+        LF_CUDA(cudaMemcpyAsync(M->bValue + off, v, sizeof(double) * n, kind, s));
+    } else {
+      throw Error{LF_ERR_INVALID_ARG, "unknown field"};
+    }
+    if (!on_device) LF_CUDA(cudaStreamSynchronize(s));
+    LF_CUDA(cudaGetLastError());
+  }, M);
+}
+
+lf_status field_get(const lf_mesh *Mc, lf_field f, int32_t patch, double *v, int64_t n, int on_device) {
+  lf_mesh *M = const_cast<lf_mesh *>(Mc);
+  return guard([&] {
+    LF_REQUIRE(M && v, "NULL argument");
+    cudaStream_t s = M->ctx->stream;
+    const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    if (f == LF_FIELD_T) {
+      LF_REQUIRE(patch == -1, "patch must be -1 for LF_FIELD_T");
+      LF_REQUIRE(n == M->n, "n must equal n_cells");
+      if (!M->renumbered) {
+        LF_CUDA(cudaMemcpyAsync(v, M->T, sizeof(double) * n, kind, s));
+      } else {
+        launch_permute(s, M->n, M->cellPerm, M->T, M->scratch, true);
+        LF_CUDA(cudaMemcpyAsync(v, M->scratch, sizeof(double) * n, kind, s));
+      }
+    } else if (f == LF_FIELD_PATCH_VALUE) {
+      LF_REQUIRE(patch >= 0 && patch < M->nPatches, "patch out of range");
+      const int32_t off = M->patchStart[patch], cnt = M->patchStart[patch + 1] - off;
+      LF_REQUIRE(n == cnt, "n must equal the patch's n_faces");
+      const int t = M->patchType[patch];
+      if (cnt > 0) {
+        if (t == LF_PATCH_FIXED_VALUE) {
+          LF_CUDA(cudaMemcpyAsync(v, M->bValue + off, sizeof(double) * n, kind, s));
+        } else if (t == LF_PATCH_ZERO_GRADIENT) {  // correctBoundaryConditions: T_b = T[faceCells]
+          launch_gather_f64(s, cnt, M->bCell + off, M->T, M->scratch);
+          LF_CUDA(cudaMemcpyAsync(v, M->scratch, sizeof(double) * n, kind, s));
+        } else {
+          LF_CUDA(cudaMemsetAsync(M->scratch, 0, sizeof(double) * n, s));
+          LF_CUDA(cudaMemcpyAsync(v, M->scratch, sizeof(double) * n, kind, s));
+        }
+      }
+    } else {
+      throw Error{LF_ERR_INVALID_ARG, "unknown field"};
+    }
+    if (!on_device) LF_CUDA(cudaStreamSynchronize(s));
+    LF_CUDA(cudaGetLastError());
+  }, M);
+}
+
+// -------------------------------------------------------------- assembly
+lf_status laplacian_assemble(lf_mesh *M, const lf_laplacian_params *p, lf_ldu **sys) {
+  return guard([&] {
+    LF_REQUIRE(M && p, "NULL argument");
+    LF_REQUIRE(p->DT > 0.0 && p->dt > 0.0, "DT and dt must be > 0");
+    lf_context *ctx = M->ctx;
+    cudaStream_t s = ctx->stream;
+    if (M->nproc > 0) {
+      ctx->launch(LF_K_PACK, [&] { launch_pack_x(s, M->nproc, M->ws.sendCell, M->T, M->ws.sendBuf); });
+      halo_exchange(M, M->ws.sendBuf, M->ws.recvBuf);
+    }
+    ctx->launch(LF_K_ASSEMBLE, [&] {
+      launch_assemble(s, M->Lasm, M->md, M->ld, p->DT, 1.0 / p->dt, M->T, M->ws.recvBuf, false, M->ws);
+    });
+    M->ldu.assembled = true;
+    if (sys) *sys = &M->ldu;
+  }, M);
+}
+
+lf_status lf_ldu_export(const lf_ldu *sys, double *diag, double *upper, double *source,
+                        double *internal_coeffs, double *boundary_coeffs) {
+  lf_mesh *M = sys ? sys->mesh : nullptr;
+  return guard([&] {
+    LF_REQUIRE(sys && M, "NULL ldu");
+    LF_REQUIRE(sys->assembled, "ldu not assembled");
+    cudaStream_t s = M->ctx->stream;
+    auto cell = [&](double *dst, const double *src) {
+      if (!dst) return;
+      if (M->renumbered) {
+        launch_permute(s, M->n, M->cellPerm, src, M->scratch, true);
+        src = M->scratch;
+      }
+      LF_CUDA(cudaMemcpyAsync(dst, src, sizeof(double) * M->n, cudaMemcpyDeviceToHost, s));
+      LF_CUDA(cudaStreamSynchronize(s));
+    };
+    cell(diag, M->ld.diag);
+    cell(source, M->ld.source);
+    if (upper && M->F > 0) {
+      std::vector<double> tmp(M->F);
+      std::vector<int32_t> perm(M->F);
+      LF_CUDA(cudaMemcpyAsync(tmp.data(), M->ld.upper, sizeof(double) * M->F, cudaMemcpyDeviceToHost, s));
+      LF_CUDA(cudaMemcpyAsync(perm.data(), M->facePerm, sizeof(int32_t) * M->F, cudaMemcpyDeviceToHost, s));
+      LF_CUDA(cudaStreamSynchronize(s));
+      for (int32_t i = 0; i < M->F; ++i) upper[perm[i]] = tmp[i];
+    }
+    if (internal_coeffs && M->B)
+      LF_CUDA(cudaMemcpyAsync(internal_coeffs, M->ld.bInt, sizeof(double) * M->B, cudaMemcpyDeviceToHost, s));
+    if (boundary_coeffs && M->B)
+      LF_CUDA(cudaMemcpyAsync(boundary_coeffs, M->ld.bBnd, sizeof(double) * M->B, cudaMemcpyDeviceToHost, s));
+    LF_CUDA(cudaStreamSynchronize(s));
+  }, M);
+}
+
+lf_status ldu_amul(const lf_ldu *sys, const double *x, double *y) {
+  lf_mesh *M = sys ? sys->mesh : nullptr;
+  return guard([&] {
+    LF_REQUIRE(sys && M && x && y, "NULL argument");
+    LF_REQUIRE(x != y, "x and y must not alias");
+    LF_REQUIRE(sys->assembled, "ldu not assembled");
+    lf_context *ctx = M->ctx;
+    cudaStream_t s = ctx->stream;
+    if (M->nproc > 0) {
+      ctx->launch(LF_K_PACK, [&] { launch_pack_x(s, M->nproc, M->ws.sendCell, x, M->ws.sendBuf); });
+      halo_exchange(M, M->ws.sendBuf, M->ws.recvBuf);
+    }
+    ctx->launch(LF_K_AMUL, [&] { launch_amul(s, M->Lamul, M->md, M->ld, M->ws.recvBuf, x, y); });
+  }, M);
+}
+
+// ------------------------------------------------------------------- PCG
+lf_status pcg_solve(lf_ldu *sys, double *psi, const lf_solver_controls *c, lf_solver_perf *out) {
+  lf_mesh *M = sys ? sys->mesh : nullptr;
+  return guard([&] {
+    LF_REQUIRE(sys && M && psi && c, "NULL argument");
+    LF_REQUIRE(sys->assembled, "ldu not assembled");
+    upload_controls(M, c, psi);
+    solve_loop(M, c, psi, false, nullptr, out);
+  }, M);
+}
+
+lf_status laplacianFoam_step(lf_mesh *M, const lf_laplacian_params *p, const lf_solver_controls *c,
+                             int32_t n_steps, lf_solver_perf *per_step) {
+  return guard([&] {
+    LF_REQUIRE(M && p && c, "NULL argument");
+    LF_REQUIRE(p->DT > 0.0 && p->dt > 0.0, "DT and dt must be > 0");
+    LF_REQUIRE(n_steps >= 0, "n_steps must be >= 0");
+    if (n_steps == 0) return;
+    upload_controls(M, c, M->T);
+    for (int32_t st = 0; st < n_steps; ++st) {
+      solve_loop(M, c, M->T, true, p, per_step ? per_step + st : nullptr);
+      M->ldu.assembled = true;
+    }
+  }, M);
+}
+
+// -------------------------------------------------------- instrumentation
+lf_status lf_set_instrumentation(lf_context *ctx, int enable) {
+  return guard([&] {
+    LF_REQUIRE(ctx != nullptr, "ctx is NULL");
+    LF_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->harvest();
+    ctx->instrument = enable != 0;
+    ctx->kLaunches.fill(0);
+    ctx->kMs.fill(0.0);
+    ctx->launches = 0;
+  });
+}
+
+lf_status lf_kernel_stats(const lf_context *ctx, lf_kernel_kind k, int64_t *launches, double *ms) {
+  return guard([&] {
+    LF_REQUIRE(ctx != nullptr, "ctx is NULL");
+    LF_REQUIRE(k >= 0 && k < LF_K_COUNT, "bad kernel kind");
+    LF_CUDA(cudaStreamSynchronize(ctx->stream));
+    const_cast<lf_context *>(ctx)->harvest();
+    if (launches) *launches = ctx->kLaunches[k];
+    if (ms) *ms = ctx->kMs[k];
+  });
+}
+
+lf_status lf_launch_count(const lf_context *ctx, int64_t *n) {
+  return guard([&] {
+    LF_REQUIRE(ctx && n, "NULL argument");
+    *n = ctx->launches;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,107 @@
+// Host-side objects behind the opaque ABI handles.
+#pragma once
+#include <array>
+#include <functional>
+#include <string>
+#include <vector>
+
+#include "lfoam_internal.h"
+
+namespace lf {
+
+// ------------------------------------------------------------------ comm
+// NCCL, loaded with dlopen at lf_comm_init (no link-time dependency).
+struct Nccl;
+Nccl *nccl_load();  // throws Error{LF_ERR_NCCL} if unavailable
+void nccl_unique_id(void *out128);
+void *nccl_comm_init(const void *uid128, int nranks, int rank, int device);
+void nccl_comm_destroy(void *comm);
+void nccl_allreduce_sum(void *comm, const double *send, double *recv, size_t count, cudaStream_t s);
+void nccl_group_start();
+void nccl_group_end();
+void nccl_send(void *comm, const double *buf, size_t count, int peer, cudaStream_t s);
+void nccl_recv(void *comm, double *buf, size_t count, int peer, cudaStream_t s);
+void nccl_check_async(void *comm);
+
+}  // namespace lf
+
+struct lf_context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool ownStream = false;
+  int nranks = 1, rank = 0;
+  void *comm = nullptr;  // ncclComm_t
+  int smCount = 0;
+  // instrumentation
+  bool instrument = false;
+  bool capturing = false;  // stream capture in progress: no events, no counting
+  bool useGraphs = true;   // replay iteration chunks as CUDA graphs
+  struct Pending {
+    int kind;
+    cudaEvent_t a, b;
+  };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> evFree;
+  std::array<int64_t, LF_K_COUNT> kLaunches{};
+  std::array<double, LF_K_COUNT> kMs{};
+  int64_t launches = 0;
+
+  // Launch wrapper: counts the launch and, if instrumented, brackets it
+  // with CUDA events on the context stream.
+  void launch(int kind, const std::function<void()> &fn);
+  void harvest();  // after a stream sync: accumulate event timings
+  cudaEvent_t event();
+  ~lf_context();
+};
+
+struct HaloSeg {
+  int32_t offset, count, peer;  // slots [offset, offset+count) of send/recv buffers
+  int32_t partner;              // self pairs: index of the partner segment, else -1
+};
+
+struct lf_ldu {
+  lf_mesh *mesh = nullptr;
+  bool assembled = false;
+};
+
+struct lf_mesh {
+  lf_context *ctx = nullptr;
+  int32_t n = 0, F = 0, B = 0, nproc = 0;
+  int32_t nPatches = 0;
+  lf::DevArena arena;
+  lf::MeshDev md{};
+  lf::LduDev ld{};
+  lf::Workspace ws{};
+  lf::Launch Lasm{}, Lp1{}, Lp2{}, Lamul{}, Lsetup{}, Lsum{};
+  std::vector<int32_t> patchType, patchStart, patchRank;
+  std::vector<HaloSeg> segs;
+  bool renumbered = false;
+  int32_t *facePerm = nullptr;   // internal face -> caller face
+  int32_t *cellPerm = nullptr;   // internal cell -> caller cell (renumbered only)
+  int32_t *cellIperm = nullptr;  // caller cell -> internal cell (renumbered only)
+  int32_t *ownerInt = nullptr;   // internal owner per internal face (export)
+  int32_t *bCell = nullptr;      // per flat boundary face (internal numbering)
+  double *bValue = nullptr;
+  double *T = nullptr;
+  double *scratch = nullptr;     // n doubles (permutation staging)
+  lf::PcgCtl *hctl = nullptr;    // pinned host mirror
+  double nTotal = 0.0;
+  bool sumPsiValid = false;
+  int32_t lastIters = -1;
+  bool broken = false;
+  lf_ldu ldu;
+  // CUDA graphs of 2^i PCG iterations (captured once per mesh, replayed)
+  static constexpr int kMaxGraphLog = 8;
+  cudaGraphExec_t chunkGraph[kMaxGraphLog] = {};
+  int kernelsPerIteration = 0;
+  ~lf_mesh();
+};
+
+namespace lf {
+// solver.cpp
+void solve_loop(lf_mesh *M, const lf_solver_controls *c, double *psi, bool fromAssembly,
+                const lf_laplacian_params *p, lf_solver_perf *out);
+void halo_exchange(lf_mesh *M, const double *send, double *recv);
+void allreduce(lf_mesh *M, const double *local, double *global, size_t count);
+void upload_controls(lf_mesh *M, const lf_solver_controls *c, double *psi);
+}  // namespace lf

@@ -1,0 +1,745 @@
+// Hot-path CUDA kernels for sm_100a (B200).
+//
+// All kernels are memory-bound FP64 work (Amul ~0.18 flop/B
+// against a ~5 flop/B FP64 ridge) — no tensor cores.  One thread per cell,
+// grid-stride over a RESIDENT grid (numSMs x blocks/SM), so every SM sweeps
+// the cell range in lock-step and the neighbour-side re-reads (N^2 cells
+// behind on a cube) hit in the 126 MB L2.
+//
+// Two row layouts for the off-diagonal gather:
+//  * CSR (the paper's atomic-free lists, §5.2): ownerStart/nbr for
+//    the owner side, losortStart/losort/losortOwner for the neighbour side.
+//    Used by the assembly and as the general fallback.
+//  * ELL slices derived from the CSR lists at mesh_create (DESIGN.md "Data
+//    layout"): slot k of cell c at k*n + c (coalesced, no start offsets):
+//      upperE[k*n+c]  coefficient of c's k-th owned face (0 if none)
+//      nbrE[k*n+c]    its neighbour cell (-1 if none)
+//      loE[k*n+c]     c's k-th neighbour-side face (losort order) as the
+//                     packed owner-slot (kk<<29 | owner): its coefficient is
+//                     upperE[kk*n + owner] (an L2 re-read), -1 if none.
+//    This reads exactly the algorithmic 16 B/face (coefficient + 2 labels)
+//    instead of the CSR's 28 B/face + 8 B/cell, with dependency depth 2
+//    (index -> value) instead of 3 (start -> index -> value).
+//
+// Determinism: no float atomics anywhere.  Reductions are fixed-order
+// (grid-stride partial per thread -> xor-shuffle tree -> per-block partial
+// -> the last block, chosen by an integer ticket, sums the block partials in
+// block order).  Same grid => bitwise-identical results run to run.
+#include <cub/device/device_radix_sort.cuh>
+
+#include "lfoam_internal.h"
+
+namespace lf {
+
+// ---- tuning knobs (defaults = the shipped configuration; variants are built
+// with -D for measurements, see scripts/variants.py and profiles/)
+#ifndef LF_BS
+#define LF_BS 256        // threads per block
+#endif
+#ifndef LF_MINB
+#define LF_MINB 4        // __launch_bounds__ min blocks/SM (register cap 65536/(BS*MINB))
+#endif
+#ifndef LF_P2_UNROLL
+#define LF_P2_UNROLL 4   // cells per thread per grid-stride trip in phase 2
+#endif
+#ifndef LF_NO_ELL
+#define LF_NO_ELL 0      // 1: force the CSR gather (ablation)
+#endif
+
+constexpr int BS = LF_BS;
+constexpr unsigned FULL = 0xffffffffu;
+enum { T_SUM = 0, T_ASM = 1, T_SETUP = 2, T_P1 = 3, T_P2 = 4 };
+constexpr int ELL_SHIFT = 29;  // slot kk <= 3 in bits 29-30: the packed label stays >= 0
+constexpr int ELL_MASK = (1 << ELL_SHIFT) - 1;
+
+int kernel_block_size() { return BS; }
+
+// ------------------------------------------------------------ reductions
+template <int NV>
+__device__ __forceinline__ void warp_sum(double (&v)[NV]) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] += __shfl_xor_sync(FULL, v[k], o);
+}
+
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&v)[NV], double (*sm)[32]) {
+  warp_sum<NV>(v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < NV; ++k) sm[k][wid] = v[k];
+  __syncthreads();
+  if (wid == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] = lane < nw ? sm[k][lane] : 0.0;
+    warp_sum<NV>(v);
+  }
+}
+
+// Block partial -> partials[k*grid + block]; the last block (ticket) sums
+// the partials in block order and writes out[0..NV).  Returns true in every
+// thread of the last block; its thread 0 then holds the totals in v.
+template <int NV>
+__device__ bool reduce_grid(double (&v)[NV], double *partials, unsigned *ticket, double *out) {
+  __shared__ double sm[NV][32];
+  __shared__ int amLast;
+  block_sum<NV>(v, sm);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) partials[k * gridDim.x + blockIdx.x] = v[k];
+    __threadfence();
+    const unsigned t = atomicAdd(ticket, 1u);
+    amLast = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!amLast) return false;
+  __threadfence();
+  double s[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) s[k] = 0.0;
+  // all partial loads of a trip in flight at once (one L2 round trip for
+  // grids up to 4*blockDim); summation order per thread: b, b+BS, b+2BS, ...
+  constexpr int U = 4;
+  for (int b0 = threadIdx.x; b0 < (int)gridDim.x; b0 += blockDim.x * U) {
+    double t[U][NV];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int b = b0 + u * blockDim.x;
+#pragma unroll
+      for (int k = 0; k < NV; ++k) t[u][k] = b < (int)gridDim.x ? __ldcg(&partials[k * gridDim.x + b]) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int k = 0; k < NV; ++k) s[k] += t[u][k];
+  }
+  block_sum<NV>(s, sm);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      out[k] = s[k];
+      v[k] = s[k];
+    }
+    *ticket = 0u;
+  }
+  return true;
+}
+
+// ------------------------------------------------------------ row gathers
+// Off-diagonal part of row c: the neighbour side (faces whose neighbour is
+// c, in losort order) then the owner side (faces owned by c) — for
+// upper-triangular face order exactly the face-loop order of
+// lduMatrix::Amul.  Returns acc + sum upper_f x_other(f);
+// sU (optional) receives sum upper_f (row sum for sumA).
+template <int KE, class XF>
+__device__ __forceinline__ double row_offdiag(const MeshDev &m, const LduDev &a, int c, double acc,
+                                              XF xval, double *sU = nullptr) {
+  if constexpr (KE > 0) {
+    const int n = m.n;
+    int lo[KE], nb[KE];
+    double uo[KE];
+#pragma unroll
+    for (int k = 0; k < KE; ++k) {
+      lo[k] = __ldg(m.loE + k * n + c);
+      nb[k] = __ldg(m.nbrE + k * n + c);
+      uo[k] = a.upperE[k * n + c];
+    }
+    double lu[KE], lx[KE], ox[KE];
+#pragma unroll
+    for (int k = 0; k < KE; ++k) {
+      const int oc = lo[k] & ELL_MASK;
+      lu[k] = lo[k] >= 0 ? a.upperE[(lo[k] >> ELL_SHIFT) * n + oc] : 0.0;
+      lx[k] = lo[k] >= 0 ? xval(oc) : 0.0;
+      ox[k] = nb[k] >= 0 ? xval(nb[k]) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < KE; ++k)
+      if (lo[k] >= 0) acc = fma(lu[k], lx[k], acc);
+#pragma unroll
+    for (int k = 0; k < KE; ++k)
+      if (nb[k] >= 0) acc = fma(uo[k], ox[k], acc);
+    if (sU) {
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < KE; ++k) s += lu[k];
+#pragma unroll
+      for (int k = 0; k < KE; ++k) s += uo[k];
+      *sU = s;
+    }
+    return acc;
+  } else {
+    const int l0 = m.losortStart[c], l1 = m.losortStart[c + 1];
+    const int o0 = m.ownerStart[c], o1 = m.ownerStart[c + 1];
+    double s = 0.0;
+    for (int j = l0; j < l1; ++j) {
+      const double u = a.upper[m.losort[j]];
+      acc = fma(u, xval(m.losortOwner[j]), acc);
+      s += u;
+    }
+    for (int i = o0; i < o1; ++i) {
+      const double u = a.upper[i];
+      acc = fma(u, xval(m.nbr[i]), acc);
+      s += u;
+    }
+    if (sU) *sU = s;
+    return acc;
+  }
+}
+
+// Processor-interface term  sum_i bc_i * x_remote_i  (subtracted by callers);
+// sBc (optional) receives sum_i bc_i.
+__device__ __forceinline__ double row_proc(const MeshDev &m, const double *__restrict__ bBnd,
+                                           const double *__restrict__ halo, int c,
+                                           double *sBc = nullptr) {
+  double s = 0.0, sb = 0.0;
+  if (m.hasProc) {
+    const int k0 = m.pcStart[c], k1 = m.pcStart[c + 1];
+    for (int k = k0; k < k1; ++k) {
+      const int i = m.pcFace[k];
+      s = fma(bBnd[i], halo[m.bSlot[i]], s);
+      sb += bBnd[i];
+    }
+  }
+  if (sBc) *sBc = sb;
+  return s;
+}
+
+__device__ __forceinline__ bool conv(double res, double init, const PcgCtl *ctl) {
+  return res < ctl->tol || (ctl->relTol > 0.0 && res < ctl->relTol * init);
+}
+
+// Dispatch a KE-templated kernel on the mesh's ELL width.
+#define LF_DISPATCH_KE(m, KERNEL, ...)                                     \
+  do {                                                                     \
+    if (!LF_NO_ELL && (m).K > 0 && (m).K <= 3) KERNEL<3> __VA_ARGS__;       \
+    else if (!LF_NO_ELL && (m).K == 4) KERNEL<4> __VA_ARGS__;               \
+    else KERNEL<0> __VA_ARGS__;                                            \
+  } while (0)
+
+// ------------------------------------------------------------------ sum
+__global__ void __launch_bounds__(BS, LF_MINB)
+    k_sum(const double *__restrict__ x, int32_t n, double *partials, unsigned *ticket, double *out) {
+  double v[1] = {0.0};
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) v[0] += x[c];
+  reduce_grid<1>(v, partials, ticket, out);
+}
+
+void launch_sum(cudaStream_t s, const Launch &L, const double *x, int32_t n, const Workspace &ws,
+                double *out) {
+  k_sum<<<L.grid, BS, 0, s>>>(x, n, ws.partials, ws.tickets + T_SUM, out);
+}
+
+// -------------------------------------------------------------- assembly
+// fvm::ddt(T) - fvm::laplacian(DT,T) (SURVEY §8(c.1) lines 1-4, readings
+// A3-A5) as a per-cell gather over the CSR lists.  Every coefficient is
+// formed with the same rounded operations, in the same order, as the face
+// loop of the definition (explicit _rn intrinsics: no FMA contraction), so
+// diag/upper/source are bitwise those of the definition on upper-triangular
+// meshes.  The owner side also writes the ELL copy upperE.
+// SETUP additionally fuses the PCG prologue for psi = T0 = T: A psi (from
+// the just-formed coefficients), r = b - A psi, normFactor terms with
+// psibar = gSum(psi)/nTotal, sum|r|, w = r/diag and sum w.r.
+template <bool SETUP>
+__global__ void __launch_bounds__(BS, LF_MINB)
+    k_assemble(MeshDev m, LduDev a, double DT, double rDeltaT, const double *__restrict__ T,
+               const double *__restrict__ halo, Workspace ws) {
+  double psibar = 0.0;
+  if (SETUP) psibar = ws.gsum->p1[1] / ws.ctl->nTotal;
+  double v[3] = {0.0, 0.0, 0.0};
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < m.n; c += gridDim.x * blockDim.x) {
+    double L = 0.0, sOff = 0.0, sU = 0.0;
+    const int l0 = m.losortStart[c], l1 = m.losortStart[c + 1];
+    for (int j = l0; j < l1; ++j) {
+      const int f = m.losort[j];
+      const double u = __dmul_rn(m.delta[f], __dmul_rn(DT, m.magSf[f]));
+      L = __dsub_rn(L, u);
+      if (SETUP) {
+        sOff = fma(-u, T[m.losortOwner[j]], sOff);
+        sU -= u;
+      }
+    }
+    const int o0 = m.ownerStart[c], o1 = m.ownerStart[c + 1];
+    for (int i = o0; i < o1; ++i) {
+      const double u = __dmul_rn(m.delta[i], __dmul_rn(DT, m.magSf[i]));
+      a.upper[i] = -u;
+      if (m.K > 0) a.upperE[(i - o0) * m.n + c] = -u;
+      L = __dsub_rn(L, u);
+      if (SETUP) {
+        sOff = fma(-u, T[m.nbr[i]], sOff);
+        sU -= u;
+      }
+    }
+    const double Tc = T[c];
+    double d = __dsub_rn(__dmul_rn(rDeltaT, m.V[c]), L);
+    double b = __dmul_rn(__dmul_rn(rDeltaT, Tc), m.V[c]);
+    double sP = 0.0, sBc = 0.0;
+    const int b0 = m.bcStart[c], b1 = m.bcStart[c + 1];
+    for (int k = b0; k < b1; ++k) {
+      const int i = m.bcFace[k];
+      const double gms = __dmul_rn(DT, m.bMagSf[i]);
+      const double aa = __dmul_rn(gms, m.bDelta[i]);
+      d = __dadd_rn(d, aa);
+      a.bInt[i] = aa;
+      if (m.bType[i] == LF_PATCH_FIXED_VALUE) {
+        const double bb = __dmul_rn(gms, __dmul_rn(m.bDelta[i], m.bValue[i]));
+        b = __dadd_rn(b, bb);
+        a.bBnd[i] = bb;
+      } else {  // processor: interfaceBouCoeffs = a, coupled via Amul
+        a.bBnd[i] = aa;
+        if (SETUP) {
+          sP = fma(aa, halo[m.bSlot[i]], sP);
+          sBc += aa;
+        }
+      }
+    }
+    a.diag[c] = d;
+    a.source[c] = b;
+    if (SETUP) {
+      const double Ap = fma(d, Tc, sOff) - sP;
+      const double sumA = d + sU - sBc;
+      const double r = b - Ap;
+      const double tmp = sumA * psibar;
+      v[0] += fabs(Ap - tmp) + fabs(b - tmp);
+      v[1] += fabs(r);
+      const double w = (1.0 / d) * r;
+      v[2] = fma(w, r, v[2]);
+      ws.r[c] = r;
+      ws.w[c] = w;
+    }
+  }
+  if (SETUP) {
+    if (reduce_grid<3>(v, ws.partials, ws.tickets + T_ASM, ws.lsum->setup) && threadIdx.x == 0) {
+      PcgCtl *ctl = ws.ctl;
+      ctl->it = 0;
+      ctl->stop = 0;
+      ctl->converged = 0;
+      ctl->singular = 0;
+    }
+  }
+}
+
+void launch_assemble(cudaStream_t s, const Launch &L, const MeshDev &m, const LduDev &a, double DT,
+                     double rDeltaT, const double *T, const double *halo, bool setup,
+                     const Workspace &ws) {
+  if (setup)
+    k_assemble<true><<<L.grid, BS, 0, s>>>(m, a, DT, rDeltaT, T, halo, ws);
+  else
+    k_assemble<false><<<L.grid, BS, 0, s>>>(m, a, DT, rDeltaT, T, halo, ws);
+}
+
+// ------------------------------------------------------------- PCG setup
+// Prologue of a standalone pcg_solve: A psi from the stored coefficients,
+// r = source - A psi, normFactor terms, sum|r|, w = r/diag, sum w.r.
+template <int KE>
+__global__ void __launch_bounds__(BS, LF_MINB)
+    k_pcg_setup(MeshDev m, LduDev a, const double *__restrict__ halo, Workspace ws) {
+  const double *psi = ws.ctl->psi;
+  const double psibar = ws.gsum->p1[1] / ws.ctl->nTotal;
+  double v[3] = {0.0, 0.0, 0.0};
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < m.n; c += gridDim.x * blockDim.x) {
+    const double d = a.diag[c];
+    double sU = 0.0, sBc = 0.0;
+    const double sOff = row_offdiag<KE>(m, a, c, 0.0, [&](int j) { return psi[j]; }, &sU);
+    const double Ap = fma(d, psi[c], sOff) - row_proc(m, a.bBnd, halo, c, &sBc);
+    const double b = a.source[c];
+    const double sumA = d + sU - sBc;
+    const double r = b - Ap;
+    const double tmp = sumA * psibar;
+    v[0] += fabs(Ap - tmp) + fabs(b - tmp);
+    v[1] += fabs(r);
+    const double w = (1.0 / d) * r;
+    v[2] = fma(w, r, v[2]);
+    ws.r[c] = r;
+    ws.w[c] = w;
+  }
+  if (reduce_grid<3>(v, ws.partials, ws.tickets + T_SETUP, ws.lsum->setup) && threadIdx.x == 0) {
+    PcgCtl *ctl = ws.ctl;
+    ctl->it = 0;
+    ctl->stop = 0;
+    ctl->converged = 0;
+    ctl->singular = 0;
+  }
+}
+
+void launch_pcg_setup(cudaStream_t s, const Launch &L, const MeshDev &m, const LduDev &a,
+                      const double *halo, const Workspace &ws) {
+  LF_DISPATCH_KE(m, k_pcg_setup, <<<L.grid, BS, 0, s>>>(m, a, halo, ws));
+}
+
+// ------------------------------------------------------ iteration state
+// Everything a launch of iteration k derives from the previous launch's
+// global sums (identical on every rank and every block).
+struct IterState {
+  int k;
+  bool cont;
+  double nf, initRes, finRes, wArA, beta;
+};
+
+__device__ __forceinline__ IterState derive_phase1(const Workspace &ws) {
+  const PcgCtl *ctl = ws.ctl;
+  IterState s;
+  s.k = ctl->it;
+  s.beta = 0.0;
+  if (s.k == 0) {
+    // OpenFOAM: normFactor = gSum(...) + small_; initRes = gSumMag(r)/normFactor;
+    // iterate if minIter > 0 || !checkConvergence
+    s.nf = ws.gsum->setup[0] + 1e-20;
+    s.initRes = ws.gsum->setup[1] / s.nf;
+    s.finRes = s.initRes;
+    s.cont = ctl->minIter > 0 || !conv(s.finRes, s.initRes, ctl);
+    s.wArA = ws.gsum->setup[2];
+  } else {
+    // while ((++it < maxIter && !converged) || it < minIter)
+    s.nf = ctl->normFactor;
+    s.initRes = ctl->initRes;
+    s.finRes = ws.gsum->p2[0] / s.nf;
+    s.cont = (s.k < ctl->maxIter && !conv(s.finRes, s.initRes, ctl)) || s.k < ctl->minIter;
+    s.wArA = ws.gsum->p2[1];
+    s.beta = s.wArA / ctl->wArA;
+  }
+  return s;
+}
+
+// p = w (first iteration) or w + beta*p_old — evaluated identically for a
+// cell's own value and for the same cell seen as a neighbour (recomputed
+// there instead of a third kernel / extra HBM pass), so A p uses exactly
+// the stored p.
+__device__ __forceinline__ double pval(const double *__restrict__ w, const double *__restrict__ pold,
+                                       double beta, bool first, int j) {
+  return first ? w[j] : fma(beta, pold[j], w[j]);
+}
+
+// ---------------------------------------------------------------- phase 1
+// Deferred psi += alpha_{k-1} p_{k-1}; stopping test on the previous
+// iteration's residual; p_k = w + beta p_{k-1}; q = A p_k; sum p.q, sum psi.
+template <int KE>
+__global__ void __launch_bounds__(BS, LF_MINB)
+    k_phase1(MeshDev m, LduDev a, const double *__restrict__ halo, Workspace ws) {
+  const PcgCtl *ctl = ws.ctl;
+  if (ctl->stop) return;
+  const IterState s = derive_phase1(ws);
+  const bool first = (s.k == 0);
+  const double alpha = ctl->alpha;
+  double *psi = ctl->psi;
+  const double *__restrict__ pold = (s.k & 1) ? ws.p[0] : ws.p[1];
+  double *__restrict__ pnew = (s.k & 1) ? ws.p[1] : ws.p[0];
+  const double *__restrict__ w = ws.w;
+  double v[2] = {0.0, 0.0};
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < m.n; c += gridDim.x * blockDim.x) {
+    double ps = psi[c];
+    if (!first) {
+      ps = fma(alpha, pold[c], ps);
+      psi[c] = ps;
+    }
+    v[1] += ps;
+    if (s.cont) {
+      const double pc = pval(w, pold, s.beta, first, c);
+      pnew[c] = pc;
+      double q = a.diag[c] * pc;
+      q = row_offdiag<KE>(m, a, c, q, [&](int j) { return pval(w, pold, s.beta, first, j); });
+      q -= row_proc(m, a.bBnd, halo, c);
+      ws.q[c] = q;
+      v[0] = fma(pc, q, v[0]);
+    }
+  }
+  if (reduce_grid<2>(v, ws.partials, ws.tickets + T_P1, ws.lsum->p1) && threadIdx.x == 0) {
+    PcgCtl *c = ws.ctl;
+    if (first) {
+      c->normFactor = s.nf;
+      c->initRes = s.initRes;
+    }
+    c->finRes = s.finRes;
+    c->wArA = s.wArA;
+    if (!s.cont) {
+      c->stop = 1;
+      c->converged = conv(s.finRes, s.initRes, c) ? 1 : 0;
+    }
+  }
+}
+
+void launch_phase1(cudaStream_t s, const Launch &L, const MeshDev &m, const LduDev &a,
+                   const double *halo, const Workspace &ws) {
+  LF_DISPATCH_KE(m, k_phase1, <<<L.grid, BS, 0, s>>>(m, a, halo, ws));
+}
+
+// ---------------------------------------------------------------- phase 2
+// checkSingularity(|wApA|/normFactor); alpha = wArA/wApA; r -= alpha q;
+// w = rD r (diagonal preconditioner, rD = 1/diag); sum|r|, sum w.r.
+__global__ void __launch_bounds__(BS, LF_MINB)
+    k_phase2(int32_t n, LduDev a, Workspace ws) {
+  const PcgCtl *ctl = ws.ctl;
+  if (ctl->stop) return;
+  const int k = ctl->it;
+  const double pq = ws.gsum->p1[0];
+  const bool singular = fabs(pq) / ctl->normFactor < 1e-300;
+  const double alpha = ctl->wArA / pq;
+  double v[2] = {0.0, 0.0};
+  if (!singular) {
+    // LF_P2_UNROLL cells per trip: all loads of the trip issued first
+    constexpr int U = LF_P2_UNROLL;
+    const int stride = gridDim.x * blockDim.x;
+    for (int c0 = blockIdx.x * blockDim.x + threadIdx.x; c0 < n; c0 += stride * U) {
+      double q[U], r[U], d[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int c = c0 + u * stride;
+        const bool ok = c < n;
+        q[u] = ok ? ws.q[c] : 0.0;
+        r[u] = ok ? ws.r[c] : 0.0;
+        d[u] = ok ? a.diag[c] : 1.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int c = c0 + u * stride;
+        if (c < n) {
+          const double rn = fma(-alpha, q[u], r[u]);
+          const double w = (1.0 / d[u]) * rn;
+          ws.r[c] = rn;
+          ws.w[c] = w;
+          v[0] += fabs(rn);
+          v[1] = fma(w, rn, v[1]);
+        }
+      }
+    }
+  }
+  if (reduce_grid<2>(v, ws.partials, ws.tickets + T_P2, ws.lsum->p2) && threadIdx.x == 0) {
+    PcgCtl *c = ws.ctl;
+    if (singular) {
+      c->stop = 1;
+      c->singular = 1;
+      c->converged = conv(c->finRes, c->initRes, c) ? 1 : 0;
+    } else {
+      c->alpha = alpha;
+      c->it = k + 1;
+    }
+  }
+}
+
+void launch_phase2(cudaStream_t s, const Launch &L, int32_t n, const LduDev &a, const Workspace &ws) {
+  k_phase2<<<L.grid, BS, 0, s>>>(n, a, ws);
+}
+
+// ------------------------------------------------------------------ Amul
+template <int KE>
+__global__ void __launch_bounds__(BS, LF_MINB)
+    k_amul(MeshDev m, LduDev a, const double *__restrict__ halo, const double *__restrict__ x,
+           double *__restrict__ y) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < m.n; c += gridDim.x * blockDim.x) {
+    double acc = a.diag[c] * x[c];
+    acc = row_offdiag<KE>(m, a, c, acc, [&](int j) { return x[j]; });
+    y[c] = acc - row_proc(m, a.bBnd, halo, c);
+  }
+}
+
+void launch_amul(cudaStream_t s, const Launch &L, const MeshDev &m, const LduDev &a,
+                 const double *halo, const double *x, double *y) {
+  LF_DISPATCH_KE(m, k_amul, <<<L.grid, BS, 0, s>>>(m, a, halo, x, y));
+}
+
+// ------------------------------------------------------------ halo packs
+__global__ void k_pack_x(int32_t ns, const int32_t *__restrict__ cells, const double *__restrict__ x,
+                         double *__restrict__ buf) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ns; i += gridDim.x * blockDim.x)
+    buf[i] = x[cells[i]];
+}
+
+void launch_pack_x(cudaStream_t s, int32_t ns, const int32_t *cells, const double *x, double *buf) {
+  if (ns <= 0) return;
+  k_pack_x<<<(ns + BS - 1) / BS, BS, 0, s>>>(ns, cells, x, buf);
+}
+
+// p_k at the send cells, evaluated exactly as k_phase1 will (same derive).
+__global__ void k_pack_p(int32_t ns, const int32_t *__restrict__ cells, Workspace ws) {
+  if (ws.ctl->stop) return;
+  const IterState s = derive_phase1(ws);
+  if (!s.cont) return;
+  const bool first = (s.k == 0);
+  const double *pold = (s.k & 1) ? ws.p[0] : ws.p[1];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ns; i += gridDim.x * blockDim.x)
+    ws.sendBuf[i] = pval(ws.w, pold, s.beta, first, cells[i]);
+}
+
+void launch_pack_p(cudaStream_t s, int32_t ns, const int32_t *cells, const Workspace &ws) {
+  if (ns <= 0) return;
+  k_pack_p<<<(ns + BS - 1) / BS, BS, 0, s>>>(ns, cells, ws);
+}
+
+// ------------------------------------------------------------ utilities
+static int grid_for(int64_t n) {
+  int64_t g = (n + BS - 1) / BS;
+  if (g < 1) g = 1;
+  if (g > 65535L * 8) g = 65535L * 8;
+  return (int)g;
+}
+
+__global__ void k_permute(int32_t n, const int32_t *__restrict__ idx, const double *__restrict__ in,
+                          double *__restrict__ out, bool scatter) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    if (scatter)
+      out[idx[i]] = in[i];
+    else
+      out[i] = in[idx[i]];
+  }
+}
+
+void launch_permute(cudaStream_t s, int32_t n, const int32_t *idx, const double *in, double *out,
+                    bool scatter) {
+  if (n <= 0) return;
+  k_permute<<<grid_for(n), BS, 0, s>>>(n, idx, in, out, scatter);
+}
+
+__global__ void k_gather_f64(int64_t n, const int32_t *__restrict__ idx, const double *__restrict__ in,
+                             double *__restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = in[idx[i]];
+}
+
+void launch_gather_f64(cudaStream_t s, int64_t n, const int32_t *idx, const double *in, double *out) {
+  if (n <= 0) return;
+  k_gather_f64<<<grid_for(n), BS, 0, s>>>(n, idx, in, out);
+}
+
+__global__ void k_gather_i32(int64_t n, const int32_t *__restrict__ idx, const int32_t *__restrict__ in,
+                             int32_t *__restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = in[idx[i]];
+}
+
+void launch_gather_i32(cudaStream_t s, int64_t n, const int32_t *idx, const int32_t *in, int32_t *out) {
+  if (n <= 0) return;
+  k_gather_i32<<<grid_for(n), BS, 0, s>>>(n, idx, in, out);
+}
+
+__global__ void k_iota(int32_t *a, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    a[i] = (int32_t)i;
+}
+
+void launch_iota(cudaStream_t s, int32_t *a, int64_t n) {
+  if (n <= 0) return;
+  k_iota<<<grid_for(n), BS, 0, s>>>(a, n);
+}
+
+// starts[g] = first position of key >= g in a sorted key list (n+1 entries,
+// total appended — reading A14).  Every starts[] entry is written by exactly
+// one thread: thread f covers groups (sorted[f-1], sorted[f]].  This is the
+// exclusive scan of the per-group counts of P:419-427 without the sentinel
+// sort (any equivalent primitive, A17).
+__global__ void k_starts(const int32_t *__restrict__ sorted, int64_t m, int32_t n, int32_t *starts) {
+  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f <= m; f += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t prev = f > 0 ? sorted[f - 1] : -1;
+    const int32_t cur = f < m ? sorted[f] : n;
+    for (int32_t g = prev + 1; g <= cur; ++g) starts[g] = (int32_t)f;
+  }
+}
+
+void launch_starts_from_sorted(cudaStream_t s, const int32_t *sorted, int64_t m, int32_t n,
+                               int32_t *starts) {
+  k_starts<<<grid_for(m + 1), BS, 0, s>>>(sorted, m, n, starts);
+}
+
+__global__ void k_make_keys(const int32_t *__restrict__ a, const int32_t *__restrict__ b, int64_t m,
+                            uint64_t *keys) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t x = (uint32_t)a[i], y = (uint32_t)b[i];
+    const uint32_t lo = x < y ? x : y, hi = x < y ? y : x;
+    keys[i] = ((uint64_t)lo << 32) | hi;
+  }
+}
+
+void launch_make_keys(cudaStream_t s, const int32_t *a, const int32_t *b, int64_t m, uint64_t *keys) {
+  if (m <= 0) return;
+  k_make_keys<<<grid_for(m), BS, 0, s>>>(a, b, m, keys);
+}
+
+__global__ void k_split_keys(const uint64_t *__restrict__ keys, int64_t m, int32_t *lo, int32_t *hi) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    lo[i] = (int32_t)(keys[i] >> 32);
+    hi[i] = (int32_t)(keys[i] & 0xffffffffu);
+  }
+}
+
+void launch_split_keys(cudaStream_t s, const uint64_t *keys, int64_t m, int32_t *lo, int32_t *hi) {
+  if (m <= 0) return;
+  k_split_keys<<<grid_for(m), BS, 0, s>>>(keys, m, lo, hi);
+}
+
+// ELL slices from the CSR lists (see the header comment).  Padding: -1.
+__global__ void k_build_ell(MeshDev m, const int32_t *__restrict__ owner, int32_t K, int32_t *nbrE,
+                            int32_t *loE) {
+  const int n = m.n;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
+    const int o0 = m.ownerStart[c], o1 = m.ownerStart[c + 1];
+    const int l0 = m.losortStart[c], l1 = m.losortStart[c + 1];
+    for (int k = 0; k < K; ++k) {
+      nbrE[k * n + c] = o0 + k < o1 ? m.nbr[o0 + k] : -1;
+      int packed = -1;
+      if (l0 + k < l1) {
+        const int f = m.losort[l0 + k];
+        const int oc = owner[f];
+        packed = ((f - m.ownerStart[oc]) << ELL_SHIFT) | oc;
+      }
+      loE[k * n + c] = packed;
+    }
+  }
+}
+
+void launch_build_ell(cudaStream_t s, const MeshDev &m, const int32_t *owner, int32_t K, int32_t *nbrE,
+                      int32_t *loE) {
+  k_build_ell<<<grid_for(m.n), BS, 0, s>>>(m, owner, K, nbrE, loE);
+}
+
+// ------------------------------------------------------------- CUB sorts
+// Stable LSD radix sort (the paper's "std::sort" of P:409, made stable per
+// reading A13).  In-place interface over a scratch double buffer.
+template <class Key>
+static void sort_pairs(cudaStream_t s, Key *keys, int32_t *vals, int64_t m, int end_bit) {
+  if (m <= 1) return;
+  Key *k2 = nullptr;
+  int32_t *v2 = nullptr;
+  void *tmp = nullptr;
+  size_t tb = 0;
+  LF_CUDA(cudaMallocAsync(&k2, sizeof(Key) * m, s));
+  LF_CUDA(cudaMallocAsync(&v2, sizeof(int32_t) * m, s));
+  cub::DoubleBuffer<Key> kb(keys, k2);
+  cub::DoubleBuffer<int32_t> vb(vals, v2);
+  LF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kb, vb, m, 0, end_bit, s));
+  LF_CUDA(cudaMallocAsync(&tmp, tb, s));
+  LF_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, kb, vb, m, 0, end_bit, s));
+  if (kb.Current() != keys) LF_CUDA(cudaMemcpyAsync(keys, kb.Current(), sizeof(Key) * m, cudaMemcpyDeviceToDevice, s));
+  if (vb.Current() != vals) LF_CUDA(cudaMemcpyAsync(vals, vb.Current(), sizeof(int32_t) * m, cudaMemcpyDeviceToDevice, s));
+  LF_CUDA(cudaFreeAsync(tmp, s));
+  LF_CUDA(cudaFreeAsync(k2, s));
+  LF_CUDA(cudaFreeAsync(v2, s));
+}
+
+void sort_pairs_u64(cudaStream_t s, uint64_t *keys, int32_t *vals, int64_t m, int end_bit) {
+  sort_pairs<uint64_t>(s, keys, vals, m, end_bit);
+}
+void sort_pairs_i32(cudaStream_t s, int32_t *keys, int32_t *vals, int64_t m, int end_bit) {
+  sort_pairs<int32_t>(s, keys, vals, m, end_bit);
+}
+
+// ------------------------------------------------------------- occupancy
+int occupancy_grid(int kernel_id, int device) {
+  int sms = 0, nb = 0;
+  LF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  const void *fn = nullptr;
+  switch (kernel_id) {
+    case 0: fn = (const void *)k_assemble<true>; break;
+    case 1: fn = (const void *)k_phase1<3>; break;
+    case 2: fn = (const void *)k_phase2; break;
+    case 3: fn = (const void *)k_amul<3>; break;
+    case 4: fn = (const void *)k_pcg_setup<3>; break;
+    case 5: fn = (const void *)k_sum; break;
+    default: fn = (const void *)k_assemble<false>; break;
+  }
+  LF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, BS, 0));
+  if (nb < 1) nb = 1;
+  return sms * nb;
+}
+
+}  // namespace lf

@@ -1,0 +1,158 @@
+// Internal declarations of liblfoam.so (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "lfoam.h"
+
+namespace lf {
+
+struct Error {
+  lf_status st;
+  std::string msg;
+};
+
+#define LF_CUDA(x)                                                                     \
+  do {                                                                                 \
+    cudaError_t e_ = (x);                                                              \
+    if (e_ != cudaSuccess)                                                             \
+      throw ::lf::Error{e_ == cudaErrorMemoryAllocation ? LF_ERR_OOM : LF_ERR_CUDA,    \
+                        std::string(#x) + ": " + cudaGetErrorString(e_)};              \
+  } while (0)
+
+#define LF_REQUIRE(cond, msg)                                                          \
+  do {                                                                                 \
+    if (!(cond)) throw ::lf::Error{LF_ERR_INVALID_ARG, (msg)};                         \
+  } while (0)
+
+// ------------------------------------------------------------ device memory
+// Every device array of a mesh is allocated once at mesh_create.
+struct DevArena {
+  std::vector<void *> ptrs;
+  int64_t bytes = 0;
+  template <class T>
+  T *alloc(size_t n) {
+    void *p = nullptr;
+    size_t b = sizeof(T) * (n > 0 ? n : 1);
+    LF_CUDA(cudaMalloc(&p, b));
+    ptrs.push_back(p);
+    bytes += (int64_t)b;
+    return static_cast<T *>(p);
+  }
+  void release() {
+    for (void *p : ptrs) cudaFree(p);
+    ptrs.clear();
+    bytes = 0;
+  }
+  ~DevArena() { release(); }
+};
+
+// ---------------------------------------------------------- solver control
+// Device-resident PCG state.  Kernels read it at entry; only the LAST block
+// of a launch (ticket order) writes it, after every block has read it, so a
+// launch never observes its own updates.  See DESIGN.md "Device-side loop".
+struct PcgCtl {
+  double tol, relTol;
+  int32_t maxIter, minIter;
+  double nTotal;        // global cell count (gAverage denominator)
+  double *psi;          // solution vector of the current solve
+  double normFactor, initRes, finRes;
+  double wArA, alpha;
+  int32_t it, stop, converged, singular;
+};
+
+// Global sums consumed by the next launch (after the allreduce in multi-GPU).
+struct RedSlots {
+  double setup[3];  // sum(|A psi - tmp| + |b - tmp|), sum|r|, sum w.r
+  double p1[2];     // sum p.q, sum psi
+  double p2[2];     // sum|r|, sum w.r
+};
+
+// Read-only view of a mesh on the device (kernel argument, by value).
+struct MeshDev {
+  int32_t n, F;
+  const int32_t *ownerStart, *nbr, *losortStart, *losort, *losortOwner;
+  const double *magSf, *delta, *V;
+  // boundary faces with coefficients (fixedValue + processor) grouped per cell
+  const int32_t *bcStart, *bcFace;
+  const int8_t *bType;  // per flat boundary face (lf_patch_type)
+  const double *bMagSf, *bDelta, *bValue;
+  const int32_t *bSlot;  // per flat boundary face: halo slot (processor) or -1
+  // processor faces grouped per cell (Amul interface term); null if none
+  const int32_t *pcStart, *pcFace;
+  int32_t hasProc;
+  // ELL slices of the same addressing (K = max faces per side, 0 = none);
+  // slot k of cell c at k*n + c.  See kernels.cu header.
+  int32_t K;
+  const int32_t *nbrE, *loE;
+};
+
+struct LduDev {
+  double *upperE;  // [K*n] ELL copy of upper (owner side), 0 in padding
+  double *diag, *upper, *source;
+  double *bInt, *bBnd;  // per flat boundary face: internalCoeffs, boundaryCoeffs
+};
+
+// ---------------------------------------------------------------- kernels
+struct Launch {
+  int grid, block;
+};
+
+struct Workspace {
+  double *r, *w, *q, *p[2];
+  double *partials;     // [4 * maxGrid]
+  unsigned *tickets;    // [16]
+  PcgCtl *ctl;
+  RedSlots *gsum;       // global sums
+  RedSlots *lsum;       // local sums (== gsum when single rank)
+  double *sendBuf, *recvBuf;
+  int32_t *sendCell;    // [n_proc] local cell of each send slot
+  int maxGrid;
+};
+
+// kernels.cu launchers (all stream-ordered, no host sync)
+void launch_sum(cudaStream_t s, const Launch &L, const double *x, int32_t n, const Workspace &ws,
+                double *out);
+void launch_assemble(cudaStream_t s, const Launch &L, const MeshDev &m, const LduDev &a,
+                     double DT, double rDeltaT, const double *T, const double *halo,
+                     bool setup, const Workspace &ws);
+void launch_pcg_setup(cudaStream_t s, const Launch &L, const MeshDev &m, const LduDev &a,
+                      const double *halo, const Workspace &ws);
+void launch_phase1(cudaStream_t s, const Launch &L, const MeshDev &m, const LduDev &a,
+                   const double *halo, const Workspace &ws);
+void launch_phase2(cudaStream_t s, const Launch &L, int32_t n, const LduDev &a,
+                   const Workspace &ws);
+void launch_amul(cudaStream_t s, const Launch &L, const MeshDev &m, const LduDev &a,
+                 const double *halo, const double *x, double *y);
+void launch_pack_x(cudaStream_t s, int32_t nsend, const int32_t *cells, const double *x,
+                   double *buf);
+void launch_pack_p(cudaStream_t s, int32_t nsend, const int32_t *cells, const Workspace &ws);
+void launch_permute(cudaStream_t s, int32_t n, const int32_t *idx, const double *in, double *out,
+                    bool scatter);
+void launch_gather_f64(cudaStream_t s, int64_t n, const int32_t *idx, const double *in,
+                       double *out);
+
+// mesh-build kernels (kernels.cu)
+void launch_iota(cudaStream_t s, int32_t *a, int64_t n);
+void launch_starts_from_sorted(cudaStream_t s, const int32_t *sorted, int64_t m, int32_t n,
+                               int32_t *starts);
+void launch_split_keys(cudaStream_t s, const uint64_t *keys, int64_t m, int32_t *lo, int32_t *hi);
+void launch_make_keys(cudaStream_t s, const int32_t *a, const int32_t *b, int64_t m,
+                      uint64_t *keys);
+void launch_gather_i32(cudaStream_t s, int64_t n, const int32_t *idx, const int32_t *in,
+                       int32_t *out);
+void launch_build_ell(cudaStream_t s, const MeshDev &m, const int32_t *owner, int32_t K, int32_t *nbrE,
+                      int32_t *loE);
+// CUB wrappers (kernels.cu): stable radix sort of (key, value) pairs.
+void sort_pairs_u64(cudaStream_t s, uint64_t *keys, int32_t *vals, int64_t m, int end_bit);
+void sort_pairs_i32(cudaStream_t s, int32_t *keys, int32_t *vals, int64_t m, int end_bit);
+
+int kernel_block_size();
+int occupancy_grid(int kernel_id, int device);  // resident-grid size for a kernel
+
+}  // namespace lf

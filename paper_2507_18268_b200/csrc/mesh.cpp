@@ -1,0 +1,438 @@
+// mesh_create: validation, optional RCM renumbering, upload and the
+// device-side build of the atomic-free addressing of P:387-429 / P:471-481.
+#include <algorithm>
+#include <cmath>
+#include <numeric>
+
+#include "host.h"
+
+namespace lf {
+
+// Reverse Cuthill-McKee on the cell graph (host, once per mesh).  Returns
+// order[i] = caller label of internal cell i.  Start of each component: a
+// pseudo-peripheral cell (two BFS sweeps from the minimum-degree cell).
+static std::vector<int32_t> rcm_order(int32_t n, int32_t F, const int32_t *own, const int32_t *nbr) {
+  std::vector<int32_t> deg(n, 0), start(n + 1, 0), adj(2 * (size_t)F);
+  for (int32_t f = 0; f < F; ++f) {
+    deg[own[f]]++;
+    deg[nbr[f]]++;
+  }
+  for (int32_t c = 0; c < n; ++c) start[c + 1] = start[c] + deg[c];
+  std::vector<int32_t> fill(start.begin(), start.end() - 1);
+  for (int32_t f = 0; f < F; ++f) {
+    adj[fill[own[f]]++] = nbr[f];
+    adj[fill[nbr[f]]++] = own[f];
+  }
+  for (int32_t c = 0; c < n; ++c)
+    std::sort(adj.begin() + start[c], adj.begin() + start[c + 1], [&](int32_t a, int32_t b) {
+      return deg[a] != deg[b] ? deg[a] < deg[b] : a < b;
+    });
+  std::vector<int32_t> order;
+  order.reserve(n);
+  std::vector<int32_t> level(n, -1);
+  std::vector<char> visited(n, 0);
+  auto bfs_last = [&](int32_t s, std::vector<int32_t> &touched) {
+    // BFS from s; returns min-degree cell of the last level
+    touched.clear();
+    touched.push_back(s);
+    level[s] = 0;
+    size_t head = 0;
+    int32_t maxl = 0;
+    while (head < touched.size()) {
+      int32_t u = touched[head++];
+      for (int32_t k = start[u]; k < start[u + 1]; ++k) {
+        int32_t v = adj[k];
+        if (level[v] < 0) {
+          level[v] = level[u] + 1;
+          maxl = std::max(maxl, level[v]);
+          touched.push_back(v);
+        }
+      }
+    }
+    int32_t best = s;
+    for (int32_t u : touched)
+      if (level[u] == maxl && (deg[u] < deg[best] || level[best] != maxl)) best = u;
+    for (int32_t u : touched) level[u] = -1;
+    return best;
+  };
+  std::vector<int32_t> touched;
+  std::vector<int32_t> byDeg(n);
+  std::iota(byDeg.begin(), byDeg.end(), 0);
+  std::stable_sort(byDeg.begin(), byDeg.end(), [&](int32_t a, int32_t b) { return deg[a] < deg[b]; });
+  for (int32_t s0 : byDeg) {
+    if (visited[s0]) continue;
+    int32_t s = bfs_last(s0, touched);
+    s = bfs_last(s, touched);
+    size_t head = order.size();
+    order.push_back(s);
+    visited[s] = 1;
+    while (head < order.size()) {
+      int32_t u = order[head++];
+      for (int32_t k = start[u]; k < start[u + 1]; ++k) {
+        int32_t v = adj[k];
+        if (!visited[v]) {
+          visited[v] = 1;
+          order.push_back(v);
+        }
+      }
+    }
+  }
+  std::reverse(order.begin(), order.end());
+  return order;
+}
+
+static void validate(const lf_mesh_desc *d, int rank) {
+  LF_REQUIRE(d != nullptr, "desc is NULL");
+  LF_REQUIRE(d->n_cells >= 1, "n_cells must be >= 1");
+  LF_REQUIRE(d->n_faces >= 0, "n_faces must be >= 0");
+  LF_REQUIRE(d->n_patches >= 0, "n_patches must be >= 0");
+  LF_REQUIRE(d->n_faces == 0 || (d->owner && d->neighbour && d->mag_sf && d->delta_coeffs),
+             "owner/neighbour/mag_sf/delta_coeffs required");
+  LF_REQUIRE(d->V != nullptr, "V required");
+  LF_REQUIRE(d->n_patches == 0 || d->patches, "patches required");
+  const int32_t n = d->n_cells;
+  for (int32_t f = 0; f < d->n_faces; ++f) {
+    const int32_t o = d->owner[f], nb = d->neighbour[f];
+    if (o < 0 || o >= n || nb < 0 || nb >= n)
+      throw Error{LF_ERR_INVALID_ARG, "face " + std::to_string(f) + ": label out of range"};
+    if (o == nb) throw Error{LF_ERR_INVALID_ARG, "face " + std::to_string(f) + ": owner == neighbour"};
+    if (!(d->mag_sf[f] > 0.0) || !std::isfinite(d->mag_sf[f]))
+      throw Error{LF_ERR_INVALID_ARG, "face " + std::to_string(f) + ": mag_sf must be > 0"};
+    if (!(d->delta_coeffs[f] > 0.0) || !std::isfinite(d->delta_coeffs[f]))
+      throw Error{LF_ERR_INVALID_ARG, "face " + std::to_string(f) + ": delta_coeffs must be > 0"};
+  }
+  for (int32_t c = 0; c < n; ++c)
+    if (!(d->V[c] > 0.0) || !std::isfinite(d->V[c]))
+      throw Error{LF_ERR_INVALID_ARG, "cell " + std::to_string(c) + ": V must be > 0"};
+  int selfOpen = 0;
+  for (int32_t p = 0; p < d->n_patches; ++p) {
+    const lf_patch_desc &P = d->patches[p];
+    const std::string pn = "patch " + std::to_string(p);
+    LF_REQUIRE(P.type == LF_PATCH_FIXED_VALUE || P.type == LF_PATCH_ZERO_GRADIENT ||
+                   P.type == LF_PATCH_PROCESSOR,
+               pn + ": unknown type");
+    LF_REQUIRE(P.n_faces >= 0, pn + ": n_faces < 0");
+    LF_REQUIRE(P.n_faces == 0 || (P.face_cells && P.mag_sf && P.delta_coeffs),
+               pn + ": face_cells/mag_sf/delta_coeffs required");
+    for (int32_t i = 0; i < P.n_faces; ++i) {
+      LF_REQUIRE(P.face_cells[i] >= 0 && P.face_cells[i] < n, pn + ": face_cells out of range");
+      LF_REQUIRE(P.mag_sf[i] > 0.0 && std::isfinite(P.mag_sf[i]), pn + ": mag_sf must be > 0");
+      LF_REQUIRE(P.delta_coeffs[i] > 0.0 && std::isfinite(P.delta_coeffs[i]),
+                 pn + ": delta_coeffs must be > 0");
+    }
+    if (P.type == LF_PATCH_PROCESSOR && P.neighb_rank == rank) selfOpen ^= 1;
+  }
+  LF_REQUIRE(selfOpen == 0, "self-coupled processor patches must come in pairs");
+}
+
+}  // namespace lf
+
+using namespace lf;
+
+lf_mesh::~lf_mesh() {
+  for (auto &g : chunkGraph)
+    if (g) cudaGraphExecDestroy(g);
+  if (hctl) cudaFreeHost(hctl);
+  arena.release();
+}
+
+static void build_mesh(lf_context *ctx, const lf_mesh_desc *d, lf_mesh *M) {
+  validate(d, ctx->rank);
+  cudaStream_t s = ctx->stream;
+  DevArena &A = M->arena;
+  const int32_t n = d->n_cells, F = d->n_faces;
+  M->ctx = ctx;
+  M->n = n;
+  M->F = F;
+  M->nPatches = d->n_patches;
+
+  // ---------------------------------------------- optional renumbering
+  std::vector<int32_t> iperm;  // caller -> internal
+  if (d->renumber) {
+    std::vector<int32_t> order = rcm_order(n, F, d->owner, d->neighbour);
+    iperm.assign(n, 0);
+    for (int32_t i = 0; i < n; ++i) iperm[order[i]] = i;
+    M->renumbered = true;
+    M->cellPerm = A.alloc<int32_t>(n);
+    M->cellIperm = A.alloc<int32_t>(n);
+    LF_CUDA(cudaMemcpyAsync(M->cellPerm, order.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+    LF_CUDA(cudaMemcpyAsync(M->cellIperm, iperm.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+    LF_CUDA(cudaStreamSynchronize(s));
+  }
+  auto relabel = [&](const int32_t *src, size_t m) {
+    std::vector<int32_t> out(src, src + m);
+    if (!iperm.empty())
+      for (auto &x : out) x = iperm[x];
+    return out;
+  };
+
+  // ------------------------------------------------- internal faces
+  // upper-triangular re-sort: key = (min label, max label), stable
+  int32_t *ownerU = A.alloc<int32_t>(F), *nbrU = A.alloc<int32_t>(F);
+  uint64_t *keys = nullptr;
+  LF_CUDA(cudaMallocAsync(&keys, sizeof(uint64_t) * std::max(F, 1), s));
+  {
+    std::vector<int32_t> o = relabel(d->owner, F), nb = relabel(d->neighbour, F);
+    LF_CUDA(cudaMemcpyAsync(ownerU, o.data(), sizeof(int32_t) * F, cudaMemcpyHostToDevice, s));
+    LF_CUDA(cudaMemcpyAsync(nbrU, nb.data(), sizeof(int32_t) * F, cudaMemcpyHostToDevice, s));
+    launch_make_keys(s, ownerU, nbrU, F, keys);
+    LF_CUDA(cudaStreamSynchronize(s));
+  }
+  M->facePerm = A.alloc<int32_t>(F);
+  launch_iota(s, M->facePerm, F);
+  int bits = 1;
+  while ((1ll << bits) < (long long)n) ++bits;
+  sort_pairs_u64(s, keys, M->facePerm, F, 32 + bits);
+  int32_t *owner = ownerU, *nbr = nbrU;  // reuse buffers for the sorted labels
+  launch_split_keys(s, keys, F, owner, nbr);
+  LF_CUDA(cudaFreeAsync(keys, s));
+  M->ownerInt = owner;
+
+  double *magSf = A.alloc<double>(F), *delta = A.alloc<double>(F);
+  {
+    double *tmp = nullptr;
+    LF_CUDA(cudaMallocAsync(&tmp, sizeof(double) * std::max(F, 1), s));
+    LF_CUDA(cudaMemcpyAsync(tmp, d->mag_sf, sizeof(double) * F, cudaMemcpyHostToDevice, s));
+    launch_gather_f64(s, F, M->facePerm, tmp, magSf);
+    LF_CUDA(cudaMemcpyAsync(tmp, d->delta_coeffs, sizeof(double) * F, cudaMemcpyHostToDevice, s));
+    launch_gather_f64(s, F, M->facePerm, tmp, delta);
+    LF_CUDA(cudaFreeAsync(tmp, s));
+  }
+  int32_t *ownerStart = A.alloc<int32_t>(n + 1);
+  launch_starts_from_sorted(s, owner, F, n, ownerStart);
+  // losort = stable argsort of neighbour (the paper's neighbourList)
+  int32_t *losort = A.alloc<int32_t>(F), *losortStart = A.alloc<int32_t>(n + 1),
+          *losortOwner = A.alloc<int32_t>(F);
+  {
+    int32_t *k2 = nullptr;
+    LF_CUDA(cudaMallocAsync(&k2, sizeof(int32_t) * std::max(F, 1), s));
+    LF_CUDA(cudaMemcpyAsync(k2, nbr, sizeof(int32_t) * F, cudaMemcpyDeviceToDevice, s));
+    launch_iota(s, losort, F);
+    sort_pairs_i32(s, k2, losort, F, bits);
+    launch_starts_from_sorted(s, k2, F, n, losortStart);
+    launch_gather_i32(s, F, losort, owner, losortOwner);
+    LF_CUDA(cudaFreeAsync(k2, s));
+  }
+  double *V = A.alloc<double>(n);
+  {
+    if (iperm.empty()) {
+      LF_CUDA(cudaMemcpyAsync(V, d->V, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    } else {
+      std::vector<double> v(n);
+      for (int32_t c = 0; c < n; ++c) v[iperm[c]] = d->V[c];
+      LF_CUDA(cudaMemcpyAsync(V, v.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s));
+      LF_CUDA(cudaStreamSynchronize(s));
+    }
+  }
+
+  // ------------------------------------------------------ boundary
+  int32_t B = 0;
+  for (int32_t p = 0; p < d->n_patches; ++p) B += d->patches[p].n_faces;
+  M->B = B;
+  std::vector<int32_t> hCell(B), hSlot(B, -1);
+  std::vector<int8_t> hType(B);
+  std::vector<double> hMag(B), hDel(B), hVal(B, 0.0);
+  M->patchStart.assign(d->n_patches + 1, 0);
+  int32_t nproc = 0;
+  std::vector<int32_t> sendCells;
+  std::vector<int32_t> selfOpenSeg;
+  for (int32_t p = 0, off = 0; p < d->n_patches; ++p) {
+    const lf_patch_desc &P = d->patches[p];
+    M->patchType.push_back(P.type);
+    M->patchRank.push_back(P.type == LF_PATCH_PROCESSOR ? P.neighb_rank : -1);
+    if (P.type == LF_PATCH_PROCESSOR) {
+      LF_REQUIRE(P.neighb_rank >= 0 && P.neighb_rank < ctx->nranks,
+                 "patch " + std::to_string(p) + ": neighb_rank out of range for the communicator");
+      HaloSeg sg{nproc, P.n_faces, P.neighb_rank, -1};
+      if (P.neighb_rank == ctx->rank) {
+        if (selfOpenSeg.empty()) {
+          selfOpenSeg.push_back((int32_t)M->segs.size());
+        } else {
+          const int32_t a = selfOpenSeg.back();
+          selfOpenSeg.pop_back();
+          LF_REQUIRE(M->segs[a].count == P.n_faces, "self-coupled processor patches differ in size");
+          sg.partner = a;
+          M->segs[a].partner = (int32_t)M->segs.size();
+        }
+      }
+      M->segs.push_back(sg);
+    }
+    for (int32_t i = 0; i < P.n_faces; ++i) {
+      const int32_t fi = off + i;
+      hCell[fi] = iperm.empty() ? P.face_cells[i] : iperm[P.face_cells[i]];
+      hType[fi] = (int8_t)P.type;
+      hMag[fi] = P.mag_sf[i];
+      hDel[fi] = P.delta_coeffs[i];
+      if (P.type == LF_PATCH_FIXED_VALUE && P.value) hVal[fi] = P.value[i];
+      if (P.type == LF_PATCH_PROCESSOR) {
+        hSlot[fi] = nproc++;
+        sendCells.push_back(hCell[fi]);
+      }
+    }
+    off += P.n_faces;
+    M->patchStart[p + 1] = off;
+  }
+  M->nproc = nproc;
+  M->bCell = A.alloc<int32_t>(B);
+  int8_t *bType = A.alloc<int8_t>(B);
+  double *bMag = A.alloc<double>(B), *bDel = A.alloc<double>(B);
+  M->bValue = A.alloc<double>(B);
+  int32_t *bSlot = A.alloc<int32_t>(B);
+  LF_CUDA(cudaMemcpyAsync(M->bCell, hCell.data(), sizeof(int32_t) * B, cudaMemcpyHostToDevice, s));
+  LF_CUDA(cudaMemcpyAsync(bType, hType.data(), B, cudaMemcpyHostToDevice, s));
+  LF_CUDA(cudaMemcpyAsync(bMag, hMag.data(), sizeof(double) * B, cudaMemcpyHostToDevice, s));
+  LF_CUDA(cudaMemcpyAsync(bDel, hDel.data(), sizeof(double) * B, cudaMemcpyHostToDevice, s));
+  LF_CUDA(cudaMemcpyAsync(M->bValue, hVal.data(), sizeof(double) * B, cudaMemcpyHostToDevice, s));
+  LF_CUDA(cudaMemcpyAsync(bSlot, hSlot.data(), sizeof(int32_t) * B, cudaMemcpyHostToDevice, s));
+
+  // per-cell groups of coefficient faces (fixedValue + processor), kept in
+  // (patch, face) order by the stable sort: facePatchIndex/facePatchStart
+  // of P:471-481 over all patches at once.
+  auto group_cells = [&](const std::vector<int32_t> &sel, int32_t *&startOut, int32_t *&itemsOut) {
+    const int32_t m = (int32_t)sel.size();
+    startOut = A.alloc<int32_t>(n + 1);
+    itemsOut = A.alloc<int32_t>(m);
+    std::vector<int32_t> k(m);
+    for (int32_t i = 0; i < m; ++i) k[i] = hCell[sel[i]];
+    int32_t *dk = nullptr;
+    LF_CUDA(cudaMallocAsync(&dk, sizeof(int32_t) * std::max(m, 1), s));
+    LF_CUDA(cudaMemcpyAsync(dk, k.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, s));
+    LF_CUDA(cudaMemcpyAsync(itemsOut, sel.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, s));
+    sort_pairs_i32(s, dk, itemsOut, m, bits);
+    launch_starts_from_sorted(s, dk, m, n, startOut);
+    LF_CUDA(cudaFreeAsync(dk, s));
+    LF_CUDA(cudaStreamSynchronize(s));
+  };
+  std::vector<int32_t> selBc, selProc;
+  for (int32_t i = 0; i < B; ++i) {
+    if (hType[i] != LF_PATCH_ZERO_GRADIENT) selBc.push_back(i);
+    if (hType[i] == LF_PATCH_PROCESSOR) selProc.push_back(i);
+  }
+  int32_t *bcStart, *bcFace;
+  group_cells(selBc, bcStart, bcFace);
+  int32_t *pcStart = nullptr, *pcFace = nullptr;
+  if (nproc > 0) group_cells(selProc, pcStart, pcFace);
+
+  // ------------------------------------------------------- matrix
+  LduDev &L = M->ld;
+  L.diag = A.alloc<double>(n);
+  L.upper = A.alloc<double>(F);
+  L.source = A.alloc<double>(n);
+  L.bInt = A.alloc<double>(B);
+  L.bBnd = A.alloc<double>(B);
+  LF_CUDA(cudaMemsetAsync(L.bInt, 0, sizeof(double) * std::max(B, 1), s));
+  LF_CUDA(cudaMemsetAsync(L.bBnd, 0, sizeof(double) * std::max(B, 1), s));
+
+  MeshDev &md = M->md;
+  md.n = n;
+  md.F = F;
+  md.ownerStart = ownerStart;
+  md.nbr = nbr;
+  md.losortStart = losortStart;
+  md.losort = losort;
+  md.losortOwner = losortOwner;
+  md.magSf = magSf;
+  md.delta = delta;
+  md.V = V;
+  md.bcStart = bcStart;
+  md.bcFace = bcFace;
+  md.bType = bType;
+  md.bMagSf = bMag;
+  md.bDelta = bDel;
+  md.bValue = M->bValue;
+  md.bSlot = bSlot;
+  md.pcStart = pcStart;
+  md.pcFace = pcFace;
+  md.hasProc = nproc > 0;
+
+  // ------------------------------------------ ELL slices for the solve
+  // K = max faces per side (3 on hex meshes); built when 1 <= K <= 4 and the
+  // packed owner-slot label fits (n < 2^29), else the CSR gather is used.
+  md.K = 0;
+  md.nbrE = md.loE = nullptr;
+  L.upperE = nullptr;
+  if (F > 0 && n < (1 << 29)) {
+    std::vector<int32_t> hs(n + 1), hl(n + 1);
+    LF_CUDA(cudaMemcpyAsync(hs.data(), ownerStart, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost, s));
+    LF_CUDA(cudaMemcpyAsync(hl.data(), losortStart, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost, s));
+    LF_CUDA(cudaStreamSynchronize(s));
+    int K = 0;
+    for (int32_t c = 0; c < n; ++c) K = std::max({K, hs[c + 1] - hs[c], hl[c + 1] - hl[c]});
+    if (K >= 1 && K <= 4) {
+      const int KE = K <= 3 ? 3 : 4;  // kernels are specialised for 3 and 4 slots
+      int32_t *nbrE = A.alloc<int32_t>((size_t)KE * n), *loE = A.alloc<int32_t>((size_t)KE * n);
+      L.upperE = A.alloc<double>((size_t)KE * n);
+      LF_CUDA(cudaMemsetAsync(L.upperE, 0, sizeof(double) * KE * (size_t)n, s));
+      md.K = KE;
+      launch_build_ell(s, md, owner, KE, nbrE, loE);
+      md.nbrE = nbrE;
+      md.loE = loE;
+    }
+  }
+
+  // ------------------------------------------------------ workspace
+  const int BSZ = kernel_block_size();
+  auto grid = [&](int kid) {
+    int g = occupancy_grid(kid, ctx->device);
+    int need = (int)((n + BSZ - 1) / BSZ);
+    return Launch{std::max(1, std::min(g, need)), BSZ};
+  };
+  M->Lasm = grid(0);
+  M->Lp1 = grid(1);
+  M->Lp2 = grid(2);
+  M->Lamul = grid(3);
+  M->Lsetup = grid(4);
+  M->Lsum = grid(5);
+  int maxGrid = std::max({M->Lasm.grid, M->Lp1.grid, M->Lp2.grid, M->Lamul.grid, M->Lsetup.grid, M->Lsum.grid});
+  Workspace &ws = M->ws;
+  ws.maxGrid = maxGrid;
+  ws.r = A.alloc<double>(n);
+  ws.w = A.alloc<double>(n);
+  ws.q = A.alloc<double>(n);
+  ws.p[0] = A.alloc<double>(n);
+  ws.p[1] = A.alloc<double>(n);
+  ws.partials = A.alloc<double>(4 * (size_t)maxGrid);
+  ws.tickets = A.alloc<unsigned>(16);
+  LF_CUDA(cudaMemsetAsync(ws.tickets, 0, 16 * sizeof(unsigned), s));
+  ws.ctl = A.alloc<PcgCtl>(1);
+  LF_CUDA(cudaMemsetAsync(ws.ctl, 0, sizeof(PcgCtl), s));
+  ws.gsum = A.alloc<RedSlots>(1);
+  LF_CUDA(cudaMemsetAsync(ws.gsum, 0, sizeof(RedSlots), s));
+  ws.lsum = ctx->comm ? A.alloc<RedSlots>(1) : ws.gsum;
+  if (ctx->comm) LF_CUDA(cudaMemsetAsync(ws.lsum, 0, sizeof(RedSlots), s));
+  ws.sendBuf = A.alloc<double>(nproc);
+  ws.recvBuf = A.alloc<double>(nproc);
+  ws.sendCell = A.alloc<int32_t>(nproc);
+  LF_CUDA(cudaMemcpyAsync(ws.sendCell, sendCells.data(), sizeof(int32_t) * nproc, cudaMemcpyHostToDevice, s));
+  M->T = A.alloc<double>(n);
+  LF_CUDA(cudaMemsetAsync(M->T, 0, sizeof(double) * n, s));
+  M->scratch = A.alloc<double>(n);
+  LF_CUDA(cudaMallocHost(&M->hctl, sizeof(PcgCtl)));
+  std::memset(M->hctl, 0, sizeof(PcgCtl));
+
+  // global cell count for gAverage (allreduce once)
+  double nloc = (double)n;
+  if (ctx->comm) {
+    double *dn = nullptr;
+    LF_CUDA(cudaMallocAsync(&dn, 2 * sizeof(double), s));
+    LF_CUDA(cudaMemcpyAsync(dn, &nloc, sizeof(double), cudaMemcpyHostToDevice, s));
+    nccl_allreduce_sum(ctx->comm, dn, dn + 1, 1, s);
+    LF_CUDA(cudaMemcpyAsync(&M->nTotal, dn + 1, sizeof(double), cudaMemcpyDeviceToHost, s));
+    LF_CUDA(cudaFreeAsync(dn, s));
+  } else {
+    M->nTotal = nloc;
+  }
+  LF_CUDA(cudaStreamSynchronize(s));
+  LF_CUDA(cudaGetLastError());
+  M->ldu.mesh = M;
+}
+
+namespace lf {
+void mesh_create_impl(lf_context *ctx, const lf_mesh_desc *d, lf_mesh **out) {
+  LF_REQUIRE(ctx != nullptr && out != nullptr, "NULL context or out");
+  LF_CUDA(cudaSetDevice(ctx->device));
+  std::unique_ptr<lf_mesh> M(new lf_mesh());
+  build_mesh(ctx, d, M.get());
+  *out = M.release();
+}
+}  // namespace lf

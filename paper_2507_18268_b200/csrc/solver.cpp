@@ -1,0 +1,186 @@
+// L3 solver driver: step loop, PCG loop control, halo exchange, reductions.
+//
+// The PCG loop is device-driven (SURVEY.md §7 "loop control without host
+// round trips"): alpha, beta and the OpenFOAM stopping rule are evaluated by
+// the kernels from device-resident sums (PcgCtl); iterations past the stop
+// are no-op launches.  The host enqueues iterations in chunks — the first
+// chunk sized from the previous solve's iteration count — and reads the
+// stop flag once per chunk, so a steady step costs one host sync.
+#include <algorithm>
+
+#include "host.h"
+
+namespace lf {
+
+void allreduce(lf_mesh *M, const double *local, double *global, size_t count) {
+  lf_context *ctx = M->ctx;
+  if (!ctx->comm) return;  // single rank: kernels wrote the global slot directly
+  nccl_allreduce_sum(ctx->comm, local, global, count, ctx->stream);
+}
+
+// recv[seg] <- neighbour's send[seg'] for every processor patch.
+void halo_exchange(lf_mesh *M, const double *send, double *recv) {
+  if (M->nproc == 0) return;
+  lf_context *ctx = M->ctx;
+  cudaStream_t s = ctx->stream;
+  if (!ctx->comm) {
+    for (const HaloSeg &g : M->segs) {
+      if (g.partner < 0) throw Error{LF_ERR_STATE, "processor patch to another rank needs lf_comm_init"};
+      const HaloSeg &p = M->segs[g.partner];
+      LF_CUDA(cudaMemcpyAsync(recv + g.offset, send + p.offset, sizeof(double) * g.count,
+                              cudaMemcpyDeviceToDevice, s));
+    }
+    return;
+  }
+  // NCCL: per peer, the i-th send matches the i-th recv.  Real peers have one
+  // patch each side in the same face order.  Self pairs (a,b): sends a,b;
+  // recvs b,a so that recv[b] <- send[a] and recv[a] <- send[b].
+  nccl_group_start();
+  for (const HaloSeg &g : M->segs) nccl_send(ctx->comm, send + g.offset, g.count, g.peer, s);
+  for (const HaloSeg &g : M->segs) {
+    const HaloSeg &dst = g.partner >= 0 ? M->segs[g.partner] : g;
+    nccl_recv(ctx->comm, recv + dst.offset, dst.count, g.peer, s);
+  }
+  nccl_group_end();
+}
+
+void upload_controls(lf_mesh *M, const lf_solver_controls *c, double *psi) {
+  LF_REQUIRE(c != nullptr, "controls is NULL");
+  LF_REQUIRE(c->tolerance >= 0.0 && c->rel_tol >= 0.0, "tolerances must be >= 0");
+  LF_REQUIRE(c->max_iter >= 0 && c->min_iter >= 0, "max_iter/min_iter must be >= 0");
+  PcgCtl *h = M->hctl;
+  std::memset(h, 0, sizeof(PcgCtl));
+  h->tol = c->tolerance;
+  h->relTol = c->rel_tol;
+  h->maxIter = c->max_iter;
+  h->minIter = c->min_iter;
+  h->nTotal = M->nTotal;
+  h->psi = psi;
+  h->stop = 1;  // nothing runs until a setup kernel resets it
+  LF_CUDA(cudaMemcpyAsync(M->ws.ctl, h, sizeof(PcgCtl), cudaMemcpyHostToDevice, M->ctx->stream));
+  // the pinned mirror is read by the copy engine asynchronously: wait before reuse
+  LF_CUDA(cudaStreamSynchronize(M->ctx->stream));
+}
+
+static void iteration(lf_mesh *M) {
+  lf_context *ctx = M->ctx;
+  cudaStream_t s = ctx->stream;
+  const Workspace &ws = M->ws;
+  if (M->nproc > 0) {
+    ctx->launch(LF_K_PACK, [&] { launch_pack_p(s, M->nproc, ws.sendCell, ws); });
+    halo_exchange(M, ws.sendBuf, ws.recvBuf);
+  }
+  ctx->launch(LF_K_PHASE1, [&] { launch_phase1(s, M->Lp1, M->md, M->ld, ws.recvBuf, ws); });
+  allreduce(M, ws.lsum->p1, ws.gsum->p1, 2);
+  ctx->launch(LF_K_PHASE2, [&] { launch_phase2(s, M->Lp2, M->n, M->ld, ws); });
+  allreduce(M, ws.lsum->p2, ws.gsum->p2, 2);
+}
+
+// Enqueue `count` PCG iterations: as CUDA-graph replays of 2^i-iteration
+// chunks (binary decomposition of count), or as direct launches when the
+// context is instrumented (events bracket every kernel).
+static void enqueue_iterations(lf_mesh *M, int count) {
+  lf_context *ctx = M->ctx;
+  cudaStream_t s = ctx->stream;
+  if (ctx->instrument || !ctx->useGraphs) {
+    for (int i = 0; i < count; ++i) iteration(M);
+    return;
+  }
+  if (M->kernelsPerIteration == 0) M->kernelsPerIteration = (M->nproc > 0 ? 3 : 2);
+  for (int b = lf_mesh::kMaxGraphLog - 1; b >= 0 && count > 0;) {
+    const int k = 1 << b;
+    if (count < k) {
+      --b;
+      continue;
+    }
+    if (!M->chunkGraph[b]) {
+      cudaGraph_t g = nullptr;
+      ctx->capturing = true;
+      LF_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+      try {
+        for (int i = 0; i < k; ++i) iteration(M);
+      } catch (...) {
+        cudaStreamEndCapture(s, &g);
+        if (g) cudaGraphDestroy(g);
+        ctx->capturing = false;
+        throw;
+      }
+      LF_CUDA(cudaStreamEndCapture(s, &g));
+      ctx->capturing = false;
+      cudaError_t e = cudaGraphInstantiate(&M->chunkGraph[b], g, 0);
+      cudaGraphDestroy(g);
+      LF_CUDA(e);
+    }
+    LF_CUDA(cudaGraphLaunch(M->chunkGraph[b], s));
+    ctx->launches += (int64_t)k * M->kernelsPerIteration;
+    ctx->kLaunches[LF_K_PHASE1] += k;
+    ctx->kLaunches[LF_K_PHASE2] += k;
+    if (M->nproc > 0) ctx->kLaunches[LF_K_PACK] += k;
+    count -= k;
+  }
+}
+
+// Runs the iterations after a setup launch (assembly+setup or pcg setup)
+// until the device sets ctl->stop; fills *out.
+static void run_iterations(lf_mesh *M, lf_solver_perf *out) {
+  lf_context *ctx = M->ctx;
+  cudaStream_t s = ctx->stream;
+  const int maxIter = M->hctl->maxIter, minIter = M->hctl->minIter;
+  const int64_t bound = (int64_t)std::max(maxIter, minIter) + 2;
+  int64_t launched = 0;
+  int chunk = M->lastIters >= 0 ? M->lastIters + 1 : 8;
+  for (;;) {
+    chunk = (int)std::max<int64_t>(1, std::min<int64_t>(chunk, bound + 1 - launched));
+    enqueue_iterations(M, chunk);
+    launched += chunk;
+    LF_CUDA(cudaMemcpyAsync(M->hctl, M->ws.ctl, sizeof(PcgCtl), cudaMemcpyDeviceToHost, s));
+    LF_CUDA(cudaStreamSynchronize(s));
+    ctx->harvest();
+    if (ctx->comm) nccl_check_async(ctx->comm);
+    if (M->hctl->stop) break;
+    if (launched > bound) throw Error{LF_ERR_INTERNAL, "PCG loop did not stop within max_iter"};
+    chunk = 8;
+  }
+  const PcgCtl *h = M->hctl;
+  M->lastIters = h->it;
+  if (out) {
+    out->initial_residual = h->initRes;
+    out->final_residual = h->finRes;
+    out->n_iterations = h->it;
+    out->converged = h->converged;
+    out->singular = h->singular;
+    out->reserved = 0;
+  }
+}
+
+static void sum_psi(lf_mesh *M, const double *psi) {
+  lf_context *ctx = M->ctx;
+  ctx->launch(LF_K_SUMPSI, [&] { launch_sum(ctx->stream, M->Lsum, psi, M->n, M->ws, &M->ws.lsum->p1[1]); });
+  allreduce(M, M->ws.lsum->p1, M->ws.gsum->p1, 2);
+}
+
+void solve_loop(lf_mesh *M, const lf_solver_controls *c, double *psi, bool fromAssembly,
+                const lf_laplacian_params *p, lf_solver_perf *out) {
+  lf_context *ctx = M->ctx;
+  cudaStream_t s = ctx->stream;
+  const Workspace &ws = M->ws;
+  const bool psiIsT = (psi == M->T);
+  if (!(psiIsT && M->sumPsiValid)) sum_psi(M, psi);
+  if (M->nproc > 0) {
+    ctx->launch(LF_K_PACK, [&] { launch_pack_x(s, M->nproc, ws.sendCell, psi, ws.sendBuf); });
+    halo_exchange(M, ws.sendBuf, ws.recvBuf);
+  }
+  if (fromAssembly) {
+    ctx->launch(LF_K_ASSEMBLE, [&] {
+      launch_assemble(s, M->Lasm, M->md, M->ld, p->DT, 1.0 / p->dt, psi, ws.recvBuf, true, ws);
+    });
+  } else {
+    ctx->launch(LF_K_SETUP, [&] { launch_pcg_setup(s, M->Lsetup, M->md, M->ld, ws.recvBuf, ws); });
+  }
+  allreduce(M, ws.lsum->setup, ws.gsum->setup, 3);
+  run_iterations(M, out);
+  // gsum->p1[1] now holds sum(psi) of the final psi (last phase-1 launch)
+  M->sumPsiValid = psiIsT;
+}
+
+}  // namespace lf

@@ -470,3 +470,21 @@ def test_step0_normfactor_closed_form(canonical_constants):
     nf = np.sum(np.abs(row["mu"] * s - tmp) + np.abs(V / dt * s - tmp)) + 1e-20
     _, _, perfs = oracle.laplacian_foam(m, s, 1)
     assert abs(perfs[0]["initial_residual"] - row["r0_l1"] / nf) < 1e-10 * row["r0_l1"] / nf
+
+
+def test_reading_A30_normfactor_floor():
+    """Reading A30: with amplitude 1 the decaying mode falls below OpenFOAM's
+    absolute normFactor floor (1e-20) after ~25 steps and the solve
+    degenerates (0 iterations, T stalls); with the canonical 1e80 amplitude
+    the 100-step run keeps the exact discrete decay T^n = g^n T0."""
+    m = meshgen.block_mesh(10)
+    g = 1.0 / (1.0 + 0.2 * lam_h(10))
+    s = meshgen.sine_field(m)
+    T, _, perfs = oracle.laplacian_foam(m, s, 60)
+    assert perfs[-1]["n_iterations"] == 0 and perfs[5]["n_iterations"] >= 15
+    assert np.max(np.abs(T)) > 1e6 * g ** 60          # stalled far above the decay
+    c = meshgen.canonical_field(m)
+    T, _, perfs = oracle.laplacian_foam(m, c, 100)
+    ref = g ** 100 * c
+    assert np.max(np.abs(T - ref)) <= 1e-8 * np.max(np.abs(ref))
+    assert min(p["n_iterations"] for p in perfs) >= 15
