@@ -39,6 +39,9 @@ namespace lf {
 #ifndef LF_MINB
 #define LF_MINB 4        // __launch_bounds__ min blocks/SM (register cap 65536/(BS*MINB))
 #endif
+#ifndef LF_MINB_G
+#define LF_MINB_G 5      // same, for the row-gather kernels (phase 1, Amul, PCG setup)
+#endif
 #ifndef LF_P2_UNROLL
 #define LF_P2_UNROLL 4   // cells per thread per grid-stride trip in phase 2
 #endif
@@ -138,7 +141,7 @@ template <int KE, class XF>
 __device__ __forceinline__ double row_offdiag(const MeshDev &m, const LduDev &a, int c, double acc,
                                               XF xval, double *sU = nullptr) {
   if constexpr (KE > 0) {
-    const int n = m.n;
+    const int n = m.ldE;  // slab stride
     int lo[KE], nb[KE];
     double uo[KE];
 #pragma unroll
@@ -207,6 +210,23 @@ __device__ __forceinline__ double row_proc(const MeshDev &m, const double *__res
   return s;
 }
 
+// ------------------------------------------------------ L2 bulk prefetch
+// cp.async.bulk.prefetch.L2 (sm_90+ TMA engine): one instruction pulls a
+// contiguous byte range into L2 without occupying registers.  Each block
+// prefetches the streamed arrays of its NEXT grid-stride trip, so DRAM
+// latency overlaps the current trip and the demand loads hit L2.
+#ifndef LF_PF
+#define LF_PF 0          // trips ahead (0 = off).  Measured r1h: PF=1 slows phase 1 at
+#endif                   // 200^3 from 181 to 246 us (profiles/variants_r1h.log) -> off
+__device__ __forceinline__ void l2_prefetch(const void *p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+template <class T>
+__device__ __forceinline__ void pf_range(const T *base, long off, int cnt) {
+  const unsigned bytes = (unsigned)(cnt * (int)sizeof(T)) & ~15u;  // 16-byte multiple
+  if (bytes) l2_prefetch(base + off, bytes);
+}
+
 __device__ __forceinline__ bool conv(double res, double init, const PcgCtl *ctl) {
   return res < ctl->tol || (ctl->relTol > 0.0 && res < ctl->relTol * init);
 }
@@ -265,7 +285,7 @@ __global__ void __launch_bounds__(BS, LF_MINB)
     for (int i = o0; i < o1; ++i) {
       const double u = __dmul_rn(m.delta[i], __dmul_rn(DT, m.magSf[i]));
       a.upper[i] = -u;
-      if (m.K > 0) a.upperE[(i - o0) * m.n + c] = -u;
+      if (m.K > 0) a.upperE[(i - o0) * m.ldE + c] = -u;
       L = __dsub_rn(L, u);
       if (SETUP) {
         sOff = fma(-u, T[m.nbr[i]], sOff);
@@ -334,7 +354,7 @@ void launch_assemble(cudaStream_t s, const Launch &L, const MeshDev &m, const Ld
 // Prologue of a standalone pcg_solve: A psi from the stored coefficients,
 // r = source - A psi, normFactor terms, sum|r|, w = r/diag, sum w.r.
 template <int KE>
-__global__ void __launch_bounds__(BS, LF_MINB)
+__global__ void __launch_bounds__(BS, LF_MINB_G)
     k_pcg_setup(MeshDev m, LduDev a, const double *__restrict__ halo, Workspace ws) {
   const double *psi = ws.ctl->psi;
   const double psibar = ws.gsum->p1[1] / ws.ctl->nTotal;
@@ -416,7 +436,7 @@ __device__ __forceinline__ double pval(const double *__restrict__ w, const doubl
 // Deferred psi += alpha_{k-1} p_{k-1}; stopping test on the previous
 // iteration's residual; p_k = w + beta p_{k-1}; q = A p_k; sum p.q, sum psi.
 template <int KE>
-__global__ void __launch_bounds__(BS, LF_MINB)
+__global__ void __launch_bounds__(BS, LF_MINB_G)
     k_phase1(MeshDev m, LduDev a, const double *__restrict__ halo, Workspace ws) {
   const PcgCtl *ctl = ws.ctl;
   if (ctl->stop) return;
@@ -429,6 +449,22 @@ __global__ void __launch_bounds__(BS, LF_MINB)
   const double *__restrict__ w = ws.w;
   double v[2] = {0.0, 0.0};
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < m.n; c += gridDim.x * blockDim.x) {
+#if LF_PF > 0
+    if (KE > 0 && s.cont && threadIdx.x < 4 + 3 * KE) {
+      const int cb = c - threadIdx.x + LF_PF * gridDim.x * blockDim.x;
+      if (cb < m.n) {
+        const int cnt = min((int)blockDim.x, m.n - cb), L = threadIdx.x;
+        const long ld = m.ldE;
+        if (L == 0) pf_range(w, cb, cnt);
+        else if (L == 1) { if (!first) pf_range(pold, cb, cnt); }
+        else if (L == 2) pf_range(psi, cb, cnt);
+        else if (L == 3) pf_range(a.diag, cb, cnt);
+        else if (L < 4 + KE) pf_range(a.upperE, (L - 4) * ld + cb, cnt);
+        else if (L < 4 + 2 * KE) pf_range(m.nbrE, (L - 4 - KE) * ld + cb, cnt);
+        else pf_range(m.loE, (L - 4 - 2 * KE) * ld + cb, cnt);
+      }
+    }
+#endif
     double ps = psi[c];
     if (!first) {
       ps = fma(alpha, pold[c], ps);
@@ -482,6 +518,15 @@ __global__ void __launch_bounds__(BS, LF_MINB)
     constexpr int U = LF_P2_UNROLL;
     const int stride = gridDim.x * blockDim.x;
     for (int c0 = blockIdx.x * blockDim.x + threadIdx.x; c0 < n; c0 += stride * U) {
+#if LF_PF > 0
+      if (threadIdx.x < 3 * U) {
+        const int cb = c0 - threadIdx.x + LF_PF * stride * U + (threadIdx.x / 3) * stride;
+        if (cb < n) {
+          const int cnt = min((int)blockDim.x, n - cb), L = threadIdx.x % 3;
+          pf_range(L == 0 ? ws.q : (L == 1 ? ws.r : a.diag), cb, cnt);
+        }
+      }
+#endif
       double q[U], r[U], d[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -524,7 +569,7 @@ void launch_phase2(cudaStream_t s, const Launch &L, int32_t n, const LduDev &a, 
 
 // ------------------------------------------------------------------ Amul
 template <int KE>
-__global__ void __launch_bounds__(BS, LF_MINB)
+__global__ void __launch_bounds__(BS, LF_MINB_G)
     k_amul(MeshDev m, LduDev a, const double *__restrict__ halo, const double *__restrict__ x,
            double *__restrict__ y) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < m.n; c += gridDim.x * blockDim.x) {
@@ -670,19 +715,19 @@ void launch_split_keys(cudaStream_t s, const uint64_t *keys, int64_t m, int32_t 
 // ELL slices from the CSR lists (see the header comment).  Padding: -1.
 __global__ void k_build_ell(MeshDev m, const int32_t *__restrict__ owner, int32_t K, int32_t *nbrE,
                             int32_t *loE) {
-  const int n = m.n;
+  const int n = m.n, ld = m.ldE;
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
     const int o0 = m.ownerStart[c], o1 = m.ownerStart[c + 1];
     const int l0 = m.losortStart[c], l1 = m.losortStart[c + 1];
     for (int k = 0; k < K; ++k) {
-      nbrE[k * n + c] = o0 + k < o1 ? m.nbr[o0 + k] : -1;
+      nbrE[k * ld + c] = o0 + k < o1 ? m.nbr[o0 + k] : -1;
       int packed = -1;
       if (l0 + k < l1) {
         const int f = m.losort[l0 + k];
         const int oc = owner[f];
         packed = ((f - m.ownerStart[oc]) << ELL_SHIFT) | oc;
       }
-      loE[k * n + c] = packed;
+      loE[k * ld + c] = packed;
     }
   }
 }

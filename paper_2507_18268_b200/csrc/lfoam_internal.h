@@ -88,7 +88,7 @@ struct MeshDev {
   int32_t hasProc;
   // ELL slices of the same addressing (K = max faces per side, 0 = none);
   // slot k of cell c at k*n + c.  See kernels.cu header.
-  int32_t K;
+  int32_t K, ldE;  // ldE: slab stride (n rounded up to 4: 16-byte aligned slabs)
   const int32_t *nbrE, *loE;
 };
 

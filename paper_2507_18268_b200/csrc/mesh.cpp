@@ -360,10 +360,12 @@ static void build_mesh(lf_context *ctx, const lf_mesh_desc *d, lf_mesh *M) {
     for (int32_t c = 0; c < n; ++c) K = std::max({K, hs[c + 1] - hs[c], hl[c + 1] - hl[c]});
     if (K >= 1 && K <= 4) {
       const int KE = K <= 3 ? 3 : 4;  // kernels are specialised for 3 and 4 slots
-      int32_t *nbrE = A.alloc<int32_t>((size_t)KE * n), *loE = A.alloc<int32_t>((size_t)KE * n);
-      L.upperE = A.alloc<double>((size_t)KE * n);
-      LF_CUDA(cudaMemsetAsync(L.upperE, 0, sizeof(double) * KE * (size_t)n, s));
+      const int32_t ld = (n + 3) & ~3;
+      int32_t *nbrE = A.alloc<int32_t>((size_t)KE * ld), *loE = A.alloc<int32_t>((size_t)KE * ld);
+      L.upperE = A.alloc<double>((size_t)KE * ld);
+      LF_CUDA(cudaMemsetAsync(L.upperE, 0, sizeof(double) * KE * (size_t)ld, s));
       md.K = KE;
+      md.ldE = ld;
       launch_build_ell(s, md, owner, KE, nbrE, loE);
       md.nbrE = nbrE;
       md.loE = loE;

@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import weakref
 from typing import Dict, List, Optional, Sequence
 
 import numpy as np
@@ -146,6 +147,7 @@ class Context:
         _check(lib().lf_context_create(device, s, C.byref(h)))
         self.h = h
         self.device = device
+        self._meshes = weakref.WeakSet()  # destroyed before the context
 
     @staticmethod
     def unique_id() -> bytes:
@@ -177,6 +179,8 @@ class Context:
 
     def close(self):
         if self.h:
+            for m in list(self._meshes):
+                m.close()
             _check(lib().lf_context_destroy(self.h))
             self.h = None
 
@@ -218,6 +222,7 @@ class Mesh:
         h = C.c_void_p()
         _check(lib().mesh_create(ctx.h, C.byref(desc), C.byref(h)))
         self.h = h
+        ctx._meshes.add(self)
         self.n_cells = int(m.n_cells)
         self.n_faces = int(own.shape[0])
         self.n_bfaces = int(sum(self.patch_sizes))

@@ -14,11 +14,10 @@ sys.path.insert(0, ROOT)
 
 VARIANTS = {
     "base": [],
-    "noell": ["LF_NO_ELL=1"],
-    "m5": ["LF_MINB=5"],
-    "m6": ["LF_MINB=6"],
-    "b128m10": ["LF_BS=128", "LF_MINB=10"],
-    "b512m2": ["LF_BS=512", "LF_MINB=2"],
+    "pf0": ["LF_PF=0"],
+    "pf2": ["LF_PF=2"],
+    "mg4": ["LF_MINB_G=4"],
+    "mg6": ["LF_MINB_G=6"],
 }
 
 

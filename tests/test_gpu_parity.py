@@ -276,8 +276,42 @@ def test_config2_full_run_closed_form(ctx, canonical_constants):
     assert np.max(np.abs(T - ref)) <= 1e-8 * np.max(np.abs(ref))
     its = [p["n_iterations"] for p in pg]
     assert all(p["converged"] for p in pg)
-    assert 90 <= min(its) and max(its) <= 104, its   # SCRATCH 96-97 (indicative)
+    assert 90 <= min(its) and max(its) <= 130, its   # SCRATCH 96-97 early on (indicative)
     mesh.close()
+
+
+@pytest.mark.slow
+def test_config2_full_run_vs_oracle(ctx):
+    """Config 2 exactly as bench.py times it (100^3, 100 steps, canonical
+    field) against the oracle: every cell and every step's iteration count."""
+    m = meshgen.block_mesh(100)
+    s = meshgen.canonical_field(m)
+    To, _, po = oracle.laplacian_foam(m, s, 100)
+    mesh = P.Mesh(ctx, m)
+    mesh.set_T(s)
+    pg = mesh.step(100)
+    T = mesh.get_T()
+    assert np.max(np.abs(T - To)) <= 1e-8 * np.max(np.abs(To))
+    check_iterations(pg, po, tol=1e-10)
+    mesh.close()
+
+
+def check_iterations(pg, po, tol):
+    """Iterations within +-1 per step, except criterion flips: OpenFOAM's L1
+    residual is not monotone in CG, so when one side stops with a residual
+    within 10% below tol the other side may need to ride out a bump
+    (observed 97 vs 109 at 100^3).  Such a step and the one after it (which
+    starts from a slightly different T) are exempt; totals must agree to 2%."""
+    flip = [max(a["final_residual"], b["final_residual"]) >= 0.9 * tol for a, b in zip(pg, po)]
+    bad = []
+    for i, (a, b) in enumerate(zip(pg, po)):
+        exempt = flip[i] or (i > 0 and flip[i - 1])
+        if abs(a["n_iterations"] - b["n_iterations"]) > 1 and not exempt:
+            bad.append((i, a["n_iterations"], b["n_iterations"]))
+    assert not bad, bad
+    tg = sum(p["n_iterations"] for p in pg)
+    to = sum(p["n_iterations"] for p in po)
+    assert abs(tg - to) <= max(2, 0.02 * to), (tg, to)
 
 
 def test_determinism_bitwise(ctx):
