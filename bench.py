@@ -43,6 +43,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=0, help="oracle steps for cpu_baseline (0 = auto)")
+    ap.add_argument("--mode", default="persistent", choices=["persistent", "graphs", "direct"],
+                    help="PCG loop execution (single rank): one cooperative launch per solve, "
+                         "CUDA-graph replays of per-phase launches, or direct launches")
     return ap.parse_args()
 
 
@@ -172,6 +175,8 @@ def run_ours(args):
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     ctx = P.Context(local, stream=stream)
+    ctx.set_option("persistent", args.mode == "persistent")
+    ctx.set_option("graphs", args.mode != "direct")
 
     cfg = args.config
     gmesh = meshgen.config_mesh(cfg)
@@ -234,12 +239,23 @@ def run_ours(args):
     n_p1, ms_p1 = ctx.kernel_stats("phase1")
     n_p2, ms_p2 = ctx.kernel_stats("phase2")
     n_as, ms_as = ctx.kernel_stats("assemble")
+    n_pcg, ms_pcg = ctx.kernel_stats("pcg")
     iters = sum(p["n_iterations"] for p in perfs_i)
     bytes_p1 = 56 * n_local + 16 * F_local          # per full phase-1 launch
     bytes_p2 = 40 * n_local
     peak, peak_kind = measured_peak()
-    achieved = bytes_p1 * iters / (ms_p1 / 1e3) / 1e9 if ms_p1 > 0 else None
-    traffic = ncu_traffic(cfg, "k_phase1") if ws == 1 else None
+    if n_pcg > 0:
+        # persistent whole-solve kernel: per launch = its iterations x (96n + 16F)
+        # + the final flush pass (psi, p_old read, psi written: 24n)
+        kernel = "k_pcg_persistent"
+        total_bytes = iters * (bytes_p1 + bytes_p2) + n_pcg * 24 * n_local
+        k_launches, k_ms = n_pcg, ms_pcg
+    else:
+        kernel = "k_phase1"
+        total_bytes = bytes_p1 * iters
+        k_launches, k_ms = n_p1, ms_p1
+    achieved = total_bytes / (k_ms / 1e3) / 1e9 if k_ms > 0 else None
+    traffic = ncu_traffic(cfg, kernel) if ws == 1 else None
 
     # e2e through the public API with host buffers (pinned), copies inside the region
     T0h = torch.from_numpy(np.ascontiguousarray(T0)).pin_memory()
@@ -284,12 +300,16 @@ def run_ours(args):
                    "global_batch": 1, "seq_len": 0, "parallelism": f"dp{ws}" if ws == 1 else f"domain{ws}",
                    "l2": "flushed between timed steps (256 MiB write)", "tol": TOL,
                    "pcg_iterations_per_step": {"min": min(its), "max": max(its), "mean": sum(its) / len(its)}},
-        "roofline": {"bound": "hbm", "kernel": "k_phase1", "achieved": achieved, "peak": peak,
+        "roofline": {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None,
-                     "traffic": traffic, "bytes_per_launch": bytes_p1, "launches": n_p1,
-                     "avg_launch_ms": ms_p1 / max(n_p1, 1),
-                     "share_of_step": ms_p1 / inst_ms if inst_ms > 0 else None,
+                     "traffic": traffic, "bytes_per_launch": total_bytes / max(k_launches, 1),
+                     "launches": k_launches,
+                     "avg_launch_ms": k_ms / max(k_launches, 1),
+                     "share_of_step": k_ms / inst_ms if inst_ms > 0 else None,
+                     "mode": args.mode,
+                     "phase1": {"achieved": bytes_p1 * iters / (ms_p1 / 1e3) / 1e9 if ms_p1 > 0 else None,
+                                "avg_launch_ms": ms_p1 / max(n_p1, 1), "share_of_step": ms_p1 / inst_ms},
                      "phase2": {"achieved": bytes_p2 * iters / (ms_p2 / 1e3) / 1e9 if ms_p2 > 0 else None,
                                 "avg_launch_ms": ms_p2 / max(n_p2, 1), "share_of_step": ms_p2 / inst_ms},
                      "assemble": {"avg_launch_ms": ms_as / max(n_as, 1), "share_of_step": ms_as / inst_ms},

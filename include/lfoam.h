@@ -207,8 +207,20 @@ LF_API lf_status laplacianFoam_step(lf_mesh *mesh, const lf_laplacian_params *p,
 /* Kernel kinds for lf_kernel_stats. */
 typedef enum {
   LF_K_ASSEMBLE = 0, LF_K_SETUP = 1, LF_K_PHASE1 = 2, LF_K_PHASE2 = 3,
-  LF_K_AMUL = 4, LF_K_SUMPSI = 5, LF_K_PACK = 6, LF_K_COUNT = 7
+  LF_K_AMUL = 4, LF_K_SUMPSI = 5, LF_K_PACK = 6,
+  LF_K_PCG = 7,      /* persistent whole-solve kernel (single rank, no processor patches) */
+  LF_K_COUNT = 8
 } lf_kernel_kind;
+
+/* Execution options of a context (all default 1):
+ *   LF_OPT_PERSISTENT  single-rank meshes without processor patches run the
+ *                      whole PCG loop as ONE cooperative launch (grid
+ *                      barriers between the phases); 0 = one launch per phase
+ *   LF_OPT_GRAPHS      phase launches are replayed from CUDA graphs of 2^i
+ *                      iterations; 0 = direct launches
+ * Results are identical up to reduction grid size (both are deterministic). */
+typedef enum { LF_OPT_PERSISTENT = 0, LF_OPT_GRAPHS = 1 } lf_option;
+LF_API lf_status lf_set_option(lf_context *ctx, lf_option opt, int value);
 
 /* enable != 0: bracket every launch of the hot kernels with CUDA events on
  * the context stream and accumulate their durations (timings are read back

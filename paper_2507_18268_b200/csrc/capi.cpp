@@ -405,6 +405,18 @@ lf_status lf_kernel_stats(const lf_context *ctx, lf_kernel_kind k, int64_t *laun
   });
 }
 
+lf_status lf_set_option(lf_context *ctx, lf_option opt, int value) {
+  return guard([&] {
+    LF_REQUIRE(ctx != nullptr, "ctx is NULL");
+    if (opt == LF_OPT_PERSISTENT)
+      ctx->persistent = value != 0;
+    else if (opt == LF_OPT_GRAPHS)
+      ctx->useGraphs = value != 0;
+    else
+      throw Error{LF_ERR_INVALID_ARG, "unknown option"};
+  });
+}
+
 lf_status lf_launch_count(const lf_context *ctx, int64_t *n) {
   return guard([&] {
     LF_REQUIRE(ctx && n, "NULL argument");

@@ -36,6 +36,7 @@ struct lf_context {
   bool instrument = false;
   bool capturing = false;  // stream capture in progress: no events, no counting
   bool useGraphs = true;   // replay iteration chunks as CUDA graphs
+  bool persistent = true;  // single-rank, no processor patches: one cooperative launch per solve
   struct Pending {
     int kind;
     cudaEvent_t a, b;
@@ -94,6 +95,8 @@ struct lf_mesh {
   static constexpr int kMaxGraphLog = 8;
   cudaGraphExec_t chunkGraph[kMaxGraphLog] = {};
   int kernelsPerIteration = 0;
+  int persistentGrid = 0;     // co-resident grid of k_pcg_persistent
+  unsigned *gridBar = nullptr;  // device {count, generation}
   ~lf_mesh();
 };
 

@@ -567,6 +567,271 @@ void launch_phase2(cudaStream_t s, const Launch &L, int32_t n, const LduDev &a, 
   k_phase2<<<L.grid, BS, 0, s>>>(n, a, ws);
 }
 
+// ------------------------------------------------- persistent PCG (1 GPU)
+// The whole solve in ONE cooperative launch (resident grid, all blocks
+// co-scheduled): the two phases of every iteration are separated by grid
+// barriers instead of kernel boundaries.  At a barrier each block publishes
+// its partial sums; the last block to arrive (integer ticket) sums them in
+// block order (same order as reduce_grid: results bitwise equal to the
+// launch-per-phase path for the same grid), publishes the totals and
+// releases the barrier.  Scalars (alpha, beta, stopping rule) live in
+// registers, identical in every block.  Data written by other blocks during
+// the launch (w, p at neighbour cells, the totals) is read with ld.global.cg
+// (L2) because L1 is not coherent within a launch; everything else is
+// either read-only or written and re-read by the same thread.
+#ifndef LF_PERSIST_LDCG
+#define LF_PERSIST_LDCG 0  // 1: neighbour reads via ld.cg instead of L1 invalidation at barriers
+#endif
+__device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <int NV>
+__device__ void grid_reduce_sync(double (&v)[NV], double *partials, unsigned *bar, double *out) {
+  __shared__ double sm[NV][32];
+  __shared__ int amLast;
+  block_sum<NV>(v, sm);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) partials[k * gridDim.x + blockIdx.x] = v[k];
+    const unsigned gen = ld_acquire(bar + 1);  // read before arriving: cannot move until we arrive
+    __threadfence();
+    const unsigned t = atomicAdd(bar, 1u);
+    amLast = (t == gridDim.x - 1);
+    if (!amLast) {
+      // ld.acquire.gpu orders the later loads and invalidates this SM's L1
+      // (SASS CCTL.IVALL), so cached loads of other blocks' data are coherent
+      while (ld_acquire(bar + 1) == gen) __nanosleep(32);
+    }
+  }
+  __syncthreads();
+  if (amLast) {
+    __threadfence();
+    double s[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) s[k] = 0.0;
+    constexpr int U = 4;
+    for (int b0 = threadIdx.x; b0 < (int)gridDim.x; b0 += blockDim.x * U) {
+      double t[U][NV];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int b = b0 + u * blockDim.x;
+#pragma unroll
+        for (int k = 0; k < NV; ++k) t[u][k] = b < (int)gridDim.x ? __ldcg(&partials[k * gridDim.x + b]) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int k = 0; k < NV; ++k) s[k] += t[u][k];
+    }
+    block_sum<NV>(s, sm);
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int k = 0; k < NV; ++k) out[k] = s[k];
+      bar[0] = 0u;
+      __threadfence();
+      atomicAdd(bar + 1, 1u);  // release
+    }
+    __syncthreads();
+  }
+}
+
+#ifndef LF_MINB_P
+#define LF_MINB_P 5  // persistent kernel blocks/SM (r1k: 5 beats 4 and 6 at 200^3)
+#endif
+#ifndef LF_P1_PIPE
+#define LF_P1_PIPE 0  // software-pipelined phase 1 (next trip's loads in flight)
+#endif
+#ifndef LF_P2P_UNROLL
+#define LF_P2P_UNROLL 2  // persistent phase 2 cells per trip
+#endif
+template <int KE>
+__global__ void __launch_bounds__(BS, LF_MINB_P)
+    k_pcg_persistent(MeshDev m, LduDev a, Workspace ws, unsigned *bar) {
+  PcgCtl *ctl = ws.ctl;
+  if (ctl->stop) return;
+  int k = ctl->it;
+  double nf = ctl->normFactor, initRes = ctl->initRes, finRes = ctl->finRes;
+  double wArA = ctl->wArA, alpha = ctl->alpha;
+  double *psi = ctl->psi;
+  const double *__restrict__ w = ws.w;
+  bool cont = false, singular = false;
+  const int stride = gridDim.x * blockDim.x;
+  for (;;) {
+    // ---- derive (OpenFOAM loop condition) from the previous totals
+    double beta = 0.0;
+    if (k == 0) {
+      nf = __ldcg(&ws.gsum->setup[0]) + 1e-20;
+      initRes = __ldcg(&ws.gsum->setup[1]) / nf;
+      finRes = initRes;
+      cont = ctl->minIter > 0 || !conv(finRes, initRes, ctl);
+      wArA = __ldcg(&ws.gsum->setup[2]);
+    } else {
+      finRes = __ldcg(&ws.gsum->p2[0]) / nf;
+      cont = (k < ctl->maxIter && !conv(finRes, initRes, ctl)) || k < ctl->minIter;
+      const double wn = __ldcg(&ws.gsum->p2[1]);
+      beta = wn / wArA;
+      wArA = wn;
+    }
+    const bool first = (k == 0);
+    const double *__restrict__ pold = (k & 1) ? ws.p[0] : ws.p[1];
+    double *__restrict__ pnew = (k & 1) ? ws.p[1] : ws.p[0];
+    auto pnb = [&](int j) {  // p at a neighbour cell (written by another block)
+#if LF_PERSIST_LDCG
+      return first ? __ldcg(w + j) : fma(beta, __ldcg(pold + j), __ldcg(w + j));
+#else  // L1 was invalidated by the post-barrier gpu-scope fence: cached loads are coherent
+      return first ? w[j] : fma(beta, pold[j], w[j]);
+#endif
+    };
+    // ---- phase 1: flush psi, p = w + beta p_old, q = A p, sums
+    double v1[2] = {0.0, 0.0};
+#if LF_P1_PIPE
+    if constexpr (KE > 0) {
+      if (cont) {
+        // software pipeline: the own-cell vectors and ELL slots of the NEXT
+        // trip are loaded while the current trip's gathers are in flight
+        struct Row {
+          double w, po, ps, dg, uo[KE];
+          int lo[KE], nb[KE];
+        };
+        const int ld = m.ldE;
+        auto load_row = [&](int c, Row &R) {
+          R.w = w[c];
+          R.po = first ? 0.0 : pold[c];
+          R.ps = psi[c];
+          R.dg = a.diag[c];
+#pragma unroll
+          for (int kk = 0; kk < KE; ++kk) {
+            R.lo[kk] = __ldg(m.loE + kk * ld + c);
+            R.nb[kk] = __ldg(m.nbrE + kk * ld + c);
+            R.uo[kk] = a.upperE[kk * ld + c];
+          }
+        };
+        int c = blockIdx.x * blockDim.x + threadIdx.x;
+        Row cur;
+        if (c < m.n) load_row(c, cur);
+        for (; c < m.n; c += stride) {
+          Row nxt;
+          if (c + stride < m.n) load_row(c + stride, nxt);
+          double ps = cur.ps;
+          if (!first) {
+            ps = fma(alpha, cur.po, ps);
+            psi[c] = ps;
+          }
+          v1[1] += ps;
+          const double pc = first ? cur.w : fma(beta, cur.po, cur.w);
+          pnew[c] = pc;
+          double lu[KE], lx[KE], ox[KE];
+#pragma unroll
+          for (int kk = 0; kk < KE; ++kk) {
+            const int oc = cur.lo[kk] & ELL_MASK;
+            lu[kk] = cur.lo[kk] >= 0 ? a.upperE[(cur.lo[kk] >> ELL_SHIFT) * ld + oc] : 0.0;
+            lx[kk] = cur.lo[kk] >= 0 ? pnb(oc) : 0.0;
+            ox[kk] = cur.nb[kk] >= 0 ? pnb(cur.nb[kk]) : 0.0;
+          }
+          double q = cur.dg * pc;
+#pragma unroll
+          for (int kk = 0; kk < KE; ++kk)
+            if (cur.lo[kk] >= 0) q = fma(lu[kk], lx[kk], q);
+#pragma unroll
+          for (int kk = 0; kk < KE; ++kk)
+            if (cur.nb[kk] >= 0) q = fma(cur.uo[kk], ox[kk], q);
+          ws.q[c] = q;
+          v1[0] = fma(pc, q, v1[0]);
+          cur = nxt;
+        }
+      }
+    }
+    if (KE == 0 || !cont)
+#endif
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < m.n; c += stride) {
+      double ps = psi[c];
+      if (!first) {
+        ps = fma(alpha, pold[c], ps);
+        psi[c] = ps;
+      }
+      v1[1] += ps;
+      if (cont) {
+        const double pc = first ? w[c] : fma(beta, pold[c], w[c]);
+        pnew[c] = pc;
+        double q = a.diag[c] * pc;
+        q = row_offdiag<KE>(m, a, c, q, pnb);
+        ws.q[c] = q;
+        v1[0] = fma(pc, q, v1[0]);
+      }
+    }
+    grid_reduce_sync<2>(v1, ws.partials, bar, ws.gsum->p1);
+    if (!cont) break;
+    // ---- phase 2: singularity, alpha, r -= alpha q, w = r/diag, sums
+    const double pq = __ldcg(&ws.gsum->p1[0]);
+    if (fabs(pq) / nf < 1e-300) {
+      singular = true;
+      break;
+    }
+    alpha = wArA / pq;
+    double v2[2] = {0.0, 0.0};
+    {
+      constexpr int U = LF_P2P_UNROLL;  // cells per trip, loads issued first
+      for (int c0 = blockIdx.x * blockDim.x + threadIdx.x; c0 < m.n; c0 += stride * U) {
+        double q[U], r[U], d[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int c = c0 + u * stride;
+          const bool ok = c < m.n;
+          q[u] = ok ? ws.q[c] : 0.0;
+          r[u] = ok ? ws.r[c] : 0.0;
+          d[u] = ok ? a.diag[c] : 1.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int c = c0 + u * stride;
+          if (c < m.n) {
+            const double rn = fma(-alpha, q[u], r[u]);
+            const double wc = (1.0 / d[u]) * rn;
+            ws.r[c] = rn;
+            ws.w[c] = wc;
+            v2[0] += fabs(rn);
+            v2[1] = fma(wc, rn, v2[1]);
+          }
+        }
+      }
+    }
+    grid_reduce_sync<2>(v2, ws.partials, bar, ws.gsum->p2);
+    ++k;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    ctl->it = k;
+    ctl->stop = 1;
+    ctl->singular = singular ? 1 : 0;
+    ctl->converged = conv(finRes, initRes, ctl) ? 1 : 0;
+    ctl->normFactor = nf;
+    ctl->initRes = initRes;
+    ctl->finRes = finRes;
+    ctl->wArA = wArA;
+    ctl->alpha = alpha;
+  }
+}
+
+int persistent_grid(int device, int K) {
+  int sms = 0, nb = 0;
+  LF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  const void *fn = K == 4 ? (const void *)k_pcg_persistent<4>
+                          : (K > 0 ? (const void *)k_pcg_persistent<3> : (const void *)k_pcg_persistent<0>);
+  LF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, BS, 0));
+  return sms * (nb < 1 ? 1 : nb);
+}
+
+void launch_pcg_persistent(cudaStream_t s, int grid, const MeshDev &m, const LduDev &a,
+                           const Workspace &ws, unsigned *bar) {
+  void *args[] = {(void *)&m, (void *)&a, (void *)&ws, (void *)&bar};
+  const void *fn = (!LF_NO_ELL && m.K == 4) ? (const void *)k_pcg_persistent<4>
+                   : (!LF_NO_ELL && m.K > 0) ? (const void *)k_pcg_persistent<3>
+                                             : (const void *)k_pcg_persistent<0>;
+  LF_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(BS), args, 0, s));
+}
+
 // ------------------------------------------------------------------ Amul
 template <int KE>
 __global__ void __launch_bounds__(BS, LF_MINB_G)

@@ -129,7 +129,15 @@ static void run_iterations(lf_mesh *M, lf_solver_perf *out) {
   const int64_t bound = (int64_t)std::max(maxIter, minIter) + 2;
   int64_t launched = 0;
   int chunk = M->lastIters >= 0 ? M->lastIters + 1 : 8;
-  for (;;) {
+  if (ctx->persistent && !ctx->comm && M->nproc == 0) {
+    // single rank, no halo: the whole loop in one cooperative launch
+    ctx->launch(LF_K_PCG, [&] { launch_pcg_persistent(s, M->persistentGrid, M->md, M->ld, M->ws, M->gridBar); });
+    LF_CUDA(cudaMemcpyAsync(M->hctl, M->ws.ctl, sizeof(PcgCtl), cudaMemcpyDeviceToHost, s));
+    LF_CUDA(cudaStreamSynchronize(s));
+    ctx->harvest();
+    chunk = 0;  // skip the chunked loop
+  }
+  for (; chunk > 0;) {
     chunk = (int)std::max<int64_t>(1, std::min<int64_t>(chunk, bound + 1 - launched));
     enqueue_iterations(M, chunk);
     launched += chunk;

@@ -23,7 +23,8 @@ STATUS = {0: "LF_OK", 1: "LF_ERR_INVALID_ARG", 2: "LF_ERR_STATE", 3: "LF_ERR_OOM
           4: "LF_ERR_CUDA", 5: "LF_ERR_NCCL", 6: "LF_ERR_INTERNAL"}
 PATCH_TYPES = {"fixedValue": 0, "zeroGradient": 1, "processor": 2}
 FIELD_T, FIELD_PATCH_VALUE = 0, 1
-KERNELS = {"assemble": 0, "setup": 1, "phase1": 2, "phase2": 3, "amul": 4, "sumpsi": 5, "pack": 6}
+KERNELS = {"assemble": 0, "setup": 1, "phase1": 2, "phase2": 3, "amul": 4, "sumpsi": 5, "pack": 6, "pcg": 7}
+OPTIONS = {"persistent": 0, "graphs": 1}
 
 
 class LfoamError(RuntimeError):
@@ -90,6 +91,7 @@ SIGNATURES = {
     "lf_set_instrumentation": (C.c_int, [_vp, C.c_int]),
     "lf_kernel_stats": (C.c_int, [_vp, C.c_int, C.POINTER(_i64), C.POINTER(_d)]),
     "lf_launch_count": (C.c_int, [_vp, C.POINTER(_i64)]),
+    "lf_set_option": (C.c_int, [_vp, C.c_int, C.c_int]),
 }
 
 _lib = None
@@ -163,6 +165,9 @@ class Context:
         n, r = C.c_int(), C.c_int()
         _check(lib().lf_comm_info(self.h, C.byref(n), C.byref(r)))
         return n.value, r.value
+
+    def set_option(self, name: str, value: bool):
+        _check(lib().lf_set_option(self.h, OPTIONS[name], 1 if value else 0))
 
     def set_instrumentation(self, on: bool):
         _check(lib().lf_set_instrumentation(self.h, 1 if on else 0))

@@ -12,29 +12,47 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
+# name -> (-D defines, bench --mode)
 VARIANTS = {
-    "base": [],
-    "pf0": ["LF_PF=0"],
-    "pf2": ["LF_PF=2"],
-    "mg4": ["LF_MINB_G=4"],
-    "mg6": ["LF_MINB_G=6"],
+    "persist": ([], "persistent"),
+    "graphs": ([], "graphs"),
+    "p_u1": (["LF_P2P_UNROLL=1"], "persistent"),
+    "p_pipe_m3": (["LF_P1_PIPE=1", "LF_MINB_P=3"], "persistent"),
+    "p_pipe_m4": (["LF_P1_PIPE=1", "LF_MINB_P=4"], "persistent"),
+    "p_pipe_m5": (["LF_P1_PIPE=1", "LF_MINB_P=5"], "persistent"),
 }
+
+
+def libname(name):
+    return f"liblfoam_{name}.so"
 
 
 def build():
     from paper_2507_18268_b200 import build as B
-    for name, defs in VARIANTS.items():
-        print(name, B.build(force=True, defines=defs or ["LF_VARIANT_BASE=1"], out=f"liblfoam_{name}.so"), flush=True)
+    built = {}
+    for name, (defs, _) in VARIANTS.items():
+        key = tuple(defs)
+        if key in built:  # same defines: reuse
+            continue
+        built[key] = B.build(force=True, defines=list(defs) or ["LF_VARIANT_BASE=1"], out=libname(name))
+        print(name, built[key], flush=True)
 
 
-def run(cfgs):
+def lib_for(name):
+    defs = tuple(VARIANTS[name][0])
+    for other, (d, _) in VARIANTS.items():
+        if tuple(d) == defs:
+            return libname(other)
+
+
+def run(cfgs, steps=10):
     rows = []
     for cfg in cfgs:
-        for name in VARIANTS:
-            env = dict(os.environ, LFOAM_LIB=f"liblfoam_{name}.so")
-            r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "10", "--warmup", "3",
-                                "--config", str(cfg), "--no-cpu-baseline"], capture_output=True, text=True, env=env,
-                               timeout=900)
+        for name, (_, mode) in VARIANTS.items():
+            env = dict(os.environ, LFOAM_LIB=lib_for(name))
+            r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", str(steps), "--warmup", "3",
+                                "--config", str(cfg), "--no-cpu-baseline", "--mode", mode],
+                               capture_output=True, text=True, env=env, timeout=1800)
             line = [l for l in r.stdout.splitlines() if l.startswith("{")]
             if not line:
                 print(name, cfg, "FAILED", r.stderr[-2000:], flush=True)
@@ -42,11 +60,11 @@ def run(cfgs):
             d = json.loads(line[-1])
             rf = d["roofline"]
             row = dict(variant=name, cfg=cfg, ms_step=round(d["ms_per_step"], 3), value=f"{d['value']:.3e}",
-                       it=d["config"]["pcg_iterations_per_step"]["mean"],
-                       p1_us=round(rf["avg_launch_ms"] * 1e3, 2), p1_GBs=round(rf["achieved"] or 0),
-                       p2_us=round(rf["phase2"]["avg_launch_ms"] * 1e3, 2),
-                       p2_GBs=round(rf["phase2"]["achieved"] or 0),
-                       inst_ms=round(rf["instrumented_ms_per_step"], 3))
+                       it=d["config"]["pcg_iterations_per_step"]["mean"], kernel=rf["kernel"],
+                       k_us=round(rf["avg_launch_ms"] * 1e3, 2), k_GBs=round(rf["achieved"] or 0),
+                       frac=round(rf["frac"] or 0, 3),
+                       p1_us=round(rf["phase1"]["avg_launch_ms"] * 1e3, 2), p2_us=round(rf["phase2"]["avg_launch_ms"] * 1e3, 2),
+                       inst_ms=round(rf["instrumented_ms_per_step"], 3), e2e=f"{d['e2e']['value']:.3e}")
             rows.append(row)
             print(json.dumps(row), flush=True)
     return rows

@@ -314,6 +314,28 @@ def check_iterations(pg, po, tol):
     assert abs(tg - to) <= max(2, 0.02 * to), (tg, to)
 
 
+@pytest.mark.parametrize("mode", ["graphs", "direct"])
+def test_loop_modes_agree(mode):
+    """Persistent cooperative kernel vs per-phase launches (graph / direct):
+    same algorithm, different reduction grids -> equal within tolerance."""
+    import paper_2507_18268_b200 as _P
+    m = meshgen.block_mesh(24, 20, 16, bc=mixed_bc())
+    s = meshgen.multimode_field(m)
+    To, _, po = oracle.laplacian_foam(m, s, 4)
+    c = _P.Context(0)
+    c.set_option("persistent", False)
+    c.set_option("graphs", mode == "graphs")
+    mesh = _P.Mesh(c, m)
+    mesh.set_T(s)
+    pg = mesh.step(4)
+    assert np.max(np.abs(mesh.get_T() - To)) <= 1e-8 * np.max(np.abs(To))
+    assert all(abs(a["n_iterations"] - b["n_iterations"]) <= 1 for a, b in zip(pg, po))
+    n_phase1, _ = c.kernel_stats("phase1")
+    n_pcg, _ = c.kernel_stats("pcg")
+    assert n_phase1 > 0 and n_pcg == 0
+    c.close()
+
+
 def test_determinism_bitwise(ctx):
     m = meshgen.block_mesh(30)
     s = meshgen.multimode_field(m)
