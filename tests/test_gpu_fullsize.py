@@ -1,0 +1,118 @@
+"""BASELINE configs at full size, in the launch configuration bench.py times
+(-m gpu).  Where the oracle is too slow for the whole run, properties that
+hold at any size are checked: the exact discrete decay T^n = g^n T0 of the
+canonical mode, the Amul eigenvalue, and the oracle on the
+first step / on the assembled coefficients and one Amul (every cell)."""
+import math
+
+import numpy as np
+import pytest
+
+import meshgen
+import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2507_18268_b200 as _P
+    return _P
+
+
+def g_factor(N, dt=0.2, DT=1.0):
+    h = 1.0 / N
+    lam = 3 * 4 * math.sin(math.pi * h / 2) ** 2 / h ** 2
+    return 1.0 / (1.0 + dt * DT * lam), lam
+
+
+def run(P, m, T0, steps, renumber=False):
+    ctx = P.Context(0)
+    mesh = P.Mesh(ctx, m, renumber=renumber)
+    mesh.set_T(T0)
+    perfs = mesh.step(steps)
+    T = mesh.get_T()
+    ctx.close()
+    return T, perfs
+
+
+def test_config3_full_run_closed_form(P):
+    """200^3, 100 steps (BASELINE config 3, 1 GPU)."""
+    m = meshgen.block_mesh(200)
+    s = meshgen.canonical_field(m)
+    T, perfs = run(P, m, s, 100)
+    g, _ = g_factor(200)
+    ref = g ** 100 * s
+    assert np.max(np.abs(T - ref)) <= 1e-8 * np.max(np.abs(ref))
+    its = [p["n_iterations"] for p in perfs]
+    assert all(p["converged"] for p in perfs) and 175 <= min(its) and max(its) <= 230, its
+
+
+def test_config3_first_step_and_coefficients_vs_oracle(P):
+    m = meshgen.block_mesh(200)
+    s = meshgen.canonical_field(m)
+    ref = oracle.assemble(m, 1.0, 0.2, s)
+    ctx = P.Context(0)
+    mesh = P.Mesh(ctx, m)
+    mesh.set_T(s)
+    ldu = mesh.assemble(1.0, 0.2)
+    got = ldu.export()
+    for k in ("diag", "upper", "source"):
+        assert np.array_equal(got[k], ref[k]), k
+    x = meshgen.random_field(m, seed=1)
+    y_ref = oracle.amul(m, ref["diag"], ref["upper"], x)
+    xd = torch.as_tensor(x, device="cuda")
+    yd = torch.empty_like(xd)
+    ldu.amul(xd, yd)
+    scale = np.abs(ref["diag"] * x) + 6 * 0.005 * np.abs(x).max()
+    assert np.max(np.abs(yd.cpu().numpy() - y_ref) / scale) <= 1e-12
+    To, _, po = oracle.laplacian_foam(m, s, 1)
+    mesh.set_T(s)
+    pg = mesh.step(1)
+    T = mesh.get_T()
+    assert np.max(np.abs(T - To)) <= 1e-8 * np.max(np.abs(To))
+    assert abs(pg[0]["n_iterations"] - po[0]["n_iterations"]) <= 1
+    ctx.close()
+
+
+def test_config4_closed_form(P):
+    """400^3 (64M cells, BASELINE config 4) on ONE GPU: first 6 steps vs the
+    exact decay (the full 50 steps are timed by bench.py --config 4) and the
+    Amul eigenvalue at every cell."""
+    m = meshgen.block_mesh(400)
+    s = meshgen.canonical_field(m)
+    ctx = P.Context(0)
+    mesh = P.Mesh(ctx, m)
+    mesh.set_T(s)
+    ldu = mesh.assemble(1.0, 0.2)
+    g, lam = g_factor(400)
+    h = 1.0 / 400
+    sd = torch.as_tensor(meshgen.sine_field(m), device="cuda")
+    yd = torch.empty_like(sd)
+    ldu.amul(sd, yd)
+    mu = h ** 3 / 0.2 + h ** 3 * lam
+    err = (yd - mu * sd).abs() / (sd.abs() * 12 * h + 1e-300)
+    assert float(err.max()) <= 1e-12
+    del sd, yd
+    perfs = mesh.step(6)
+    T = mesh.get_T()
+    ref = g ** 6 * s
+    assert np.max(np.abs(T - ref)) <= 1e-8 * np.max(np.abs(ref))
+    assert all(p["converged"] for p in perfs)
+    ctx.close()
+
+
+@pytest.mark.parametrize("renumber", [False, True])
+def test_config5_permuted_closed_form(P, renumber):
+    """Permuted 200^3 (BASELINE config 5): raw gather stress and RCM."""
+    m = meshgen.config_mesh(5)
+    s = meshgen.canonical_field(m)
+    T, perfs = run(P, m, s, 10, renumber=renumber)
+    g, _ = g_factor(200)
+    ref = g ** 10 * s
+    assert np.max(np.abs(T - ref)) <= 1e-8 * np.max(np.abs(ref))
+    its = [p["n_iterations"] for p in perfs]
+    assert 175 <= min(its) and max(its) <= 230, its
