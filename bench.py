@@ -43,6 +43,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=0, help="oracle steps for cpu_baseline (0 = auto)")
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
+                    help="N>1 data path: peer memory (CUDA IPC over NVLink, fused into the kernels) or NCCL")
+    ap.add_argument("--renumber", type=int, default=0, help="1: RCM renumbering inside mesh_create")
     ap.add_argument("--mode", default="persistent", choices=["persistent", "graphs", "direct"],
                     help="PCG loop execution (single rank): one cooperative launch per solve, "
                          "CUDA-graph replays of per-phase launches, or direct launches")
@@ -176,14 +179,18 @@ def run_ours(args):
 
     ws, rank, local = dist_env()
     assert ws == args.gpus or ws == 1, "launch N>1 under torchrun with --gpus N"
-    torch.cuda.set_device(local)
+    # one rank per GPU; more ranks than GPUs (test only) share devices round-robin
+    device = local % torch.cuda.device_count()
+    torch.cuda.set_device(device)
     dist = None
     if ws > 1:
+        # host-side plumbing only (handles, barriers, max-over-ranks timing);
+        # the data path is the library's own transport
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group("gloo")
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
-    ctx = P.Context(local, stream=stream)
+    ctx = P.Context(device, stream=stream)
     ctx.set_option("persistent", args.mode == "persistent")
     ctx.set_option("graphs", args.mode != "direct")
 
@@ -193,16 +200,23 @@ def run_ours(args):
     T0g = meshgen.canonical_field(gmesh)
     if ws > 1:
         from paper_2507_18268_b200 import decompose
-        uid = [P.Context.unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        ctx.comm_init(uid[0], ws, rank)
+        if args.transport == "nccl":
+            uid = [P.Context.unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            ctx.comm_init(uid[0], ws, rank)
+        else:
+            ctx.p2p_init(ws, rank)
         part = decompose.slab_partition(gmesh, ws)
         m, cells = decompose.local_mesh(gmesh, part, rank)
         T0 = T0g[cells]
     else:
         m, T0 = gmesh, T0g
     del gmesh
-    mesh = P.Mesh(ctx, m)
+    mesh = P.Mesh(ctx, m, renumber=bool(args.renumber))
+    if ws > 1 and args.transport == "p2p":
+        hs = [None] * ws
+        dist.all_gather_object(hs, mesh.p2p_export())
+        mesh.p2p_connect(hs, rank)
     n_local = m.n_cells
     F_local = m.n_faces
 
@@ -234,11 +248,11 @@ def run_ours(args):
         ms = sum(a.elapsed_time(b) for a, b in ev)
         return ms, perfs
 
-    with ClockSampler(local) as clk:
+    with ClockSampler(device) as clk:
         total_ms, perfs = timed_pass(False)
     launches = ctx.launch_count()
     if dist is not None:
-        t = torch.tensor([total_ms], device="cuda")
+        t = torch.tensor([total_ms], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     value = n_global * args.steps / (total_ms / 1e3)
@@ -285,7 +299,7 @@ def run_ours(args):
     barrier()
     e2e_ms = sum(a.elapsed_time(b) for a, b in ev)
     if dist is not None:
-        t = torch.tensor([e2e_ms], device="cuda")
+        t = torch.tensor([e2e_ms], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
     e2e = n_global * args.steps / (e2e_ms / 1e3)
@@ -317,7 +331,8 @@ def run_ours(args):
         "scaling": "weak" if ws == 1 else "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": workload_name(cfg), "n_cells": n_global, "steps_per_run": args.steps,
-                   "global_batch": 1, "seq_len": 0, "parallelism": f"dp{ws}" if ws == 1 else f"domain{ws}",
+                   "global_batch": 1, "seq_len": 0, "parallelism": "1gpu" if ws == 1 else f"domain{ws}-{args.transport}",
+                   "renumber": args.renumber, "mode": args.mode,
                    "l2": "flushed between timed steps (256 MiB write)", "tol": TOL,
                    "pcg_iterations_per_step": {"min": min(its), "max": max(its), "mean": sum(its) / len(its)}},
         "roofline": {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": peak,

@@ -119,6 +119,24 @@ typedef struct lf_mesh lf_mesh;
 LF_API lf_status mesh_create(lf_context *ctx, const lf_mesh_desc *desc, lf_mesh **out);
 LF_API lf_status mesh_destroy(lf_mesh *mesh);
 
+/* Peer-memory transport (SURVEY §8(e) option A), the
+ * alternative to NCCL: halos and the PCG sums move through device memory the
+ * ranks map from each other with CUDA IPC (NVLink 5 between GPUs; the same
+ * memory when ranks share a GPU).  Kernels store halo values straight into
+ * the neighbour's buffers and exchange the reduction sums in the last block
+ * of each reduction, so the whole solve stays on the device (persistent
+ * kernel).  Sequence:
+ *   lf_p2p_init(ctx, nranks, rank)            before mesh_create
+ *   mesh_create(...)                          processor patches as for NCCL
+ *   lf_p2p_export(mesh, h)                    LF_P2P_HANDLE_BYTES per rank
+ *   (all-gather the handles, e.g. torch.distributed)
+ *   lf_p2p_connect(mesh, nranks, rank, all)   all[q*LF_P2P_HANDLE_BYTES] = rank q's
+ * All ranks must make the same sequence of solver calls (collective). */
+#define LF_P2P_HANDLE_BYTES 1024
+LF_API lf_status lf_p2p_init(lf_context *ctx, int nranks, int rank);
+LF_API lf_status lf_p2p_export(lf_mesh *mesh, void *handle_out);
+LF_API lf_status lf_p2p_connect(lf_mesh *mesh, int nranks, int rank, const void *handles);
+
 /* Sizes: n_cells, internal faces, total boundary faces, device bytes held. */
 LF_API lf_status lf_mesh_info(const lf_mesh *mesh, int32_t *n_cells, int32_t *n_faces,
                        int32_t *n_boundary_faces, int64_t *device_bytes);

@@ -144,10 +144,32 @@ lf_status lf_comm_init(lf_context *ctx, const void *uid, int nranks, int rank) {
     LF_REQUIRE(ctx && uid, "NULL argument");
     LF_REQUIRE(nranks >= 1 && rank >= 0 && rank < nranks, "bad nranks/rank");
     LF_REQUIRE(ctx->comm == nullptr, "communicator already initialised");
+    LF_REQUIRE(!ctx->p2p, "context already uses the peer-memory transport");
     ctx->comm = nccl_comm_init(uid, nranks, rank, ctx->device);
     ctx->nranks = nranks;
     ctx->rank = rank;
   });
+}
+
+lf_status lf_p2p_init(lf_context *ctx, int nranks, int rank) {
+  return guard([&] {
+    LF_REQUIRE(ctx != nullptr, "ctx is NULL");
+    p2p_init(ctx, nranks, rank);
+  });
+}
+
+lf_status lf_p2p_export(lf_mesh *M, void *handle) {
+  return guard([&] {
+    LF_REQUIRE(M && handle, "NULL argument");
+    p2p_export(M, handle);
+  }, M);
+}
+
+lf_status lf_p2p_connect(lf_mesh *M, int nranks, int rank, const void *handles) {
+  return guard([&] {
+    LF_REQUIRE(M && handles, "NULL argument");
+    p2p_connect(M, nranks, rank, handles);
+  }, M);
 }
 
 lf_status lf_comm_info(const lf_context *ctx, int *nranks, int *rank) {
@@ -293,12 +315,9 @@ lf_status laplacian_assemble(lf_mesh *M, const lf_laplacian_params *p, lf_ldu **
     LF_REQUIRE(p->DT > 0.0 && p->dt > 0.0, "DT and dt must be > 0");
     lf_context *ctx = M->ctx;
     cudaStream_t s = ctx->stream;
-    if (M->nproc > 0) {
-      ctx->launch(LF_K_PACK, [&] { launch_pack_x(s, M->nproc, M->ws.sendCell, M->T, M->ws.sendBuf); });
-      halo_exchange(M, M->ws.sendBuf, M->ws.recvBuf);
-    }
+    field_halo(M, M->T);
     ctx->launch(LF_K_ASSEMBLE, [&] {
-      launch_assemble(s, M->Lasm, M->md, M->ld, p->DT, 1.0 / p->dt, M->T, M->ws.recvBuf, false, M->ws);
+      launch_assemble(s, M->Lasm, M->md, M->ld, p->DT, 1.0 / p->dt, M->T, M->ws.recvT, false, M->ws);
     });
     M->ldu.assembled = true;
     if (sys) *sys = &M->ldu;
@@ -347,11 +366,8 @@ lf_status ldu_amul(const lf_ldu *sys, const double *x, double *y) {
     LF_REQUIRE(sys->assembled, "ldu not assembled");
     lf_context *ctx = M->ctx;
     cudaStream_t s = ctx->stream;
-    if (M->nproc > 0) {
-      ctx->launch(LF_K_PACK, [&] { launch_pack_x(s, M->nproc, M->ws.sendCell, x, M->ws.sendBuf); });
-      halo_exchange(M, M->ws.sendBuf, M->ws.recvBuf);
-    }
-    ctx->launch(LF_K_AMUL, [&] { launch_amul(s, M->Lamul, M->md, M->ld, M->ws.recvBuf, x, y); });
+    field_halo(M, x);
+    ctx->launch(LF_K_AMUL, [&] { launch_amul(s, M->Lamul, M->md, M->ld, M->ws.recvT, x, y); });
   }, M);
 }
 

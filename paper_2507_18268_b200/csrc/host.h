@@ -30,7 +30,8 @@ struct lf_context {
   cudaStream_t stream = nullptr;
   bool ownStream = false;
   int nranks = 1, rank = 0;
-  void *comm = nullptr;  // ncclComm_t
+  void *comm = nullptr;  // ncclComm_t (transport NCCL)
+  bool p2p = false;      // transport: peer memory (lf_p2p_init)
   int smCount = 0;
   // instrumentation
   bool instrument = false;
@@ -97,6 +98,11 @@ struct lf_mesh {
   int kernelsPerIteration = 0;
   int persistentGrid = 0;     // co-resident grid of k_pcg_persistent
   unsigned *gridBar = nullptr;  // device {count, generation}
+  // peer-memory transport: one IPC-exportable block [flags | vals | recvT | recvW]
+  char *p2pBlock = nullptr;
+  size_t p2pBytes = 0, offFlags = 0, offVals = 0, offRecvT = 0, offRecvW = 0;
+  std::vector<void *> ipcOpened;  // peer blocks mapped with cudaIpcOpenMemHandle
+  bool p2pConnected = false;
   ~lf_mesh();
 };
 
@@ -105,6 +111,11 @@ namespace lf {
 void solve_loop(lf_mesh *M, const lf_solver_controls *c, double *psi, bool fromAssembly,
                 const lf_laplacian_params *p, lf_solver_perf *out);
 void halo_exchange(lf_mesh *M, const double *send, double *recv);
+void field_halo(lf_mesh *M, const double *x);
+// p2p.cpp
+void p2p_init(lf_context *ctx, int nranks, int rank);
+void p2p_export(lf_mesh *M, void *handle);
+void p2p_connect(lf_mesh *M, int nranks, int rank, const void *handles);
 void allreduce(lf_mesh *M, const double *local, double *global, size_t count);
 void upload_controls(lf_mesh *M, const lf_solver_controls *c, double *psi);
 }  // namespace lf

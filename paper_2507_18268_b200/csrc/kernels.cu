@@ -82,18 +82,101 @@ __device__ __forceinline__ void block_sum(double (&v)[NV], double (*sm)[32]) {
   }
 }
 
-// Block partial -> partials[k*grid + block]; the last block (ticket) sums
-// the partials in block order and writes out[0..NV).  Returns true in every
-// thread of the last block; its thread 0 then holds the totals in v.
+// ------------------------------------------------ peer-memory allreduce
+// Executed by every thread of ONE block per rank (the last block of a
+// launch / grid barrier).  Rank r stores its NV local totals into slot r of
+// every rank's mailbox (P2P stores over NVLink, or plain stores when the
+// mailbox is on the same GPU), publishes them with a system-scope release
+// of the slot flag = seq, waits until all P slots of its own mailbox carry
+// seq, and sums the P slots in rank order: bit-identical on every rank.
+// Mailboxes are double-buffered by seq parity (a rank can be at most one
+// allreduce ahead of any other).
+__device__ __forceinline__ void st_release_sys(unsigned *p, unsigned v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ double ld_relaxed_sys(const double *p) {
+  double v;
+  asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Spin-wait watchdog: a rank that never arrives must not hang the GPU —
+// after LF_SPIN_TIMEOUT_S seconds the kernel traps (the call returns
+// LF_ERR_CUDA) instead of spinning forever.
+#ifndef LF_SPIN_TIMEOUT_S
+#define LF_SPIN_TIMEOUT_S 30
+#endif
+__device__ __forceinline__ unsigned long long gtime_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void spin_check(unsigned long long t0, unsigned &tries) {
+  if ((++tries & 1023u) == 0u && gtime_ns() - t0 > (unsigned long long)LF_SPIN_TIMEOUT_S * 1000000000ull)
+    __trap();
+}
+
 template <int NV>
-__device__ bool reduce_grid(double (&v)[NV], double *partials, unsigned *ticket, double *out) {
+__device__ void p2p_allreduce(const P2PDev &P, double (&tot)[NV] /* valid in thread 0 */) {
+  __shared__ double sv[NV];
+  __shared__ unsigned sseq;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) sv[k] = tot[k];
+    sseq = *P.seq + 1u;
+    *P.seq = sseq;
+  }
+  __syncthreads();
+  const unsigned seq = sseq, par = seq & 1u;
+  const int q = threadIdx.x;
+  if (q < P.P) {
+    double *dst = P.vals[q] + ((int)par * LF_MAXP + P.rank) * 4;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) dst[k] = sv[k];
+    __threadfence_system();
+    st_release_sys(P.flags[q] + par * LF_MAXP + P.rank, seq);
+    const unsigned *mine = P.flags[P.rank] + par * LF_MAXP + q;
+    const unsigned long long t0 = gtime_ns();
+    unsigned tries = 0;
+    while ((int)(ld_acquire_sys(mine) - seq) < 0) {
+      __nanosleep(64);
+      spin_check(t0, tries);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const double *box = P.vals[P.rank] + (int)par * LF_MAXP * 4;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      double s = 0.0;
+      for (int r = 0; r < P.P; ++r) s += ld_relaxed_sys(box + r * 4 + k);
+      tot[k] = s;
+    }
+  }
+}
+
+// Block partial -> partials[k*grid + block]; the last block (ticket) sums
+// the partials in block order (and, with the peer-memory transport, over
+// the ranks) and writes out[0..NV).  Returns true in every thread of the
+// last block; its thread 0 then holds the totals in v.
+template <int NV>
+__device__ bool reduce_grid(double (&v)[NV], double *partials, unsigned *ticket, double *out,
+                            const P2PDev &P) {
   __shared__ double sm[NV][32];
   __shared__ int amLast;
   block_sum<NV>(v, sm);
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int k = 0; k < NV; ++k) partials[k * gridDim.x + blockIdx.x] = v[k];
-    __threadfence();
+    if (P.P > 0)
+      __threadfence_system();  // this block's peer-memory halo stores precede the ticket
+    else
+      __threadfence();
     const unsigned t = atomicAdd(ticket, 1u);
     amLast = (t == gridDim.x - 1);
   }
@@ -120,6 +203,7 @@ __device__ bool reduce_grid(double (&v)[NV], double *partials, unsigned *ticket,
       for (int k = 0; k < NV; ++k) s[k] += t[u][k];
   }
   block_sum<NV>(s, sm);
+  if (P.P > 0) p2p_allreduce<NV>(P, s);
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
@@ -210,6 +294,40 @@ __device__ __forceinline__ double row_proc(const MeshDev &m, const double *__res
   return s;
 }
 
+// PCG interface term with halo p recomputed locally from the neighbour's w:
+// p_halo = w_halo (first iteration) or fma(beta, p_halo_old, w_halo) — the
+// same operands and operation the owning rank uses for that cell, so both
+// ranks hold bitwise the same p.  The new halo p is kept for the next
+// iteration (written by the thread that owns the face's cell).
+__device__ __forceinline__ double row_proc_p(const MeshDev &m, const double *__restrict__ bBnd,
+                                             const Workspace &ws, bool first, double beta, int k,
+                                             int c) {
+  double s = 0.0;
+  if (m.hasProc) {
+    const double *phOld = (k & 1) ? ws.pH[0] : ws.pH[1];
+    double *phNew = (k & 1) ? ws.pH[1] : ws.pH[0];
+    const int k0 = m.pcStart[c], k1 = m.pcStart[c + 1];
+    for (int kk = k0; kk < k1; ++kk) {
+      const int i = m.pcFace[kk], sl = m.bSlot[i];
+      const double wh = ws.recvW[sl];
+      const double ph = first ? wh : fma(beta, phOld[sl], wh);
+      phNew[sl] = ph;
+      s = fma(bBnd[i], ph, s);
+    }
+  }
+  return s;
+}
+
+// Peer-memory halo: store a cell's new value into the neighbour's halo slot
+// of each of its processor faces (remote store over NVLink; own buffer for
+// self pairs).  Made visible by the system fence before the reduction ticket.
+__device__ __forceinline__ void push_halo(const MeshDev &m, double *const *dst, int c, double val) {
+  if (m.hasProc) {
+    const int k0 = m.pcStart[c], k1 = m.pcStart[c + 1];
+    for (int kk = k0; kk < k1; ++kk) *dst[m.bSlot[m.pcFace[kk]]] = val;
+  }
+}
+
 // ------------------------------------------------------ L2 bulk prefetch
 // cp.async.bulk.prefetch.L2 (sm_90+ TMA engine): one instruction pulls a
 // contiguous byte range into L2 without occupying registers.  Each block
@@ -240,16 +358,25 @@ __device__ __forceinline__ bool conv(double res, double init, const PcgCtl *ctl)
   } while (0)
 
 // ------------------------------------------------------------------ sum
+// sum(x) (gAverage numerator); with the peer-memory transport it also puts x
+// at the processor-face cells into the neighbours' recvT (the halo of T/psi
+// the next assembly / PCG setup reads), ordered before the allreduce.
 __global__ void __launch_bounds__(BS, LF_MINB)
-    k_sum(const double *__restrict__ x, int32_t n, double *partials, unsigned *ticket, double *out) {
+    k_sum(MeshDev m, const double *__restrict__ x, double *partials, unsigned *ticket, double *out,
+          Workspace ws) {
   double v[1] = {0.0};
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) v[0] += x[c];
-  reduce_grid<1>(v, partials, ticket, out);
+  const bool push = ws.p2p.P > 0;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < m.n; c += gridDim.x * blockDim.x) {
+    const double xc = x[c];
+    v[0] += xc;
+    if (push) push_halo(m, ws.p2p.dstT, c, xc);
+  }
+  reduce_grid<1>(v, partials, ticket, out, ws.p2p);
 }
 
-void launch_sum(cudaStream_t s, const Launch &L, const double *x, int32_t n, const Workspace &ws,
+void launch_sum(cudaStream_t s, const Launch &L, const MeshDev &m, const double *x, const Workspace &ws,
                 double *out) {
-  k_sum<<<L.grid, BS, 0, s>>>(x, n, ws.partials, ws.tickets + T_SUM, out);
+  k_sum<<<L.grid, BS, 0, s>>>(m, x, ws.partials, ws.tickets + T_SUM, out, ws);
 }
 
 // -------------------------------------------------------------- assembly
@@ -328,10 +455,11 @@ __global__ void __launch_bounds__(BS, LF_MINB)
       v[2] = fma(w, r, v[2]);
       ws.r[c] = r;
       ws.w[c] = w;
+      if (ws.p2p.P > 0) push_halo(m, ws.p2p.dstW, c, w);
     }
   }
   if (SETUP) {
-    if (reduce_grid<3>(v, ws.partials, ws.tickets + T_ASM, ws.lsum->setup) && threadIdx.x == 0) {
+    if (reduce_grid<3>(v, ws.partials, ws.tickets + T_ASM, ws.lsum->setup, ws.p2p) && threadIdx.x == 0) {
       PcgCtl *ctl = ws.ctl;
       ctl->it = 0;
       ctl->stop = 0;
@@ -374,8 +502,9 @@ __global__ void __launch_bounds__(BS, LF_MINB_G)
     v[2] = fma(w, r, v[2]);
     ws.r[c] = r;
     ws.w[c] = w;
+    if (ws.p2p.P > 0) push_halo(m, ws.p2p.dstW, c, w);
   }
-  if (reduce_grid<3>(v, ws.partials, ws.tickets + T_SETUP, ws.lsum->setup) && threadIdx.x == 0) {
+  if (reduce_grid<3>(v, ws.partials, ws.tickets + T_SETUP, ws.lsum->setup, ws.p2p) && threadIdx.x == 0) {
     PcgCtl *ctl = ws.ctl;
     ctl->it = 0;
     ctl->stop = 0;
@@ -437,7 +566,7 @@ __device__ __forceinline__ double pval(const double *__restrict__ w, const doubl
 // iteration's residual; p_k = w + beta p_{k-1}; q = A p_k; sum p.q, sum psi.
 template <int KE>
 __global__ void __launch_bounds__(BS, LF_MINB_G)
-    k_phase1(MeshDev m, LduDev a, const double *__restrict__ halo, Workspace ws) {
+    k_phase1(MeshDev m, LduDev a, Workspace ws) {
   const PcgCtl *ctl = ws.ctl;
   if (ctl->stop) return;
   const IterState s = derive_phase1(ws);
@@ -476,12 +605,12 @@ __global__ void __launch_bounds__(BS, LF_MINB_G)
       pnew[c] = pc;
       double q = a.diag[c] * pc;
       q = row_offdiag<KE>(m, a, c, q, [&](int j) { return pval(w, pold, s.beta, first, j); });
-      q -= row_proc(m, a.bBnd, halo, c);
+      q -= row_proc_p(m, a.bBnd, ws, first, s.beta, s.k, c);
       ws.q[c] = q;
       v[0] = fma(pc, q, v[0]);
     }
   }
-  if (reduce_grid<2>(v, ws.partials, ws.tickets + T_P1, ws.lsum->p1) && threadIdx.x == 0) {
+  if (reduce_grid<2>(v, ws.partials, ws.tickets + T_P1, ws.lsum->p1, ws.p2p) && threadIdx.x == 0) {
     PcgCtl *c = ws.ctl;
     if (first) {
       c->normFactor = s.nf;
@@ -497,15 +626,17 @@ __global__ void __launch_bounds__(BS, LF_MINB_G)
 }
 
 void launch_phase1(cudaStream_t s, const Launch &L, const MeshDev &m, const LduDev &a,
-                   const double *halo, const Workspace &ws) {
-  LF_DISPATCH_KE(m, k_phase1, <<<L.grid, BS, 0, s>>>(m, a, halo, ws));
+                   const Workspace &ws) {
+  LF_DISPATCH_KE(m, k_phase1, <<<L.grid, BS, 0, s>>>(m, a, ws));
 }
 
 // ---------------------------------------------------------------- phase 2
 // checkSingularity(|wApA|/normFactor); alpha = wArA/wApA; r -= alpha q;
 // w = rD r (diagonal preconditioner, rD = 1/diag); sum|r|, sum w.r.
 __global__ void __launch_bounds__(BS, LF_MINB)
-    k_phase2(int32_t n, LduDev a, Workspace ws) {
+    k_phase2(MeshDev m, LduDev a, Workspace ws) {
+  const int n = m.n;
+  const bool push = ws.p2p.P > 0;
   const PcgCtl *ctl = ws.ctl;
   if (ctl->stop) return;
   const int k = ctl->it;
@@ -544,13 +675,14 @@ __global__ void __launch_bounds__(BS, LF_MINB)
           const double w = (1.0 / d[u]) * rn;
           ws.r[c] = rn;
           ws.w[c] = w;
+          if (push) push_halo(m, ws.p2p.dstW, c, w);
           v[0] += fabs(rn);
           v[1] = fma(w, rn, v[1]);
         }
       }
     }
   }
-  if (reduce_grid<2>(v, ws.partials, ws.tickets + T_P2, ws.lsum->p2) && threadIdx.x == 0) {
+  if (reduce_grid<2>(v, ws.partials, ws.tickets + T_P2, ws.lsum->p2, ws.p2p) && threadIdx.x == 0) {
     PcgCtl *c = ws.ctl;
     if (singular) {
       c->stop = 1;
@@ -563,8 +695,8 @@ __global__ void __launch_bounds__(BS, LF_MINB)
   }
 }
 
-void launch_phase2(cudaStream_t s, const Launch &L, int32_t n, const LduDev &a, const Workspace &ws) {
-  k_phase2<<<L.grid, BS, 0, s>>>(n, a, ws);
+void launch_phase2(cudaStream_t s, const Launch &L, const MeshDev &m, const LduDev &a, const Workspace &ws) {
+  k_phase2<<<L.grid, BS, 0, s>>>(m, a, ws);
 }
 
 // ------------------------------------------------- persistent PCG (1 GPU)
@@ -589,7 +721,8 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
 }
 
 template <int NV>
-__device__ void grid_reduce_sync(double (&v)[NV], double *partials, unsigned *bar, double *out) {
+__device__ void grid_reduce_sync(double (&v)[NV], double *partials, unsigned *bar, double *out,
+                                 const P2PDev &P) {
   __shared__ double sm[NV][32];
   __shared__ int amLast;
   block_sum<NV>(v, sm);
@@ -597,13 +730,21 @@ __device__ void grid_reduce_sync(double (&v)[NV], double *partials, unsigned *ba
 #pragma unroll
     for (int k = 0; k < NV; ++k) partials[k * gridDim.x + blockIdx.x] = v[k];
     const unsigned gen = ld_acquire(bar + 1);  // read before arriving: cannot move until we arrive
-    __threadfence();
+    if (P.P > 0)
+      __threadfence_system();  // peer-memory halo stores of this block precede the arrival
+    else
+      __threadfence();
     const unsigned t = atomicAdd(bar, 1u);
     amLast = (t == gridDim.x - 1);
     if (!amLast) {
       // ld.acquire.gpu orders the later loads and invalidates this SM's L1
       // (SASS CCTL.IVALL), so cached loads of other blocks' data are coherent
-      while (ld_acquire(bar + 1) == gen) __nanosleep(32);
+      const unsigned long long t0 = gtime_ns();
+      unsigned tries = 0;
+      while (ld_acquire(bar + 1) == gen) {
+        __nanosleep(32);
+        spin_check(t0, tries);
+      }
     }
   }
   __syncthreads();
@@ -627,6 +768,7 @@ __device__ void grid_reduce_sync(double (&v)[NV], double *partials, unsigned *ba
         for (int k = 0; k < NV; ++k) s[k] += t[u][k];
     }
     block_sum<NV>(s, sm);
+    if (P.P > 0) p2p_allreduce<NV>(P, s);  // ranks exchange totals before the local release
     if (threadIdx.x == 0) {
 #pragma unroll
       for (int k = 0; k < NV; ++k) out[k] = s[k];
@@ -640,9 +782,6 @@ __device__ void grid_reduce_sync(double (&v)[NV], double *partials, unsigned *ba
 
 #ifndef LF_MINB_P
 #define LF_MINB_P 5  // persistent kernel blocks/SM (r1k: 5 beats 4 and 6 at 200^3)
-#endif
-#ifndef LF_P1_PIPE
-#define LF_P1_PIPE 0  // software-pipelined phase 1 (next trip's loads in flight)
 #endif
 #ifndef LF_P2P_UNROLL
 #define LF_P2P_UNROLL 2  // persistent phase 2 cells per trip
@@ -687,65 +826,6 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
     };
     // ---- phase 1: flush psi, p = w + beta p_old, q = A p, sums
     double v1[2] = {0.0, 0.0};
-#if LF_P1_PIPE
-    if constexpr (KE > 0) {
-      if (cont) {
-        // software pipeline: the own-cell vectors and ELL slots of the NEXT
-        // trip are loaded while the current trip's gathers are in flight
-        struct Row {
-          double w, po, ps, dg, uo[KE];
-          int lo[KE], nb[KE];
-        };
-        const int ld = m.ldE;
-        auto load_row = [&](int c, Row &R) {
-          R.w = w[c];
-          R.po = first ? 0.0 : pold[c];
-          R.ps = psi[c];
-          R.dg = a.diag[c];
-#pragma unroll
-          for (int kk = 0; kk < KE; ++kk) {
-            R.lo[kk] = __ldg(m.loE + kk * ld + c);
-            R.nb[kk] = __ldg(m.nbrE + kk * ld + c);
-            R.uo[kk] = a.upperE[kk * ld + c];
-          }
-        };
-        int c = blockIdx.x * blockDim.x + threadIdx.x;
-        Row cur;
-        if (c < m.n) load_row(c, cur);
-        for (; c < m.n; c += stride) {
-          Row nxt;
-          if (c + stride < m.n) load_row(c + stride, nxt);
-          double ps = cur.ps;
-          if (!first) {
-            ps = fma(alpha, cur.po, ps);
-            psi[c] = ps;
-          }
-          v1[1] += ps;
-          const double pc = first ? cur.w : fma(beta, cur.po, cur.w);
-          pnew[c] = pc;
-          double lu[KE], lx[KE], ox[KE];
-#pragma unroll
-          for (int kk = 0; kk < KE; ++kk) {
-            const int oc = cur.lo[kk] & ELL_MASK;
-            lu[kk] = cur.lo[kk] >= 0 ? a.upperE[(cur.lo[kk] >> ELL_SHIFT) * ld + oc] : 0.0;
-            lx[kk] = cur.lo[kk] >= 0 ? pnb(oc) : 0.0;
-            ox[kk] = cur.nb[kk] >= 0 ? pnb(cur.nb[kk]) : 0.0;
-          }
-          double q = cur.dg * pc;
-#pragma unroll
-          for (int kk = 0; kk < KE; ++kk)
-            if (cur.lo[kk] >= 0) q = fma(lu[kk], lx[kk], q);
-#pragma unroll
-          for (int kk = 0; kk < KE; ++kk)
-            if (cur.nb[kk] >= 0) q = fma(cur.uo[kk], ox[kk], q);
-          ws.q[c] = q;
-          v1[0] = fma(pc, q, v1[0]);
-          cur = nxt;
-        }
-      }
-    }
-    if (KE == 0 || !cont)
-#endif
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < m.n; c += stride) {
       double ps = psi[c];
       if (!first) {
@@ -758,11 +838,12 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
         pnew[c] = pc;
         double q = a.diag[c] * pc;
         q = row_offdiag<KE>(m, a, c, q, pnb);
+        q -= row_proc_p(m, a.bBnd, ws, first, beta, k, c);
         ws.q[c] = q;
         v1[0] = fma(pc, q, v1[0]);
       }
     }
-    grid_reduce_sync<2>(v1, ws.partials, bar, ws.gsum->p1);
+    grid_reduce_sync<2>(v1, ws.partials, bar, ws.gsum->p1, ws.p2p);
     if (!cont) break;
     // ---- phase 2: singularity, alpha, r -= alpha q, w = r/diag, sums
     const double pq = __ldcg(&ws.gsum->p1[0]);
@@ -792,13 +873,14 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
             const double wc = (1.0 / d[u]) * rn;
             ws.r[c] = rn;
             ws.w[c] = wc;
+            if (ws.p2p.P > 0) push_halo(m, ws.p2p.dstW, c, wc);
             v2[0] += fabs(rn);
             v2[1] = fma(wc, rn, v2[1]);
           }
         }
       }
     }
-    grid_reduce_sync<2>(v2, ws.partials, bar, ws.gsum->p2);
+    grid_reduce_sync<2>(v2, ws.partials, bar, ws.gsum->p2, ws.p2p);
     ++k;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -861,21 +943,6 @@ void launch_pack_x(cudaStream_t s, int32_t ns, const int32_t *cells, const doubl
   k_pack_x<<<(ns + BS - 1) / BS, BS, 0, s>>>(ns, cells, x, buf);
 }
 
-// p_k at the send cells, evaluated exactly as k_phase1 will (same derive).
-__global__ void k_pack_p(int32_t ns, const int32_t *__restrict__ cells, Workspace ws) {
-  if (ws.ctl->stop) return;
-  const IterState s = derive_phase1(ws);
-  if (!s.cont) return;
-  const bool first = (s.k == 0);
-  const double *pold = (s.k & 1) ? ws.p[0] : ws.p[1];
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ns; i += gridDim.x * blockDim.x)
-    ws.sendBuf[i] = pval(ws.w, pold, s.beta, first, cells[i]);
-}
-
-void launch_pack_p(cudaStream_t s, int32_t ns, const int32_t *cells, const Workspace &ws) {
-  if (ns <= 0) return;
-  k_pack_p<<<(ns + BS - 1) / BS, BS, 0, s>>>(ns, cells, ws);
-}
 
 // ------------------------------------------------------------ utilities
 static int grid_for(int64_t n) {

@@ -103,20 +103,38 @@ struct Launch {
   int grid, block;
 };
 
+// Peer-memory (CUDA IPC / NVLink P2P) transport, see DESIGN.md §9.
+// Mailbox of rank q: flags[2 parity][LF_MAXP] (u32) and vals[2][LF_MAXP][4]
+// (f64) in one IPC-exported allocation; every rank holds mapped pointers to
+// all mailboxes.  P == 0: transport off.
+constexpr int LF_MAXP = 16;
+struct P2PDev {
+  int32_t P, rank;
+  unsigned *seq;              // own allreduce sequence counter (device)
+  unsigned *flags[LF_MAXP];   // mailbox flags of every rank (mapped)
+  double *vals[LF_MAXP];      // mailbox values of every rank (mapped)
+  double **dstW, **dstT;      // [n_proc] destination of each send slot in the
+                              // neighbour's recvW / recvT (own buffer for self pairs)
+};
+
 struct Workspace {
   double *r, *w, *q, *p[2];
   double *partials;     // [4 * maxGrid]
   unsigned *tickets;    // [16]
   PcgCtl *ctl;
   RedSlots *gsum;       // global sums
-  RedSlots *lsum;       // local sums (== gsum when single rank)
-  double *sendBuf, *recvBuf;
+  RedSlots *lsum;       // local sums (== gsum when single rank or P2P)
+  // processor-patch halos (slot = flat processor-face index, n_proc slots)
+  double *sendBuf;      // staging for NCCL / local copies
+  double *recvT, *recvW;  // neighbour T (assembly) and w (PCG) at each slot
+  double *pH[2];        // p at the halo slots, recomputed locally (double-buffered like p)
   int32_t *sendCell;    // [n_proc] local cell of each send slot
   int maxGrid;
+  P2PDev p2p;
 };
 
 // kernels.cu launchers (all stream-ordered, no host sync)
-void launch_sum(cudaStream_t s, const Launch &L, const double *x, int32_t n, const Workspace &ws,
+void launch_sum(cudaStream_t s, const Launch &L, const MeshDev &m, const double *x, const Workspace &ws,
                 double *out);
 void launch_assemble(cudaStream_t s, const Launch &L, const MeshDev &m, const LduDev &a,
                      double DT, double rDeltaT, const double *T, const double *halo,
@@ -124,8 +142,8 @@ void launch_assemble(cudaStream_t s, const Launch &L, const MeshDev &m, const Ld
 void launch_pcg_setup(cudaStream_t s, const Launch &L, const MeshDev &m, const LduDev &a,
                       const double *halo, const Workspace &ws);
 void launch_phase1(cudaStream_t s, const Launch &L, const MeshDev &m, const LduDev &a,
-                   const double *halo, const Workspace &ws);
-void launch_phase2(cudaStream_t s, const Launch &L, int32_t n, const LduDev &a,
+                   const Workspace &ws);
+void launch_phase2(cudaStream_t s, const Launch &L, const MeshDev &m, const LduDev &a,
                    const Workspace &ws);
 void launch_amul(cudaStream_t s, const Launch &L, const MeshDev &m, const LduDev &a,
                  const double *halo, const double *x, double *y);
@@ -134,7 +152,6 @@ void launch_pcg_persistent(cudaStream_t s, int grid, const MeshDev &m, const Ldu
                            const Workspace &ws, unsigned *bar);
 void launch_pack_x(cudaStream_t s, int32_t nsend, const int32_t *cells, const double *x,
                    double *buf);
-void launch_pack_p(cudaStream_t s, int32_t nsend, const int32_t *cells, const Workspace &ws);
 void launch_permute(cudaStream_t s, int32_t n, const int32_t *idx, const double *in, double *out,
                     bool scatter);
 void launch_gather_f64(cudaStream_t s, int64_t n, const int32_t *idx, const double *in,

@@ -132,6 +132,7 @@ using namespace lf;
 lf_mesh::~lf_mesh() {
   for (auto &g : chunkGraph)
     if (g) cudaGraphExecDestroy(g);
+  for (void *p : ipcOpened) cudaIpcCloseMemHandle(p);
   if (hctl) cudaFreeHost(hctl);
   arena.release();
 }
@@ -414,7 +415,23 @@ static void build_mesh(lf_context *ctx, const lf_mesh_desc *d, lf_mesh *M) {
   ws.lsum = ctx->comm ? A.alloc<RedSlots>(1) : ws.gsum;
   if (ctx->comm) LF_CUDA(cudaMemsetAsync(ws.lsum, 0, sizeof(RedSlots), s));
   ws.sendBuf = A.alloc<double>(nproc);
-  ws.recvBuf = A.alloc<double>(nproc);
+  ws.pH[0] = A.alloc<double>(nproc);
+  ws.pH[1] = A.alloc<double>(nproc);
+  // one cudaMalloc block (IPC-exportable for the peer-memory transport):
+  // [mailbox flags 2*MAXP u32 | mailbox vals 2*MAXP*4 f64 | recvT | recvW]
+  {
+    auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    M->offFlags = 0;
+    M->offVals = up(2 * LF_MAXP * sizeof(unsigned));
+    M->offRecvT = up(M->offVals + 2 * LF_MAXP * 4 * sizeof(double));
+    M->offRecvW = up(M->offRecvT + sizeof(double) * std::max(nproc, 1));
+    M->p2pBytes = up(M->offRecvW + sizeof(double) * std::max(nproc, 1));
+    M->p2pBlock = A.alloc<char>(M->p2pBytes);
+    LF_CUDA(cudaMemsetAsync(M->p2pBlock, 0, M->p2pBytes, s));
+    ws.recvT = reinterpret_cast<double *>(M->p2pBlock + M->offRecvT);
+    ws.recvW = reinterpret_cast<double *>(M->p2pBlock + M->offRecvW);
+  }
+  std::memset(&ws.p2p, 0, sizeof(ws.p2p));
   ws.sendCell = A.alloc<int32_t>(nproc);
   LF_CUDA(cudaMemcpyAsync(ws.sendCell, sendCells.data(), sizeof(int32_t) * nproc, cudaMemcpyHostToDevice, s));
   M->T = A.alloc<double>(n);

@@ -62,17 +62,40 @@ void upload_controls(lf_mesh *M, const lf_solver_controls *c, double *psi) {
   LF_CUDA(cudaStreamSynchronize(M->ctx->stream));
 }
 
+// Host-side halo of a cell field (NCCL / local copies): x at the send cells
+// -> sendBuf -> neighbour's recv.  With the peer-memory transport the
+// kernels store straight into the neighbour's buffers instead.
+static bool host_halo(lf_mesh *M) { return M->nproc > 0 && !M->p2pConnected; }
+
+static void exchange_field(lf_mesh *M, const double *x, double *recv) {
+  lf_context *ctx = M->ctx;
+  const Workspace &ws = M->ws;
+  ctx->launch(LF_K_PACK, [&] { launch_pack_x(ctx->stream, M->nproc, ws.sendCell, x, ws.sendBuf); });
+  halo_exchange(M, ws.sendBuf, recv);
+}
+
+// Halo of a cell field into recvT for the standalone calls (assembly, Amul):
+// peer memory -> the sum kernel's put + allreduce (its sum is discarded);
+// otherwise pack + exchange.
+void field_halo(lf_mesh *M, const double *x) {
+  if (M->nproc == 0) return;
+  lf_context *ctx = M->ctx;
+  if (M->p2pConnected)
+    ctx->launch(LF_K_SUMPSI, [&] { launch_sum(ctx->stream, M->Lsum, M->md, x, M->ws, M->scratch); });
+  else
+    exchange_field(M, x, M->ws.recvT);
+}
+
+// One PCG iteration: phase 1 (uses the halo of w from the previous phase 2
+// and recomputes halo p locally), phase 2, then the halo of the new w.
 static void iteration(lf_mesh *M) {
   lf_context *ctx = M->ctx;
   cudaStream_t s = ctx->stream;
   const Workspace &ws = M->ws;
-  if (M->nproc > 0) {
-    ctx->launch(LF_K_PACK, [&] { launch_pack_p(s, M->nproc, ws.sendCell, ws); });
-    halo_exchange(M, ws.sendBuf, ws.recvBuf);
-  }
-  ctx->launch(LF_K_PHASE1, [&] { launch_phase1(s, M->Lp1, M->md, M->ld, ws.recvBuf, ws); });
+  ctx->launch(LF_K_PHASE1, [&] { launch_phase1(s, M->Lp1, M->md, M->ld, ws); });
   allreduce(M, ws.lsum->p1, ws.gsum->p1, 2);
-  ctx->launch(LF_K_PHASE2, [&] { launch_phase2(s, M->Lp2, M->n, M->ld, ws); });
+  ctx->launch(LF_K_PHASE2, [&] { launch_phase2(s, M->Lp2, M->md, M->ld, ws); });
+  if (host_halo(M)) exchange_field(M, ws.w, ws.recvW);
   allreduce(M, ws.lsum->p2, ws.gsum->p2, 2);
 }
 
@@ -86,7 +109,7 @@ static void enqueue_iterations(lf_mesh *M, int count) {
     for (int i = 0; i < count; ++i) iteration(M);
     return;
   }
-  if (M->kernelsPerIteration == 0) M->kernelsPerIteration = (M->nproc > 0 ? 3 : 2);
+  if (M->kernelsPerIteration == 0) M->kernelsPerIteration = host_halo(M) ? 3 : 2;
   for (int b = lf_mesh::kMaxGraphLog - 1; b >= 0 && count > 0;) {
     const int k = 1 << b;
     if (count < k) {
@@ -115,7 +138,7 @@ static void enqueue_iterations(lf_mesh *M, int count) {
     ctx->launches += (int64_t)k * M->kernelsPerIteration;
     ctx->kLaunches[LF_K_PHASE1] += k;
     ctx->kLaunches[LF_K_PHASE2] += k;
-    if (M->nproc > 0) ctx->kLaunches[LF_K_PACK] += k;
+    if (host_halo(M)) ctx->kLaunches[LF_K_PACK] += k;
     count -= k;
   }
 }
@@ -129,8 +152,9 @@ static void run_iterations(lf_mesh *M, lf_solver_perf *out) {
   const int64_t bound = (int64_t)std::max(maxIter, minIter) + 2;
   int64_t launched = 0;
   int chunk = M->lastIters >= 0 ? M->lastIters + 1 : 8;
-  if (ctx->persistent && !ctx->comm && M->nproc == 0) {
-    // single rank, no halo: the whole loop in one cooperative launch
+  if (ctx->persistent && !ctx->comm && !host_halo(M)) {
+    // no host-side halo (single rank, or peer-memory transport): the whole
+    // loop in one cooperative launch
     ctx->launch(LF_K_PCG, [&] { launch_pcg_persistent(s, M->persistentGrid, M->md, M->ld, M->ws, M->gridBar); });
     LF_CUDA(cudaMemcpyAsync(M->hctl, M->ws.ctl, sizeof(PcgCtl), cudaMemcpyDeviceToHost, s));
     LF_CUDA(cudaStreamSynchronize(s));
@@ -163,7 +187,7 @@ static void run_iterations(lf_mesh *M, lf_solver_perf *out) {
 
 static void sum_psi(lf_mesh *M, const double *psi) {
   lf_context *ctx = M->ctx;
-  ctx->launch(LF_K_SUMPSI, [&] { launch_sum(ctx->stream, M->Lsum, psi, M->n, M->ws, &M->ws.lsum->p1[1]); });
+  ctx->launch(LF_K_SUMPSI, [&] { launch_sum(ctx->stream, M->Lsum, M->md, psi, M->ws, &M->ws.lsum->p1[1]); });
   allreduce(M, M->ws.lsum->p1, M->ws.gsum->p1, 2);
 }
 
@@ -173,18 +197,18 @@ void solve_loop(lf_mesh *M, const lf_solver_controls *c, double *psi, bool fromA
   cudaStream_t s = ctx->stream;
   const Workspace &ws = M->ws;
   const bool psiIsT = (psi == M->T);
-  if (!(psiIsT && M->sumPsiValid)) sum_psi(M, psi);
-  if (M->nproc > 0) {
-    ctx->launch(LF_K_PACK, [&] { launch_pack_x(s, M->nproc, ws.sendCell, psi, ws.sendBuf); });
-    halo_exchange(M, ws.sendBuf, ws.recvBuf);
-  }
+  // sum(psi) for normFactor; with the peer-memory transport the same launch
+  // puts psi at the processor-face cells into the neighbours' recvT
+  if (!(psiIsT && M->sumPsiValid) || M->p2pConnected) sum_psi(M, psi);
+  if (host_halo(M)) exchange_field(M, psi, ws.recvT);
   if (fromAssembly) {
     ctx->launch(LF_K_ASSEMBLE, [&] {
-      launch_assemble(s, M->Lasm, M->md, M->ld, p->DT, 1.0 / p->dt, psi, ws.recvBuf, true, ws);
+      launch_assemble(s, M->Lasm, M->md, M->ld, p->DT, 1.0 / p->dt, psi, ws.recvT, true, ws);
     });
   } else {
-    ctx->launch(LF_K_SETUP, [&] { launch_pcg_setup(s, M->Lsetup, M->md, M->ld, ws.recvBuf, ws); });
+    ctx->launch(LF_K_SETUP, [&] { launch_pcg_setup(s, M->Lsetup, M->md, M->ld, ws.recvT, ws); });
   }
+  if (host_halo(M)) exchange_field(M, ws.w, ws.recvW);  // w of the setup for iteration 0
   allreduce(M, ws.lsum->setup, ws.gsum->setup, 3);
   run_iterations(M, out);
   // gsum->p1[1] now holds sum(psi) of the final psi (last phase-1 launch)

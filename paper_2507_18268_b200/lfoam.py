@@ -92,7 +92,11 @@ SIGNATURES = {
     "lf_kernel_stats": (C.c_int, [_vp, C.c_int, C.POINTER(_i64), C.POINTER(_d)]),
     "lf_launch_count": (C.c_int, [_vp, C.POINTER(_i64)]),
     "lf_set_option": (C.c_int, [_vp, C.c_int, C.c_int]),
+    "lf_p2p_init": (C.c_int, [_vp, C.c_int, C.c_int]),
+    "lf_p2p_export": (C.c_int, [_vp, _vp]),
+    "lf_p2p_connect": (C.c_int, [_vp, C.c_int, C.c_int, _vp]),
 }
+P2P_HANDLE_BYTES = 1024
 
 _lib = None
 
@@ -160,6 +164,10 @@ class Context:
     def comm_init(self, uid: bytes, nranks: int, rank: int):
         buf = C.create_string_buffer(bytes(uid), 128)
         _check(lib().lf_comm_init(self.h, buf, nranks, rank))
+
+    def p2p_init(self, nranks: int, rank: int):
+        """Peer-memory transport (CUDA IPC); call before creating meshes."""
+        _check(lib().lf_p2p_init(self.h, nranks, rank))
 
     def comm_info(self):
         n, r = C.c_int(), C.c_int()
@@ -237,6 +245,17 @@ class Mesh:
         n, F, B, b = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int64()
         _check(lib().lf_mesh_info(self.h, C.byref(n), C.byref(F), C.byref(B), C.byref(b)))
         return dict(n_cells=n.value, n_faces=F.value, n_boundary_faces=B.value, device_bytes=b.value)
+
+    def p2p_export(self) -> bytes:
+        buf = C.create_string_buffer(P2P_HANDLE_BYTES)
+        _check(lib().lf_p2p_export(self.h, buf))
+        return buf.raw
+
+    def p2p_connect(self, handles, rank: int):
+        """handles: list of every rank's p2p_export() bytes, in rank order."""
+        blob = b"".join(bytes(h) for h in handles)
+        buf = C.create_string_buffer(blob, len(blob))
+        _check(lib().lf_p2p_connect(self.h, len(handles), rank, buf))
 
     def export_addressing(self):
         os_ = np.zeros(self.n_cells + 1, np.int32); lo = np.zeros(self.n_faces, np.int32)

@@ -1,0 +1,127 @@
+"""Peer-memory (CUDA IPC) transport (-m gpu).
+
+* one process, self-coupled processor patches, P2P with nranks = 1: the
+  kernels' halo stores and mailbox allreduce on their own buffers;
+* TWO processes sharing the one GPU (CUDA IPC within a device), each owning
+  a slab of the cube, handles exchanged over a gloo group: the real
+  multi-rank code path (kernel-side halo puts into the other process's
+  memory, rank-ordered mailbox allreduce), compared with the undecomposed
+  oracle.  Watchdog: a missing peer traps after 30 s instead of hanging.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import meshgen
+import oracle
+from paper_2507_18268_b200 import decompose
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2507_18268_b200 as _P
+    return _P
+
+
+@pytest.mark.parametrize("persistent", [True, False])
+def test_p2p_loopback_single_process(P, persistent):
+    m = meshgen.block_mesh(14, 12, 16, bc={"ymin": ("fixedValue", 1.0)})
+    c = decompose.cut_mesh(m, decompose.z_plane_faces(m, 7))
+    s = meshgen.multimode_field(m)
+    To, _, po = oracle.laplacian_foam(m, s, 4)
+    ctx = P.Context(0)
+    ctx.set_option("persistent", persistent)
+    ctx.p2p_init(1, 0)
+    mesh = P.Mesh(ctx, c)
+    mesh.p2p_connect([mesh.p2p_export()], 0)
+    mesh.set_T(s)
+    pg = mesh.step(4)
+    T = mesh.get_T()
+    assert np.max(np.abs(T - To)) <= 1e-8 * np.max(np.abs(To))
+    assert all(abs(a["n_iterations"] - b["n_iterations"]) <= 1 for a, b in zip(pg, po))
+    n_pcg, _ = ctx.kernel_stats("pcg")
+    assert (n_pcg > 0) == persistent
+    # standalone Amul through the peer-memory halo
+    ldu = mesh.assemble(1.0, 0.2)
+    x = meshgen.random_field(m, seed=2)
+    ref = oracle.assemble(m, 1.0, 0.2, T)
+    y_ref = oracle.amul(m, ref["diag"], ref["upper"], x)
+    xd = torch.as_tensor(x, device="cuda")
+    yd = torch.empty_like(xd)
+    ldu.amul(xd, yd)
+    scale = np.abs(ref["diag"] * x) + 6 * np.abs(ref["upper"]).max() * np.abs(x).max()
+    assert np.max(np.abs(yd.cpu().numpy() - y_ref) / scale) <= 1e-12
+    ctx.close()
+
+
+def _free_port():
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def _rank_main(rank, world, port, persistent, out):
+    import torch.distributed as dist
+    import paper_2507_18268_b200 as P
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    try:
+        g = meshgen.block_mesh(18, 16, 20, bc={"xmax": "zeroGradient"})
+        part = decompose.slab_partition(g, world)
+        m, cells = decompose.local_mesh(g, part, rank)
+        ctx = P.Context(0)
+        ctx.set_option("persistent", persistent)
+        ctx.p2p_init(world, rank)
+        mesh = P.Mesh(ctx, m)
+        hs = [None] * world
+        dist.all_gather_object(hs, mesh.p2p_export())
+        mesh.p2p_connect(hs, rank)
+        mesh.set_T(meshgen.multimode_field(g)[cells])
+        perfs = mesh.step(3)
+        out[rank] = ("ok", cells, mesh.get_T(), [p["n_iterations"] for p in perfs])
+        dist.barrier()
+        ctx.close()
+    except Exception as e:  # report instead of hanging the peer
+        out[rank] = ("error", repr(e))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("persistent", [False, True])
+def test_p2p_two_processes_one_gpu(P, persistent):
+    import torch.multiprocessing as mp
+    world = 2
+    ctx = mp.get_context("spawn")
+    mgr = ctx.Manager()
+    out = mgr.dict()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank_main, args=(r, world, port, persistent, out)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+    for p in procs:
+        if p.is_alive():
+            p.kill()
+    res = dict(out)
+    assert len(res) == world, res
+    for r in range(world):
+        assert res[r][0] == "ok", res[r]
+    g = meshgen.block_mesh(18, 16, 20, bc={"xmax": "zeroGradient"})
+    s = meshgen.multimode_field(g)
+    To, _, po = oracle.laplacian_foam(g, s, 3)
+    T = np.zeros(g.n_cells)
+    for r in range(world):
+        _, cells, Tr, its = res[r]
+        T[cells] = Tr
+        assert all(abs(a - b["n_iterations"]) <= 1 for a, b in zip(its, po)), (its, po)
+    assert res[0][3] == res[1][3]          # identical stopping decisions on both ranks
+    assert np.max(np.abs(T - To)) <= 1e-8 * np.max(np.abs(To))
