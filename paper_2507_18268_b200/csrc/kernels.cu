@@ -720,9 +720,30 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
   return v;
 }
 
+#ifndef LF_BAR_ACQREL
+#define LF_BAR_ACQREL 1  // grid barrier with acq_rel atomics instead of fence + atomic
+#endif
+#if LF_TIMING
+#define LF_DBG_ARG(x) , (x)
+#else
+#define LF_DBG_ARG(x)
+#endif
+#if LF_TIMING
+// barrier anatomy snapshot (debug builds): arrival / release / wake times
+constexpr int LF_DBG_N = 64, LF_DBG_G = 1024;
+__device__ unsigned long long g_dbg_arr[LF_DBG_N][LF_DBG_G], g_dbg_wake[LF_DBG_N][LF_DBG_G];
+__device__ unsigned long long g_dbg_rel[LF_DBG_N];
+__device__ int g_dbg_last[LF_DBG_N];
+__device__ int g_dbg_i_dummy;
+#define g_dbg_i dbg_i
+#endif
 template <int NV>
 __device__ void grid_reduce_sync(double (&v)[NV], double *partials, unsigned *bar, double *out,
-                                 const P2PDev &P) {
+                                 const P2PDev &P
+#if LF_TIMING
+                                 , int dbg_i
+#endif
+                                 ) {
   __shared__ double sm[NV][32];
   __shared__ int amLast;
   block_sum<NV>(v, sm);
@@ -730,11 +751,23 @@ __device__ void grid_reduce_sync(double (&v)[NV], double *partials, unsigned *ba
 #pragma unroll
     for (int k = 0; k < NV; ++k) partials[k * gridDim.x + blockIdx.x] = v[k];
     const unsigned gen = ld_acquire(bar + 1);  // read before arriving: cannot move until we arrive
-    if (P.P > 0)
+#if LF_TIMING
+    if (g_dbg_i < LF_DBG_N && blockIdx.x < LF_DBG_G) g_dbg_arr[g_dbg_i][blockIdx.x] = gtime_ns();
+#endif
+    unsigned t;
+    if (P.P > 0) {
       __threadfence_system();  // peer-memory halo stores of this block precede the arrival
-    else
+      t = atomicAdd(bar, 1u);
+    } else {
+#if LF_BAR_ACQREL
+      // release: the block's writes (ordered by the bar.sync above) precede the
+      // arrival; acquire: the last arriver sees every block's partials
+      asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(t) : "l"(bar) : "memory");
+#else
       __threadfence();
-    const unsigned t = atomicAdd(bar, 1u);
+      t = atomicAdd(bar, 1u);
+#endif
+    }
     amLast = (t == gridDim.x - 1);
     if (!amLast) {
       // ld.acquire.gpu orders the later loads and invalidates this SM's L1
@@ -745,15 +778,20 @@ __device__ void grid_reduce_sync(double (&v)[NV], double *partials, unsigned *ba
         __nanosleep(32);
         spin_check(t0, tries);
       }
+#if LF_TIMING
+      if (g_dbg_i < LF_DBG_N && blockIdx.x < LF_DBG_G) g_dbg_wake[g_dbg_i][blockIdx.x] = gtime_ns();
+#endif
     }
   }
   __syncthreads();
   if (amLast) {
+#if !LF_BAR_ACQREL
     __threadfence();
+#endif
     double s[NV];
 #pragma unroll
     for (int k = 0; k < NV; ++k) s[k] = 0.0;
-    constexpr int U = 4;
+    constexpr int U = 8;  // one L2 round trip for grids up to 8*blockDim
     for (int b0 = threadIdx.x; b0 < (int)gridDim.x; b0 += blockDim.x * U) {
       double t[U][NV];
 #pragma unroll
@@ -773,60 +811,121 @@ __device__ void grid_reduce_sync(double (&v)[NV], double *partials, unsigned *ba
 #pragma unroll
       for (int k = 0; k < NV; ++k) out[k] = s[k];
       bar[0] = 0u;
+#if LF_TIMING
+      if (g_dbg_i < LF_DBG_N) {
+        g_dbg_rel[g_dbg_i] = gtime_ns();
+        g_dbg_last[g_dbg_i] = blockIdx.x;
+      }
+#endif
+#if LF_BAR_ACQREL
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar + 1) : "memory");  // release
+#else
       __threadfence();
       atomicAdd(bar + 1, 1u);  // release
+#endif
     }
     __syncthreads();
   }
 }
 
 #ifndef LF_MINB_P
-#define LF_MINB_P 5  // persistent kernel blocks/SM (r1k: 5 beats 4 and 6 at 200^3)
+#define LF_MINB_P 4  // persistent kernel blocks/SM: 64 registers, no spills (r1o: 100^3
+                     // 3.39 ms/step vs 3.71 with 5 blocks/SM and 60 B of spills)
 #endif
+#ifndef LF_TIMING
+#define LF_TIMING 0  // 1: per-phase / per-barrier times printed by the persistent kernel
+#endif
+#ifndef LF_CHUNKED
+#define LF_CHUNKED 0  // persistent kernel: contiguous cell chunk per block (vs grid stride).
+#endif                // r1n: chunks raise the phase-1 arrival spread 6 -> 28 us at 100^3 -> off
+bool persistent_chunked() { return LF_CHUNKED != 0; }
 #ifndef LF_P2P_UNROLL
 #define LF_P2P_UNROLL 2  // persistent phase 2 cells per trip
 #endif
-template <int KE>
+// HALO = false: single rank without processor patches — the interface
+// term, halo puts and peer allreduce are compiled out of the hot loop
+// (they cost 13% at 100^3 even when branched around, r1o).
+template <int KE, bool HALO>
 __global__ void __launch_bounds__(BS, LF_MINB_P)
     k_pcg_persistent(MeshDev m, LduDev a, Workspace ws, unsigned *bar) {
   PcgCtl *ctl = ws.ctl;
+  if (!HALO) ws.p2p.P = 0;
   if (ctl->stop) return;
-  int k = ctl->it;
-  double nf = ctl->normFactor, initRes = ctl->initRes, finRes = ctl->finRes;
-  double wArA = ctl->wArA, alpha = ctl->alpha;
+  // block-uniform solver state lives in shared memory (thread 0 updates it
+  // between barriers) so it does not occupy registers across the phases
+  struct St {
+    double nf, initRes, finRes, wArA, alpha, beta;
+    int k, cont, singular;
+  };
+  __shared__ St st;
+  if (threadIdx.x == 0) {
+    st.k = ctl->it;
+    st.nf = ctl->normFactor;
+    st.initRes = ctl->initRes;
+    st.finRes = ctl->finRes;
+    st.wArA = ctl->wArA;
+    st.alpha = ctl->alpha;
+    st.singular = 0;
+  }
   double *psi = ctl->psi;
   const double *__restrict__ w = ws.w;
-  bool cont = false, singular = false;
-  const int stride = gridDim.x * blockDim.x;
+#if LF_CHUNKED
+  // block b owns the contiguous cells [b*C, (b+1)*C): equal work per block on
+  // an SM-uniform grid (numSMs x blocks/SM), the same cells in both phases
+  const int C = (((m.n + (int)gridDim.x - 1) / (int)gridDim.x) + 31) & ~31;
+  const int cbeg = min((int)blockIdx.x * C, m.n), cend = min(cbeg + C, m.n);
+  const int cstart = cbeg + threadIdx.x, cstep = blockDim.x;
+#else
+  const int cstart = blockIdx.x * blockDim.x + threadIdx.x, cend = m.n, cstep = gridDim.x * blockDim.x;
+#endif
+#if LF_TIMING
+  unsigned long long tprev = 0, tacc[4] = {0, 0, 0, 0};
+#define LF_TSTAMP(i)                                   \
+  do {                                                 \
+    const unsigned long long tn_ = gtime_ns();         \
+    if ((i) > 0) tacc[(i) - 1] += tn_ - tprev;         \
+    tprev = tn_;                                       \
+  } while (0)
+#else
+#define LF_TSTAMP(i) \
+  do {               \
+  } while (0)
+#endif
   for (;;) {
     // ---- derive (OpenFOAM loop condition) from the previous totals
-    double beta = 0.0;
-    if (k == 0) {
-      nf = __ldcg(&ws.gsum->setup[0]) + 1e-20;
-      initRes = __ldcg(&ws.gsum->setup[1]) / nf;
-      finRes = initRes;
-      cont = ctl->minIter > 0 || !conv(finRes, initRes, ctl);
-      wArA = __ldcg(&ws.gsum->setup[2]);
-    } else {
-      finRes = __ldcg(&ws.gsum->p2[0]) / nf;
-      cont = (k < ctl->maxIter && !conv(finRes, initRes, ctl)) || k < ctl->minIter;
-      const double wn = __ldcg(&ws.gsum->p2[1]);
-      beta = wn / wArA;
-      wArA = wn;
+    if (threadIdx.x == 0) {
+      if (st.k == 0) {
+        st.nf = __ldcg(&ws.gsum->setup[0]) + 1e-20;
+        st.initRes = __ldcg(&ws.gsum->setup[1]) / st.nf;
+        st.finRes = st.initRes;
+        st.cont = ctl->minIter > 0 || !conv(st.finRes, st.initRes, ctl);
+        st.wArA = __ldcg(&ws.gsum->setup[2]);
+        st.beta = 0.0;
+      } else {
+        st.finRes = __ldcg(&ws.gsum->p2[0]) / st.nf;
+        st.cont = (st.k < ctl->maxIter && !conv(st.finRes, st.initRes, ctl)) || st.k < ctl->minIter;
+        const double wn = __ldcg(&ws.gsum->p2[1]);
+        st.beta = wn / st.wArA;
+        st.wArA = wn;
+      }
     }
-    const bool first = (k == 0);
+    __syncthreads();
+    const int k = st.k;
+    const bool first = (k == 0), cont = st.cont != 0;
+    const double beta = st.beta, alpha = st.alpha;
     const double *__restrict__ pold = (k & 1) ? ws.p[0] : ws.p[1];
     double *__restrict__ pnew = (k & 1) ? ws.p[1] : ws.p[0];
     auto pnb = [&](int j) {  // p at a neighbour cell (written by another block)
 #if LF_PERSIST_LDCG
       return first ? __ldcg(w + j) : fma(beta, __ldcg(pold + j), __ldcg(w + j));
-#else  // L1 was invalidated by the post-barrier gpu-scope fence: cached loads are coherent
+#else  // L1 was invalidated by the barrier's ld.acquire.gpu: cached loads are coherent
       return first ? w[j] : fma(beta, pold[j], w[j]);
 #endif
     };
     // ---- phase 1: flush psi, p = w + beta p_old, q = A p, sums
     double v1[2] = {0.0, 0.0};
-    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < m.n; c += stride) {
+    LF_TSTAMP(0);
+    for (int c = cstart; c < cend; c += cstep) {
       double ps = psi[c];
       if (!first) {
         ps = fma(alpha, pold[c], ps);
@@ -838,79 +937,137 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
         pnew[c] = pc;
         double q = a.diag[c] * pc;
         q = row_offdiag<KE>(m, a, c, q, pnb);
-        q -= row_proc_p(m, a.bBnd, ws, first, beta, k, c);
+        if (HALO) q -= row_proc_p(m, a.bBnd, ws, first, beta, k, c);
         ws.q[c] = q;
         v1[0] = fma(pc, q, v1[0]);
       }
     }
-    grid_reduce_sync<2>(v1, ws.partials, bar, ws.gsum->p1, ws.p2p);
+    LF_TSTAMP(1);
+    grid_reduce_sync<2>(v1, ws.partials, bar, ws.gsum->p1, ws.p2p LF_DBG_ARG(2 * k));
+    LF_TSTAMP(2);
     if (!cont) break;
     // ---- phase 2: singularity, alpha, r -= alpha q, w = r/diag, sums
-    const double pq = __ldcg(&ws.gsum->p1[0]);
-    if (fabs(pq) / nf < 1e-300) {
-      singular = true;
-      break;
+    if (threadIdx.x == 0) {
+      const double pq = __ldcg(&ws.gsum->p1[0]);
+      st.singular = fabs(pq) / st.nf < 1e-300;
+      if (!st.singular) st.alpha = st.wArA / pq;
     }
-    alpha = wArA / pq;
+    __syncthreads();
+    if (st.singular) break;
+    const double alpha2 = st.alpha;
     double v2[2] = {0.0, 0.0};
     {
       constexpr int U = LF_P2P_UNROLL;  // cells per trip, loads issued first
-      for (int c0 = blockIdx.x * blockDim.x + threadIdx.x; c0 < m.n; c0 += stride * U) {
+      for (int c0 = cstart; c0 < cend; c0 += cstep * U) {
         double q[U], r[U], d[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const int c = c0 + u * stride;
-          const bool ok = c < m.n;
+          const int c = c0 + u * cstep;
+          const bool ok = c < cend;
           q[u] = ok ? ws.q[c] : 0.0;
           r[u] = ok ? ws.r[c] : 0.0;
           d[u] = ok ? a.diag[c] : 1.0;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const int c = c0 + u * stride;
-          if (c < m.n) {
-            const double rn = fma(-alpha, q[u], r[u]);
+          const int c = c0 + u * cstep;
+          if (c < cend) {
+            const double rn = fma(-alpha2, q[u], r[u]);
             const double wc = (1.0 / d[u]) * rn;
             ws.r[c] = rn;
             ws.w[c] = wc;
-            if (ws.p2p.P > 0) push_halo(m, ws.p2p.dstW, c, wc);
+            if (HALO && ws.p2p.P > 0) push_halo(m, ws.p2p.dstW, c, wc);
             v2[0] += fabs(rn);
             v2[1] = fma(wc, rn, v2[1]);
           }
         }
       }
     }
-    grid_reduce_sync<2>(v2, ws.partials, bar, ws.gsum->p2, ws.p2p);
-    ++k;
+    LF_TSTAMP(3);
+    grid_reduce_sync<2>(v2, ws.partials, bar, ws.gsum->p2, ws.p2p LF_DBG_ARG(2 * k + 1));
+    LF_TSTAMP(4);
+    if (threadIdx.x == 0) ++st.k;
   }
+  const int k = st.k;
+#if LF_TIMING
+  if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x / 2) && k > 0)
+    printf("LF_TIMING block %d iters %d: phase1 %.2f us, bar1 %.2f us, phase2 %.2f us, bar2 %.2f us\n",
+           blockIdx.x, k, tacc[0] / 1e3 / k, tacc[1] / 1e3 / k, tacc[2] / 1e3 / k, tacc[3] / 1e3 / k);
+  if (threadIdx.x == 0 && blockIdx.x == 0 && k > 4) {
+    const int G = min((int)gridDim.x, LF_DBG_G), NB = min(LF_DBG_N, 2 * k - 2);
+    double acc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+    int cnt[2] = {0, 0};
+    for (int i = 2; i < NB; ++i) {
+      unsigned long long amin = ~0ull, amax = 0, wmax = 0, wsum = 0;
+      int nw = 0;
+      const int last = __ldcg(&g_dbg_last[i]);
+      for (int b = 0; b < G; ++b) {
+        const unsigned long long a = __ldcg(&g_dbg_arr[i][b]);
+        amin = a < amin ? a : amin;
+        amax = a > amax ? a : amax;
+        if (b != last) {
+          const unsigned long long w = __ldcg(&g_dbg_wake[i][b]);
+          wmax = w > wmax ? w : wmax;
+          wsum += w;
+          ++nw;
+        }
+      }
+      const unsigned long long rel = __ldcg(&g_dbg_rel[i]);
+      const int j = i & 1;
+      acc[j][0] += (double)(amax - amin);
+      acc[j][1] += (double)(rel - amax);
+      acc[j][2] += (double)(wmax - rel);
+      acc[j][3] += nw ? (double)(wsum / nw - rel) : 0.0;
+      ++cnt[j];
+    }
+    for (int j = 0; j < 2; ++j)
+      if (cnt[j])
+        printf("LF_BARRIER %d: arrival spread %.2f us, last-arrival->release %.2f us, "
+               "release->last wake %.2f us (mean wake %.2f us)\n", j + 1, acc[j][0] / 1e3 / cnt[j],
+               acc[j][1] / 1e3 / cnt[j], acc[j][2] / 1e3 / cnt[j], acc[j][3] / 1e3 / cnt[j]);
+  }
+#endif
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     ctl->it = k;
     ctl->stop = 1;
-    ctl->singular = singular ? 1 : 0;
-    ctl->converged = conv(finRes, initRes, ctl) ? 1 : 0;
-    ctl->normFactor = nf;
-    ctl->initRes = initRes;
-    ctl->finRes = finRes;
-    ctl->wArA = wArA;
-    ctl->alpha = alpha;
+    ctl->singular = st.singular;
+    ctl->converged = conv(st.finRes, st.initRes, ctl) ? 1 : 0;
+    ctl->normFactor = st.nf;
+    ctl->initRes = st.initRes;
+    ctl->finRes = st.finRes;
+    ctl->wArA = st.wArA;
+    ctl->alpha = st.alpha;
   }
 }
 
 int persistent_grid(int device, int K) {
   int sms = 0, nb = 0;
   LF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-  const void *fn = K == 4 ? (const void *)k_pcg_persistent<4>
-                          : (K > 0 ? (const void *)k_pcg_persistent<3> : (const void *)k_pcg_persistent<0>);
-  LF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, BS, 0));
-  return sms * (nb < 1 ? 1 : nb);
+  // the grid must be co-resident for every variant that may be launched
+  const void *fns[2] = {K == 4 ? (const void *)k_pcg_persistent<4, false>
+                               : (K > 0 ? (const void *)k_pcg_persistent<3, false> : (const void *)k_pcg_persistent<0, false>),
+                        K == 4 ? (const void *)k_pcg_persistent<4, true>
+                               : (K > 0 ? (const void *)k_pcg_persistent<3, true> : (const void *)k_pcg_persistent<0, true>)};
+  int best = 1 << 30;
+  for (const void *fn : fns) {
+    LF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, BS, 0));
+    best = std::min(best, nb);
+  }
+  return sms * (best < 1 ? 1 : best);
+}
+
+template <bool HALO>
+static const void *persistent_fn(const MeshDev &m) {
+  return (!LF_NO_ELL && m.K == 4) ? (const void *)k_pcg_persistent<4, HALO>
+         : (!LF_NO_ELL && m.K > 0) ? (const void *)k_pcg_persistent<3, HALO>
+                                   : (const void *)k_pcg_persistent<0, HALO>;
 }
 
 void launch_pcg_persistent(cudaStream_t s, int grid, const MeshDev &m, const LduDev &a,
                            const Workspace &ws, unsigned *bar) {
   void *args[] = {(void *)&m, (void *)&a, (void *)&ws, (void *)&bar};
-  const void *fn = (!LF_NO_ELL && m.K == 4) ? (const void *)k_pcg_persistent<4>
-                   : (!LF_NO_ELL && m.K > 0) ? (const void *)k_pcg_persistent<3>
-                                             : (const void *)k_pcg_persistent<0>;
+  const bool halo = m.hasProc || ws.p2p.P > 0;
+  const void *fn = halo ? persistent_fn<true>(m) : persistent_fn<false>(m);
   LF_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(BS), args, 0, s));
 }
 

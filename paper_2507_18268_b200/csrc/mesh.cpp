@@ -393,7 +393,11 @@ static void build_mesh(lf_context *ctx, const lf_mesh_desc *d, lf_mesh *M) {
   M->Lamul = grid(3);
   M->Lsetup = grid(4);
   M->Lsum = grid(5);
-  M->persistentGrid = balanced(persistent_grid(ctx->device, md.K));
+  // persistent kernel: contiguous chunks on an SM-uniform grid (every SM
+  // holds the same number of blocks), or balanced grid-stride trips
+  M->persistentGrid = persistent_chunked()
+                          ? std::max(1, std::min(persistent_grid(ctx->device, md.K), (int)((n + 31) / 32)))
+                          : balanced(persistent_grid(ctx->device, md.K));
   int maxGrid = std::max({M->Lasm.grid, M->Lp1.grid, M->Lp2.grid, M->Lamul.grid, M->Lsetup.grid, M->Lsum.grid,
                           M->persistentGrid});
   M->gridBar = A.alloc<unsigned>(2);

@@ -109,7 +109,9 @@ def lib():
             raise ImportError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
         L = C.CDLL(LIB_PATH)
         for name, (res, args) in SIGNATURES.items():
-            fn = getattr(L, name)
+            fn = getattr(L, name, None)
+            if fn is None:  # older experiment variant (LFOAM_LIB); the shipped build exports all
+                continue
             fn.restype = res
             fn.argtypes = args
         _lib = L
