@@ -380,9 +380,13 @@ static void build_mesh(lf_context *ctx, const lf_mesh_desc *d, lf_mesh *M) {
   // (e.g. 1M cells: 652 blocks x 6 trips instead of 740 blocks doing 5 or 6),
   // so no block idles at the phase end (ncu r1j: 31% of warp samples waited
   // at the grid barrier with the unbalanced grid).
+#ifndef LF_SMUNIFORM
+#define LF_SMUNIFORM 0
+#endif
   auto balanced = [&](int g0) {
     const int need = (int)((n + BSZ - 1) / BSZ);
     if (need <= g0) return std::max(1, need);
+    if (LF_SMUNIFORM) return g0;  // every SM holds the same number of blocks
     const int T = (need + g0 - 1) / g0;
     return (need + T - 1) / T;
   };
