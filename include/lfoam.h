@@ -90,6 +90,8 @@ typedef struct {
                                   sides (e.g. ascending global face id).  neighb_rank ==
                                   own rank: coupled to the NEXT processor patch that also
                                   names the own rank (self pairs, a loopback used by tests). */
+  const double *sf;            /* host [n_faces][3] outward area vectors, or NULL; required by
+                                  lf_fvc_grad / the corrected laplacian (with lf_mesh_desc.sf) */
 } lf_patch_desc;
 
 typedef struct {
@@ -104,6 +106,14 @@ typedef struct {
   const lf_patch_desc *patches;/* host [n_patches]                                          */
   int32_t renumber;            /* 0 keep numbering; 1 reverse Cuthill-McKee inside the
                                   library (fields still speak the caller's numbering)      */
+  /* Full geometry (all NULL, or all set together with every non-empty patch's
+   * sf; c != NULL marks a geometry mesh, sf/cf may be NULL only if n_faces == 0): the
+   * non-orthogonal correction path (fvc::grad and the
+   * Gauss linear corrected laplacian).  Then delta_coeffs must be OpenFOAM's
+   * nonOrthDeltaCoeffs 1/max(n.d, 0.05|d|). */
+  const double *sf;            /* host [n_faces][3] area vectors, owner -> neighbour      */
+  const double *cf;            /* host [n_faces][3] face centres                          */
+  const double *c;             /* host [n_cells][3] cell centres                          */
 } lf_mesh_desc;
 
 typedef struct lf_mesh lf_mesh;
@@ -172,6 +182,14 @@ LF_API lf_status field_get(const lf_mesh *mesh, lf_field f, int32_t patch, doubl
 typedef struct {
   double DT;   /* uniform diffusivity > 0 (reading A11)   */
   double dt;   /* time step > 0 (P:608 uses 0.2 s)        */
+  int32_t corrected;   /* 0: orthogonal two-point laplacian (A4).  1: Gauss linear
+                          corrected — adds the explicit non-orthogonal correction
+                          +V div(DT|Sf| corrVec . interpolate(grad T)) to the source
+                          (needs full geometry; no processor patches)            */
+  int32_t n_non_orth_correctors;  /* laplacianFoam_step: extra corrector passes per
+                          step (simple.correctNonOrthogonal()); each pass
+                          re-evaluates the correction from the current T and solves
+                          again from it, ddt keeping T0 of the step (0 = one pass) */
 } lf_laplacian_params;
 
 typedef struct lf_ldu lf_ldu;   /* owned by its mesh, reused every step */
@@ -179,9 +197,21 @@ typedef struct lf_ldu lf_ldu;   /* owned by its mesh, reused every step */
 /* fvm::ddt(T) - fvm::laplacian(DT,T) with T0 = current T (Listing 1
  * line 12; readings A3-A5): per internal face u = delta*(DT*magSf),
  * upper = -u; diag = V/dt + sum u (+ boundary internalCoeffs);
- * source = (T0/dt)*V (+ fixedValue boundaryCoeffs).  One kernel, a per-cell
- * gather (no float atomics); deterministic.  Errors: DT/dt <= 0 -> INVALID_ARG. */
+ * source = (T0/dt)*V (+ fixedValue boundaryCoeffs), with p->corrected the
+ * explicit non-orthogonal correction of T as well.  One kernel, a per-cell
+ * gather (no float atomics); deterministic.  Errors: DT/dt <= 0, corrected
+ * without geometry or with processor patches -> INVALID_ARG. */
 LF_API lf_status laplacian_assemble(lf_mesh *mesh, const lf_laplacian_params *p, lf_ldu **sys);
+
+/* fvc::grad(x) with gaussGrad + linear interpolation — the kernels the paper
+ * ported (§5.2: weights P:321-334, interpolation/dotInterpolate P:293-315,
+ * gradf owner/neighbour and boundary gathers P:435-497, field division
+ * P:503-528) — as atomic-free per-cell gathers, plus correctBoundaryConditions
+ * (P:539-556).  x_dev: device [n_cells] (internal numbering); boundary values
+ * from the mesh's patches (fixedValue T_b, zeroGradient x[faceCell]).
+ * grad_dev: device [n_cells][3]; bgrad_dev: device [boundary faces][3] (patch
+ * order) or NULL.  Needs full geometry and no processor patches. */
+LF_API lf_status lf_fvc_grad(lf_mesh *mesh, const double *x_dev, double *grad_dev, double *bgrad_dev);
 
 /* Host copies in the CALLER's numbering and face order; any pointer may be
  * NULL.  internal/boundary_coeffs: [total boundary faces] in patch order
@@ -215,8 +245,10 @@ typedef struct {
 LF_API lf_status pcg_solve(lf_ldu *sys, double *psi_dev, const lf_solver_controls *c, lf_solver_perf *out);
 
 /* n_steps laplacianFoam time steps on the mesh's T field: each step
- * assembles (fused with the PCG setup) and solves in place (Listing 1).
- * per_step: host [n_steps] or NULL. */
+ * assembles (fused with the PCG setup) and solves in place (Listing 1), with
+ * 1 + n_non_orth_correctors passes when p->corrected.
+ * per_step: host [n_steps * (1 + (corrected ? n_non_orth_correctors : 0))]
+ * (one entry per solve) or NULL. */
 LF_API lf_status laplacianFoam_step(lf_mesh *mesh, const lf_laplacian_params *p,
                              const lf_solver_controls *c, int32_t n_steps,
                              lf_solver_perf *per_step);
@@ -227,7 +259,8 @@ typedef enum {
   LF_K_ASSEMBLE = 0, LF_K_SETUP = 1, LF_K_PHASE1 = 2, LF_K_PHASE2 = 3,
   LF_K_AMUL = 4, LF_K_SUMPSI = 5, LF_K_PACK = 6,
   LF_K_PCG = 7,      /* persistent whole-solve kernel (single rank, no processor patches) */
-  LF_K_COUNT = 8
+  LF_K_NONORTH = 8,  /* gradient / non-orthogonal correction kernels (lf_fvc_grad, corrected) */
+  LF_K_COUNT = 9
 } lf_kernel_kind;
 
 /* Execution options of a context (all default 1):

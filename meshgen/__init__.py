@@ -14,9 +14,11 @@ dt=0.2, fixedValue 0 walls, T0 = sin(pi x) sin(pi y) sin(pi z).
 from .cube import (Mesh, Patch, block_mesh, permute_mesh, sine_field, canonical_field,
                    CANONICAL_AMPLITUDE,
                    cosine_field, multimode_field, random_field, hot_plate,
-                   cube_counts, mesh_points_faces, CONFIGS, config_mesh)
+                   cube_counts, mesh_points_faces, CONFIGS, config_mesh,
+                   skewed_block_mesh, with_geometry, PATCH_NAMES)
 
 __all__ = ["Mesh", "Patch", "block_mesh", "permute_mesh", "sine_field", "canonical_field",
            "CANONICAL_AMPLITUDE",
            "cosine_field", "multimode_field", "random_field", "hot_plate",
-           "cube_counts", "mesh_points_faces", "CONFIGS", "config_mesh"]
+           "cube_counts", "mesh_points_faces", "CONFIGS", "config_mesh",
+           "skewed_block_mesh", "with_geometry", "PATCH_NAMES"]

@@ -35,6 +35,8 @@ class Patch:
     value: np.ndarray              # f64 [nf]  fixedValue T_b (ignored otherwise)
     neighb_rank: int = -1          # processor patches only
     global_faces: Optional[np.ndarray] = None  # processor: global face ids (ordering key)
+    Sf: Optional[np.ndarray] = None  # [nf,3] outward face area vectors (full-geometry meshes)
+    Cf: Optional[np.ndarray] = None  # [nf,3] face centres
 
     @property
     def n_faces(self) -> int:
@@ -55,6 +57,13 @@ class Mesh:
     old_of_new: Optional[np.ndarray] = None   # permuted meshes: block label of each cell
     face_old_of_new: Optional[np.ndarray] = None
     cell_global: Optional[np.ndarray] = None  # decomposed meshes: global (block) label per local cell
+    # full geometry (non-orthogonal correction path):
+    # face area vectors / face centres of internal faces [F,3], cell centres [n,3]
+    Sf: Optional[np.ndarray] = None
+    Cf: Optional[np.ndarray] = None
+    C: Optional[np.ndarray] = None
+    affine: Optional[np.ndarray] = None       # 3x3 map applied to the unit block (skewed meshes)
+    grid_lines: Optional[tuple] = None        # graded blocks: grid-line coordinates per axis
 
     @property
     def n_faces(self) -> int:
@@ -74,6 +83,8 @@ class Mesh:
         return lab
 
     def cell_centres(self) -> np.ndarray:
+        if self.C is not None:
+            return self.C
         nx, ny, nz = self.dims
         hx, hy, hz = (self.extent[0] / nx, self.extent[1] / ny, self.extent[2] / nz)
         lab = self.block_labels()
@@ -149,6 +160,91 @@ def block_mesh(nx: int, ny: Optional[int] = None, nz: Optional[int] = None,
                 dims=(nx, ny, nz), extent=(Lx, Ly, Lz))
 
 
+def _grid_lines(n: int, ratio: float) -> np.ndarray:
+    """n+1 grid lines on [0,1], cell sizes growing geometrically by `ratio`."""
+    if abs(ratio - 1.0) < 1e-15:
+        return np.arange(n + 1) / n
+    sizes = ratio ** np.arange(n)
+    return np.concatenate([[0.0], np.cumsum(sizes) / sizes.sum()])
+
+
+def skewed_block_mesh(nx: int, ny: Optional[int] = None, nz: Optional[int] = None,
+                      shear: Sequence[float] = (0.3, 0.0, 0.2),
+                      bc: Optional[Dict[str, object]] = None,
+                      grading: Sequence[float] = (1.0, 1.0, 1.0)) -> Mesh:
+    """Graded unit block mapped by the shear x' = A x, A = [[1, sxy, sxz],
+    [0, 1, syz], [0, 0, 1]] (det 1): parallelepiped cells, planar faces,
+    NON-orthogonal internal faces and, with grading != 1 (geometric cell
+    growth per axis), interpolation weights != 1/2 — the input of the
+    corrected laplacian.
+
+    Full geometry in closed form from the axis-aligned boxes: C' = A C,
+    Cf' = A Cf, Sf' = det(A) A^-T Sf, V' = det(A) V.  deltaCoeffs are
+    OpenFOAM's nonOrthDeltaCoeffs 1/max(n.d, 0.05|d|) with d = C_N - C_P
+    (internal) or Cf - C_P (boundary)."""
+    m = block_mesh(nx, ny, nz, bc=bc)
+    nx, ny, nz = m.dims
+    sxy, sxz, syz = (float(s) for s in shear)
+    A = np.array([[1.0, sxy, sxz], [0.0, 1.0, syz], [0.0, 0.0, 1.0]])
+    det = float(np.linalg.det(A))
+    AinvT = np.linalg.inv(A).T
+    L = [_grid_lines(nx, grading[0]), _grid_lines(ny, grading[1]), _grid_lines(nz, grading[2])]
+    H = [np.diff(l) for l in L]
+    M = [0.5 * (l[1:] + l[:-1]) for l in L]
+    lab = np.arange(m.n_cells, dtype=np.int64)
+    I = np.stack([lab % nx, (lab // nx) % ny, lab // (nx * ny)], 1)
+    C0 = np.stack([M[0][I[:, 0]], M[1][I[:, 1]], M[2][I[:, 2]]], 1)
+    V0 = H[0][I[:, 0]] * H[1][I[:, 1]] * H[2][I[:, 2]]
+    ax = np.argmax(I[m.neighbour] - I[m.owner], axis=1)
+    E = np.eye(3)
+    Io = I[m.owner]
+    Cf0 = C0[m.owner].copy()
+    area0 = np.empty(m.n_faces)
+    for a in range(3):
+        sel = ax == a
+        Cf0[sel, a] = L[a][Io[sel, a] + 1]
+        b, c = [d for d in range(3) if d != a]
+        area0[sel] = H[b][Io[sel, b]] * H[c][Io[sel, c]]
+    Sf0 = area0[:, None] * E[ax]
+    tr = lambda X: X @ A.T
+    C = tr(C0)
+    Cf = tr(Cf0)
+    Sf = det * (Sf0 @ AinvT.T)
+    magSf = np.linalg.norm(Sf, axis=1)
+    d = C[m.neighbour] - C[m.owner]
+    nd = np.einsum("ij,ij->i", Sf / magSf[:, None], d)
+    delta = 1.0 / np.maximum(nd, 0.05 * np.linalg.norm(d, axis=1))
+    patches = []
+    for p_i, p in enumerate(m.patches):
+        a, hi = p_i // 2, p_i % 2
+        sgn = 1.0 if hi else -1.0
+        Ip = I[p.face_cells]
+        cf0 = C0[p.face_cells].copy()
+        cf0[:, a] = L[a][Ip[:, a] + (1 if hi else 0)]
+        b, c = [dd for dd in range(3) if dd != a]
+        sf0 = (sgn * H[b][Ip[:, b]] * H[c][Ip[:, c]])[:, None] * E[a]
+        pcf, psf = tr(cf0), det * (sf0 @ AinvT.T)
+        pmag = np.linalg.norm(psf, axis=1)
+        db = pcf - C[p.face_cells]
+        ndb = np.einsum("ij,ij->i", psf / pmag[:, None], db)
+        pdel = 1.0 / np.maximum(ndb, 0.05 * np.linalg.norm(db, axis=1))
+        patches.append(dataclasses.replace(p, mag_sf=pmag, delta=pdel, Sf=psf, Cf=pcf))
+    return dataclasses.replace(m, mag_sf=magSf, delta=delta, V=det * V0,
+                               patches=patches, Sf=Sf, Cf=Cf, C=C, affine=A,
+                               grid_lines=tuple(L))
+
+
+def with_geometry(m: Mesh) -> Mesh:
+    """Attach the full geometry (Sf, Cf, C) of an unsheared block mesh."""
+    g = skewed_block_mesh(*m.dims, shear=(0.0, 0.0, 0.0),
+                          bc={p.name: (p.type if p.type != "fixedValue" else ("fixedValue", 0.0))
+                              for p in m.patches})
+    # keep the boundary values of m (skewed_block_mesh sets uniform ones)
+    patches = [dataclasses.replace(gp, value=np.array(p.value, dtype=np.float64, copy=True))
+               for gp, p in zip(g.patches, m.patches)]
+    return dataclasses.replace(g, patches=patches)
+
+
 def permute_mesh(mesh: Mesh, cell_seed: int = 1, face_seed: int = 2) -> Mesh:
     """Reading A24: random cell labels pi_c, random face order pi_f,
     owner = min(pi_c(P), pi_c(N)), neighbour = max."""
@@ -166,9 +262,17 @@ def permute_mesh(mesh: Mesh, cell_seed: int = 1, face_seed: int = 2) -> Mesh:
     base = mesh.block_labels()
     patches = [dataclasses.replace(p, face_cells=new_of_old[p.face_cells].astype(np.int32))
                for p in mesh.patches]
+    geo = {}
+    if mesh.Sf is not None:
+        # Sf points owner -> neighbour: flip where the relabelled pair swapped
+        sgn = np.where(a > b, -1.0, 1.0)[:, None]
+        C = np.empty_like(mesh.C)
+        C[new_of_old] = mesh.C
+        geo = dict(Sf=mesh.Sf[fperm] * sgn, Cf=mesh.Cf[fperm].copy(), C=C, affine=mesh.affine,
+                   grid_lines=mesh.grid_lines)
     return Mesh(n, owner, neighbour, mesh.mag_sf[fperm], mesh.delta[fperm], V, patches,
                 dims=mesh.dims, extent=mesh.extent,
-                old_of_new=base[old_of_new].astype(np.int32), face_old_of_new=fperm)
+                old_of_new=base[old_of_new].astype(np.int32), face_old_of_new=fperm, **geo)
 
 
 # ----------------------------------------------------------------- fields
@@ -241,7 +345,13 @@ def mesh_points_faces(mesh: Mesh):
     I, J, K = np.meshgrid(np.arange(nx + 1), np.arange(ny + 1), np.arange(nz + 1), indexing="ij")
     pts = np.zeros(((nx + 1) * (ny + 1) * (nz + 1), 3))
     pid = lambda i, j, k: i + (nx + 1) * (j + (ny + 1) * k)
-    pts[pid(I, J, K).ravel()] = np.stack([I.ravel() * hx, J.ravel() * hy, K.ravel() * hz], axis=1)
+    if mesh.grid_lines is not None:
+        gx, gy, gz = mesh.grid_lines
+        pts[pid(I, J, K).ravel()] = np.stack([gx[I.ravel()], gy[J.ravel()], gz[K.ravel()]], axis=1)
+    else:
+        pts[pid(I, J, K).ravel()] = np.stack([I.ravel() * hx, J.ravel() * hy, K.ravel() * hz], axis=1)
+    if mesh.affine is not None:
+        pts = pts @ mesh.affine.T
 
     def quad(ax, i, j, k, outward_positive):
         # face of cell (i,j,k) on its +ax side

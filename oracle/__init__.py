@@ -42,7 +42,8 @@ class _Mesh(C.Structure):
                 ("n_bfaces", C.c_int32), ("owner", C.c_void_p), ("neighbour", C.c_void_p),
                 ("mag_sf", C.c_void_p), ("delta", C.c_void_p), ("V", C.c_void_p),
                 ("patch_type", C.c_void_p), ("patch_start", C.c_void_p), ("b_cells", C.c_void_p),
-                ("b_mag_sf", C.c_void_p), ("b_delta", C.c_void_p)]
+                ("b_mag_sf", C.c_void_p), ("b_delta", C.c_void_p),
+                ("Sf", C.c_void_p), ("Cf", C.c_void_p), ("C", C.c_void_p), ("b_Sf", C.c_void_p)]
 
 
 class Perf(C.Structure):
@@ -76,6 +77,14 @@ def lib():
                                             C.c_int32, C.c_double, C.c_double, C.c_int32,
                                             C.c_int32, GSUM, HALO, vp, C.POINTER(Perf)]
         _lib.orc_patch_values.argtypes = [C.POINTER(_Mesh), vp, vp]
+        _lib.orc_weights.argtypes = [C.POINTER(_Mesh), vp]
+        _lib.orc_corr_vectors.argtypes = [C.POINTER(_Mesh), vp]
+        _lib.orc_grad.argtypes = [C.POINTER(_Mesh), vp, vp, vp, vp]
+        _lib.orc_grad_bc.argtypes = [C.POINTER(_Mesh), vp, vp, vp, vp]
+        _lib.orc_lap_correction.argtypes = [C.POINTER(_Mesh), C.c_double, vp, vp, vp, vp]
+        _lib.orc_laplacian_foam_corrected.argtypes = [C.POINTER(_Mesh), C.c_double, C.c_double, vp, vp,
+                                                      C.c_int32, C.c_int32, C.c_double, C.c_double,
+                                                      C.c_int32, C.c_int32, C.POINTER(Perf)]
     return _lib
 
 
@@ -104,10 +113,23 @@ class OMesh:
         self.b_value = cat("value", np.float64)
         self.n_cells, self.n_faces = int(mesh.n_cells), int(self.owner.shape[0])
         self.n_bfaces = int(self.b_cells.shape[0])
+        g = lambda a: None if a is None else np.ascontiguousarray(a, dtype=np.float64)
+        self.Sf, self.Cf = g(getattr(mesh, "Sf", None)), g(getattr(mesh, "Cf", None))
+        self.C = g(getattr(mesh, "C", None))
+        if all(getattr(p, "Sf", None) is not None for p in mesh.patches):
+            self.b_Sf = (np.ascontiguousarray(np.concatenate([p.Sf for p in mesh.patches]), dtype=np.float64)
+                         if mesh.patches else np.zeros((0, 3)))
+        else:
+            self.b_Sf = None
         self.s = _Mesh(self.n_cells, self.n_faces, len(sizes), self.n_bfaces,
                        _p(self.owner), _p(self.neighbour), _p(self.mag_sf), _p(self.delta),
                        _p(self.V), _p(self.patch_type), _p(self.patch_start), _p(self.b_cells),
-                       _p(self.b_mag_sf), _p(self.b_delta))
+                       _p(self.b_mag_sf), _p(self.b_delta), _p(self.Sf), _p(self.Cf), _p(self.C),
+                       _p(self.b_Sf))
+
+    @property
+    def has_geometry(self):
+        return self.Sf is not None and self.Cf is not None and self.C is not None and self.b_Sf is not None
 
     def patch_slices(self):
         return [slice(int(self.patch_start[i]), int(self.patch_start[i + 1]))
@@ -227,3 +249,67 @@ def self_halo(mesh):
             xr[sl[a]] = x[om.b_cells[sl[b]]]
             xr[sl[b]] = x[om.b_cells[sl[a]]]
     return halo
+
+
+# ------------------------------------------- non-orthogonal correction path
+def _need_geom(om):
+    if not om.has_geometry:
+        raise ValueError("mesh has no full geometry (Sf, Cf, C, patch Sf)")
+
+
+def weights(mesh):
+    """Owner interpolation weights (Listing 'weights parallel loop')."""
+    om = _om(mesh)
+    _need_geom(om)
+    w = np.zeros(om.n_faces)
+    lib().orc_weights(C.byref(om.s), _p(w))
+    return w
+
+
+def corr_vectors(mesh):
+    om = _om(mesh)
+    _need_geom(om)
+    cv = np.zeros((om.n_faces, 3))
+    lib().orc_corr_vectors(C.byref(om.s), _p(cv))
+    return cv
+
+
+def grad(mesh, x, b_value=None):
+    """Green-Gauss cell gradient [n,3] (gaussGrad::gradf, P:375-505) and the
+    corrected boundary gradient [B,3] (correctBoundaryConditions)."""
+    om = _om(mesh)
+    _need_geom(om)
+    x = np.ascontiguousarray(x, np.float64)
+    bv = om.b_value if b_value is None else np.ascontiguousarray(b_value, np.float64)
+    w = weights(om)
+    g = np.zeros((om.n_cells, 3))
+    lib().orc_grad(C.byref(om.s), _p(w), _p(x), _p(bv), _p(g))
+    bg = np.zeros((om.n_bfaces, 3))
+    lib().orc_grad_bc(C.byref(om.s), _p(x), _p(bv), _p(g), _p(bg))
+    return g, bg
+
+
+def lap_correction(mesh, DT, g):
+    """Source contribution -V*div(gammaMagSf*(corr & interpolate(grad)))."""
+    om = _om(mesh)
+    _need_geom(om)
+    w, cv = weights(om), corr_vectors(om)
+    out = np.zeros(om.n_cells)
+    lib().orc_lap_correction(C.byref(om.s), DT, _p(w), _p(cv), _p(np.ascontiguousarray(g, np.float64)), _p(out))
+    return out
+
+
+def laplacian_foam_corrected(mesh, T0, n_steps, n_corr=1, DT=1.0, dt=0.2, tol=1e-10, rel_tol=0.0,
+                             max_iter=1000, min_iter=0, b_value=None):
+    """Listing 1 with Gauss linear corrected laplacian and n_corr non-orthogonal
+    correctors per step.  Returns (T, b_value, [perf per corrector solve])."""
+    om = _om(mesh)
+    _need_geom(om)
+    T = np.array(T0, dtype=np.float64, copy=True)
+    bv = np.array(om.b_value if b_value is None else b_value, dtype=np.float64, copy=True)
+    perfs = (Perf * max(n_steps * (n_corr + 1), 1))()
+    rc = lib().orc_laplacian_foam_corrected(C.byref(om.s), DT, dt, _p(T), _p(bv), n_steps, n_corr, tol,
+                                            rel_tol, max_iter, min_iter, perfs)
+    if rc:
+        raise MemoryError
+    return T, bv, [perfs[i].as_dict() for i in range(n_steps * (n_corr + 1))]

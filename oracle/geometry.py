@@ -76,4 +76,4 @@ def mesh_geometry(mesh, points, faces):
     np.add.at(closure, owner_all, Sf)
     np.add.at(closure, nb, -Sf[:F])
     return dict(mag_sf=magSf[:F], delta=delta, V=V, b_mag_sf=magSf[F:], b_delta=b_delta,
-                closure=closure, Sf=Sf, C=C)
+                closure=closure, Sf=Sf, Cf=Cf, C=C)

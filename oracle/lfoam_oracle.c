@@ -47,6 +47,10 @@ typedef struct {
     const int32_t *patch_start;            /* [n_patches+1] into the flat boundary arrays */
     const int32_t *b_cells;                /* [n_bfaces] faceCells */
     const double *b_mag_sf, *b_delta;      /* [n_bfaces] */
+    /* full geometry (optional, NULL if absent): non-orthogonal correction */
+    const double *Sf, *Cf;                 /* [n_faces][3] */
+    const double *C;                       /* [n_cells][3] */
+    const double *b_Sf;                    /* [n_bfaces][3] */
 } orc_mesh;
 
 typedef struct {
@@ -322,5 +326,174 @@ int orc_laplacian_foam(const orc_mesh *m, double DT, double dt, double *T,
         orc_patch_values(m, T, b_value);
     }
     free(diag); free(source); free(upper); free(b_int); free(b_bnd);
+    return rc;
+}
+
+/* ================================================================ *
+ * Non-orthogonal correction path: the gradient *
+ * kernels the paper ported (§5.2) and the corrected Gauss laplacian. *
+ * ================================================================ */
+#define ORC_ROOTVSMALL 1e-150
+
+/* weights, Listing "weights parallel loop": the owner weight
+ * lambda = SfdNei / (SfdOwn + SfdNei), 0.5 if the sum is below ROOTVSMALL. */
+void orc_weights(const orc_mesh *m, double *w)
+{
+    int32_t f, k;
+    for (f = 0; f < m->n_faces; f++) {
+        const double *s = m->Sf + 3 * f, *cf = m->Cf + 3 * f;
+        const double *cp = m->C + 3 * m->owner[f], *cn = m->C + 3 * m->neighbour[f];
+        double so = 0.0, sn = 0.0;
+        for (k = 0; k < 3; k++) {
+            so += s[k] * (cf[k] - cp[k]);
+            sn += s[k] * (cn[k] - cf[k]);
+        }
+        so = fabs(so);
+        sn = fabs(sn);
+        w[f] = fabs(so + sn) > ORC_ROOTVSMALL ? sn / (so + sn) : 0.5;
+    }
+}
+
+/* surfaceInterpolation::nonOrthCorrectionVectors: n - d * deltaCoeffs with
+ * n = Sf/|Sf| and d = C_N - C_P (deltaCoeffs = the mesh's nonOrthDeltaCoeffs). */
+void orc_corr_vectors(const orc_mesh *m, double *corr)
+{
+    int32_t f, k;
+    for (f = 0; f < m->n_faces; f++) {
+        const double *cp = m->C + 3 * m->owner[f], *cn = m->C + 3 * m->neighbour[f];
+        for (k = 0; k < 3; k++) {
+            double nk = m->Sf[3 * f + k] / m->mag_sf[f];
+            double dk = cn[k] - cp[k];
+            corr[3 * f + k] = nk - dk * m->delta[f];
+        }
+    }
+}
+
+/* Boundary value of x on boundary face i (the patch field after evaluate):
+ * fixedValue T_b, zeroGradient x[faceCell]. */
+static double orc_patch_value(const orc_mesh *m, int32_t p, int32_t i, const double *x, const double *b_value)
+{
+    return m->patch_type[p] == ORC_FIXED_VALUE ? b_value[i] : x[m->b_cells[i]];
+}
+
+/* gaussGrad::gradf with linear interpolation, as the SERIAL scatter loops the
+ * paper starts from: Listing "First cycle in the gradf routine" (P:375-382:
+ * igGrad[owner] += Sf*ssf, igGrad[neighbour] -= Sf*ssf), Listing "Second cycle
+ * gradient" (igGrad[faceCells] += pSf*pssf) and "Field division"
+ * (igGrad /= V).  ssf = lambda*(x_P - x_N) + x_N (Listing
+ * "dotInterpolate loop" form). */
+void orc_grad(const orc_mesh *m, const double *w, const double *x, const double *b_value, double *grad)
+{
+    int32_t c, f, p, i, k;
+    for (c = 0; c < 3 * m->n_cells; c++) grad[c] = 0.0;
+    for (f = 0; f < m->n_faces; f++) {
+        const int32_t P = m->owner[f], N = m->neighbour[f];
+        const double ssf = w[f] * (x[P] - x[N]) + x[N];
+        for (k = 0; k < 3; k++) {
+            const double sfssf = m->Sf[3 * f + k] * ssf;
+            grad[3 * P + k] += sfssf;
+            grad[3 * N + k] -= sfssf;
+        }
+    }
+    for (p = 0; p < m->n_patches; p++)
+        for (i = m->patch_start[p]; i < m->patch_start[p + 1]; i++) {
+            const double pssf = orc_patch_value(m, p, i, x, b_value);
+            for (k = 0; k < 3; k++) grad[3 * m->b_cells[i] + k] += m->b_Sf[3 * i + k] * pssf;
+        }
+    for (c = 0; c < m->n_cells; c++)
+        for (k = 0; k < 3; k++) grad[3 * c + k] /= m->V[c];
+}
+
+/* correctBoundaryConditions of the gradient (Listing "CorrectBoundaryConditions",
+ * P:539-556): gb = grad[faceCell] (extrapolated), then on non-coupled patches
+ * gb += n*(snGrad - n.gb) with snGrad = deltaCoeffs*(T_b - T_c) (fixedValue),
+ * 0 (zeroGradient). */
+void orc_grad_bc(const orc_mesh *m, const double *x, const double *b_value, const double *grad, double *bgrad)
+{
+    int32_t p, i, k;
+    for (p = 0; p < m->n_patches; p++)
+        for (i = m->patch_start[p]; i < m->patch_start[p + 1]; i++) {
+            const int32_t c = m->b_cells[i];
+            double n[3], ng = 0.0, sng;
+            for (k = 0; k < 3; k++) {
+                bgrad[3 * i + k] = grad[3 * c + k];
+                n[k] = m->b_Sf[3 * i + k] / m->b_mag_sf[i];
+            }
+            if (m->patch_type[p] == ORC_PROCESSOR) continue;  /* coupled: untouched */
+            for (k = 0; k < 3; k++) ng += n[k] * bgrad[3 * i + k];
+            sng = m->patch_type[p] == ORC_FIXED_VALUE ? m->b_delta[i] * (b_value[i] - x[c]) : 0.0;
+            for (k = 0; k < 3; k++) bgrad[3 * i + k] += n[k] * (sng - ng);
+        }
+}
+
+/* Explicit non-orthogonal part of the corrected Gauss laplacian
+ * (gaussLaplacianScheme::fvmLaplacian): fvm.source() -= V*fvc::div(gammaMagSf *
+ * (corrVecs & interpolate(grad T))).  Returns that source contribution
+ * lapSrc[c] = -(V * div)[c]; boundary corrections are zero (non-coupled). */
+void orc_lap_correction(const orc_mesh *m, double DT, const double *w, const double *corr,
+                        const double *grad, double *lapSrc)
+{
+    int32_t c, f, k;
+    for (c = 0; c < m->n_cells; c++) lapSrc[c] = 0.0;
+    for (f = 0; f < m->n_faces; f++) {
+        const int32_t P = m->owner[f], N = m->neighbour[f];
+        double cs = 0.0, flux;
+        for (k = 0; k < 3; k++) {  /* dotInterpolate(corr, grad) */
+            const double gf = w[f] * (grad[3 * P + k] - grad[3 * N + k]) + grad[3 * N + k];
+            cs += corr[3 * f + k] * gf;
+        }
+        flux = (DT * m->mag_sf[f]) * cs;
+        lapSrc[P] += flux;   /* surfaceIntegrate: owner +, neighbour - */
+        lapSrc[N] -= flux;
+    }
+    for (c = 0; c < m->n_cells; c++) lapSrc[c] = -(m->V[c] * (lapSrc[c] / m->V[c]));
+}
+
+/* Listing 1 with the non-orthogonal corrector loop: every step keeps
+ * T0 (old time) for ddt, and runs n_corr + 1 passes, each assembling with
+ * the explicit correction of the CURRENT T and solving from it.
+ * perf: [n_steps * (n_corr + 1)]. */
+int orc_laplacian_foam_corrected(const orc_mesh *m, double DT, double dt, double *T,
+                                 double *b_value, int32_t n_steps, int32_t n_corr, double tol,
+                                 double rel_tol, int32_t max_iter, int32_t min_iter, orc_perf *perf)
+{
+    size_t nn = (size_t)(m->n_cells > 0 ? m->n_cells : 1);
+    size_t nf = (size_t)(m->n_faces > 0 ? m->n_faces : 1);
+    size_t nb = (size_t)(m->n_bfaces > 0 ? m->n_bfaces : 1);
+    double *diag = (double *)malloc(nn * sizeof(double)), *source = (double *)malloc(nn * sizeof(double));
+    double *upper = (double *)malloc(nf * sizeof(double)), *w = (double *)malloc(nf * sizeof(double));
+    double *corr = (double *)malloc(3 * nf * sizeof(double)), *grad = (double *)malloc(3 * nn * sizeof(double));
+    double *lapSrc = (double *)malloc(nn * sizeof(double)), *T0 = (double *)malloc(nn * sizeof(double));
+    double *b_int = (double *)malloc(nb * sizeof(double)), *b_bnd = (double *)malloc(nb * sizeof(double));
+    int32_t s, k, c;
+    int rc = 0;
+    if (!diag || !source || !upper || !w || !corr || !grad || !lapSrc || !T0 || !b_int || !b_bnd) return 2;
+    orc_weights(m, w);
+    orc_corr_vectors(m, corr);
+    for (s = 0; s < n_steps && rc == 0; s++) {
+        for (c = 0; c < m->n_cells; c++) T0[c] = T[c];
+        for (k = 0; k <= n_corr && rc == 0; k++) {
+            orc_patch_values(m, T, b_value);
+            orc_grad(m, w, T, b_value, grad);
+            orc_lap_correction(m, DT, w, corr, grad, lapSrc);
+            rc = orc_assemble(m, DT, dt, T0, b_value, diag, upper, source, b_int, b_bnd);
+            /* TEqn = ddt - laplacian: source -= lapSrc, before the boundary
+             * source (added in solveSegregated): rebuild in that order */
+            if (rc == 0) {
+                double rDeltaT = 1.0 / dt;
+                int32_t p, i;
+                for (c = 0; c < m->n_cells; c++) source[c] = (rDeltaT * T0[c]) * m->V[c] - lapSrc[c];
+                for (p = 0; p < m->n_patches; p++)
+                    if (m->patch_type[p] == ORC_FIXED_VALUE)
+                        for (i = m->patch_start[p]; i < m->patch_start[p + 1]; i++)
+                            source[m->b_cells[i]] += b_bnd[i];
+                rc = orc_pcg(m, diag, upper, b_bnd, source, T, tol, rel_tol, max_iter, min_iter,
+                             NULL, NULL, NULL, &perf[s * (n_corr + 1) + k]);
+            }
+        }
+        orc_patch_values(m, T, b_value);
+    }
+    free(diag); free(source); free(upper); free(w); free(corr); free(grad); free(lapSrc); free(T0);
+    free(b_int); free(b_bnd);
     return rc;
 }

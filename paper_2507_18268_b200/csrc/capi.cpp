@@ -315,9 +315,16 @@ lf_status laplacian_assemble(lf_mesh *M, const lf_laplacian_params *p, lf_ldu **
     LF_REQUIRE(p->DT > 0.0 && p->dt > 0.0, "DT and dt must be > 0");
     lf_context *ctx = M->ctx;
     cudaStream_t s = ctx->stream;
+    const double *lapSrc = nullptr;
+    if (p->corrected) {
+      require_corrected(M);
+      correction_source(M, p->DT, M->T);
+      lapSrc = M->lapSrc;
+    }
     field_halo(M, M->T);
     ctx->launch(LF_K_ASSEMBLE, [&] {
-      launch_assemble(s, M->Lasm, M->md, M->ld, p->DT, 1.0 / p->dt, M->T, M->ws.recvT, false, M->ws);
+      launch_assemble(s, M->Lasm, M->md, M->ld, p->DT, 1.0 / p->dt, M->T, M->ws.recvT, false, M->ws, nullptr,
+                      lapSrc);
     });
     M->ldu.assembled = true;
     if (sys) *sys = &M->ldu;
@@ -371,6 +378,19 @@ lf_status ldu_amul(const lf_ldu *sys, const double *x, double *y) {
   }, M);
 }
 
+// ------------------------------------------------------------- fvc::grad
+lf_status lf_fvc_grad(lf_mesh *M, const double *x, double *grad, double *bgrad) {
+  return guard([&] {
+    LF_REQUIRE(M && x && grad, "NULL argument");
+    require_corrected(M);
+    lf_context *ctx = M->ctx;
+    cudaStream_t s = ctx->stream;
+    ctx->launch(LF_K_NONORTH, [&] { launch_grad(s, M->Lasm, M->md, M->geo, x, M->gradS, grad); });
+    if (bgrad)
+      ctx->launch(LF_K_NONORTH, [&] { launch_grad_bc(s, M->md, M->geo, M->bCell, x, M->gradS, bgrad); });
+  }, M);
+}
+
 // ------------------------------------------------------------------- PCG
 lf_status pcg_solve(lf_ldu *sys, double *psi, const lf_solver_controls *c, lf_solver_perf *out) {
   lf_mesh *M = sys ? sys->mesh : nullptr;
@@ -388,11 +408,32 @@ lf_status laplacianFoam_step(lf_mesh *M, const lf_laplacian_params *p, const lf_
     LF_REQUIRE(M && p && c, "NULL argument");
     LF_REQUIRE(p->DT > 0.0 && p->dt > 0.0, "DT and dt must be > 0");
     LF_REQUIRE(n_steps >= 0, "n_steps must be >= 0");
+    if (p->corrected) {
+      require_corrected(M);
+      LF_REQUIRE(p->n_non_orth_correctors >= 0, "n_non_orth_correctors must be >= 0");
+    }
     if (n_steps == 0) return;
     upload_controls(M, c, M->T);
+    if (!p->corrected) {
+      for (int32_t st = 0; st < n_steps; ++st) {
+        solve_loop(M, c, M->T, true, p, per_step ? per_step + st : nullptr);
+        M->ldu.assembled = true;
+      }
+      return;
+    }
+    // simple.correctNonOrthogonal() loop: ddt keeps T0 of the step,
+    // each pass re-evaluates the explicit correction from the current T
+    const int32_t passes = 1 + p->n_non_orth_correctors;
+    const bool keepT0 = passes > 1;
     for (int32_t st = 0; st < n_steps; ++st) {
-      solve_loop(M, c, M->T, true, p, per_step ? per_step + st : nullptr);
-      M->ldu.assembled = true;
+      if (keepT0)
+        LF_CUDA(cudaMemcpyAsync(M->T0, M->T, sizeof(double) * M->n, cudaMemcpyDeviceToDevice, M->ctx->stream));
+      for (int32_t k = 0; k < passes; ++k) {
+        correction_source(M, p->DT, M->T);
+        solve_loop(M, c, M->T, true, p, per_step ? per_step + (int64_t)st * passes + k : nullptr,
+                   keepT0 ? M->T0 : nullptr, M->lapSrc);
+        M->ldu.assembled = true;
+      }
     }
   }, M);
 }

@@ -103,13 +103,23 @@ struct lf_mesh {
   size_t p2pBytes = 0, offFlags = 0, offVals = 0, offRecvT = 0, offRecvW = 0;
   std::vector<void *> ipcOpened;  // peer blocks mapped with cudaIpcOpenMemHandle
   bool p2pConnected = false;
+  // non-orthogonal correction path (full geometry given at mesh_create)
+  bool hasGeom = false;
+  lf::GeomDev geo{};
+  double *gradS = nullptr;   // [3][n] fvc::grad(T), SoA
+  double *lapSrc = nullptr;  // [n] explicit laplacian correction source
+  double *T0 = nullptr;      // [n] old-time T of the current step (correctors)
   ~lf_mesh();
 };
 
 namespace lf {
 // solver.cpp
 void solve_loop(lf_mesh *M, const lf_solver_controls *c, double *psi, bool fromAssembly,
-                const lf_laplacian_params *p, lf_solver_perf *out);
+                const lf_laplacian_params *p, lf_solver_perf *out, const double *T0 = nullptr,
+                const double *lapSrc = nullptr);
+// nonorth path (solver.cpp): gradS <- grad(x), lapSrc <- correction of gradS
+void correction_source(lf_mesh *M, double DT, const double *x);
+void require_corrected(const lf_mesh *M);
 void halo_exchange(lf_mesh *M, const double *send, double *recv);
 void field_halo(lf_mesh *M, const double *x);
 // p2p.cpp

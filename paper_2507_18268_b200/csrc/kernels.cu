@@ -392,7 +392,11 @@ void launch_sum(cudaStream_t s, const Launch &L, const MeshDev &m, const double 
 template <bool SETUP>
 __global__ void __launch_bounds__(BS, LF_MINB)
     k_assemble(MeshDev m, LduDev a, double DT, double rDeltaT, const double *__restrict__ T,
-               const double *__restrict__ halo, Workspace ws) {
+               const double *__restrict__ halo, Workspace ws, const double *__restrict__ T0,
+               const double *__restrict__ lapSrc) {
+  // T: psi (current T, initial guess); T0: old-time T for ddt (== T unless
+  // non-orthogonal correctors run); lapSrc: explicit non-orthogonal part of
+  // the corrected laplacian's source (null = orthogonal scheme)
   double psibar = 0.0;
   if (SETUP) psibar = ws.gsum->p1[1] / ws.ctl->nTotal;
   double v[3] = {0.0, 0.0, 0.0};
@@ -421,7 +425,8 @@ __global__ void __launch_bounds__(BS, LF_MINB)
     }
     const double Tc = T[c];
     double d = __dsub_rn(__dmul_rn(rDeltaT, m.V[c]), L);
-    double b = __dmul_rn(__dmul_rn(rDeltaT, Tc), m.V[c]);
+    double b = __dmul_rn(__dmul_rn(rDeltaT, T0[c]), m.V[c]);
+    if (lapSrc) b = __dsub_rn(b, lapSrc[c]);  // TEqn = ddt - laplacian: source -= lap source
     double sP = 0.0, sBc = 0.0;
     const int b0 = m.bcStart[c], b1 = m.bcStart[c + 1];
     for (int k = b0; k < b1; ++k) {
@@ -471,11 +476,12 @@ __global__ void __launch_bounds__(BS, LF_MINB)
 
 void launch_assemble(cudaStream_t s, const Launch &L, const MeshDev &m, const LduDev &a, double DT,
                      double rDeltaT, const double *T, const double *halo, bool setup,
-                     const Workspace &ws) {
+                     const Workspace &ws, const double *T0, const double *lapSrc) {
+  if (!T0) T0 = T;
   if (setup)
-    k_assemble<true><<<L.grid, BS, 0, s>>>(m, a, DT, rDeltaT, T, halo, ws);
+    k_assemble<true><<<L.grid, BS, 0, s>>>(m, a, DT, rDeltaT, T, halo, ws, T0, lapSrc);
   else
-    k_assemble<false><<<L.grid, BS, 0, s>>>(m, a, DT, rDeltaT, T, halo, ws);
+    k_assemble<false><<<L.grid, BS, 0, s>>>(m, a, DT, rDeltaT, T, halo, ws, T0, lapSrc);
 }
 
 // ------------------------------------------------------------- PCG setup

@@ -138,7 +138,29 @@ void launch_sum(cudaStream_t s, const Launch &L, const MeshDev &m, const double 
                 double *out);
 void launch_assemble(cudaStream_t s, const Launch &L, const MeshDev &m, const LduDev &a,
                      double DT, double rDeltaT, const double *T, const double *halo,
-                     bool setup, const Workspace &ws);
+                     bool setup, const Workspace &ws, const double *T0 = nullptr,
+                     const double *lapSrc = nullptr);
+
+// ---------------------------------------- non-orthogonal correction path
+// (nonorth.cu).  Internal face order / numbering, SoA
+// vectors: component k of item i at k*count + i.
+struct GeomDev {
+  int32_t n, F, B;
+  const double *w;        // [F] owner interpolation weights (Listing "weights")
+  const double *corr;     // [3][F] nonOrthCorrectionVectors
+  const double *Sf;       // [3][F] area vectors (owner -> neighbour)
+  const double *bSf;      // [3][B] boundary area vectors (outward), patch order
+  const int32_t *abStart, *abFace;  // per-cell groups of ALL boundary faces
+};
+void launch_weights_corr(cudaStream_t s, int32_t F, const int32_t *owner, const int32_t *nbr,
+                         const double *SfA, const double *CfA, const double *CA, const double *magSf,
+                         const double *delta, double *w, double *corr, double *SfS);
+void launch_grad(cudaStream_t s, const Launch &L, const MeshDev &m, const GeomDev &g, const double *x,
+                 double *gradS, double *gradA);
+void launch_grad_bc(cudaStream_t s, const MeshDev &m, const GeomDev &g, const int32_t *bCell,
+                    const double *x, const double *gradS, double *bgradA);
+void launch_lap_corr(cudaStream_t s, const Launch &L, const MeshDev &m, const GeomDev &g, double DT,
+                     const double *gradS, double *lapSrc);
 void launch_pcg_setup(cudaStream_t s, const Launch &L, const MeshDev &m, const LduDev &a,
                       const double *halo, const Workspace &ws);
 void launch_phase1(cudaStream_t s, const Launch &L, const MeshDev &m, const LduDev &a,

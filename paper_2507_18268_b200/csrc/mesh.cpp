@@ -123,6 +123,16 @@ static void validate(const lf_mesh_desc *d, int rank) {
     if (P.type == LF_PATCH_PROCESSOR && P.neighb_rank == rank) selfOpen ^= 1;
   }
   LF_REQUIRE(selfOpen == 0, "self-coupled processor patches must come in pairs");
+  // full geometry (non-orthogonal path): all or nothing
+  if (d->sf || d->cf || d->c) {
+    LF_REQUIRE(d->c && (d->n_faces == 0 || (d->sf && d->cf)), "sf, cf and c must be given together");
+    for (int32_t p = 0; p < d->n_patches; ++p)
+      LF_REQUIRE(d->patches[p].n_faces == 0 || d->patches[p].sf,
+                 "patch " + std::to_string(p) + ": sf required with full geometry");
+    for (int64_t i = 0; i < 3 * (int64_t)d->n_faces; ++i)
+      LF_REQUIRE(std::isfinite(d->sf[i]) && std::isfinite(d->cf[i]), "sf/cf must be finite");
+    for (int64_t i = 0; i < 3 * (int64_t)n; ++i) LF_REQUIRE(std::isfinite(d->c[i]), "c must be finite");
+  }
 }
 
 }  // namespace lf
@@ -345,6 +355,71 @@ static void build_mesh(lf_context *ctx, const lf_mesh_desc *d, lf_mesh *M) {
   md.pcStart = pcStart;
   md.pcFace = pcFace;
   md.hasProc = nproc > 0;
+
+  // -------------------------- full geometry (non-orthogonal correction path)
+  // Internal face order and orientation: Sf is negated where the relabelled
+  // owner > neighbour (the upper-triangular re-sort swapped the sides).
+  // weights / nonOrthCorrectionVectors are then computed on the device from
+  // the internal geometry (k_weights_corr).
+  if (d->c) {
+    M->hasGeom = true;
+    std::vector<int32_t> fp(F);
+    LF_CUDA(cudaMemcpyAsync(fp.data(), M->facePerm, sizeof(int32_t) * F, cudaMemcpyDeviceToHost, s));
+    LF_CUDA(cudaStreamSynchronize(s));
+    std::vector<double> sfA(3 * (size_t)F), cfA(3 * (size_t)F), cA(3 * (size_t)n), bsf(3 * (size_t)B);
+    for (int32_t f = 0; f < F; ++f) {
+      const int32_t src = fp[f];
+      int32_t o = d->owner[src], nb = d->neighbour[src];
+      if (!iperm.empty()) {
+        o = iperm[o];
+        nb = iperm[nb];
+      }
+      const double sg = o > nb ? -1.0 : 1.0;
+      for (int k = 0; k < 3; ++k) {
+        sfA[3 * (size_t)f + k] = sg * d->sf[3 * (size_t)src + k];
+        cfA[3 * (size_t)f + k] = d->cf[3 * (size_t)src + k];
+      }
+    }
+    for (int32_t c = 0; c < n; ++c) {
+      const int32_t ci = iperm.empty() ? c : iperm[c];
+      for (int k = 0; k < 3; ++k) cA[3 * (size_t)ci + k] = d->c[3 * (size_t)c + k];
+    }
+    for (int32_t p = 0, off = 0; p < d->n_patches; ++p) {
+      const lf_patch_desc &P = d->patches[p];
+      for (int32_t i = 0; i < P.n_faces; ++i)
+        for (int k = 0; k < 3; ++k) bsf[(size_t)k * B + off + i] = P.sf[3 * (size_t)i + k];
+      off += P.n_faces;
+    }
+    double *tmp = nullptr;
+    const size_t tF = 3 * (size_t)std::max(F, 1), tN = 3 * (size_t)n;
+    LF_CUDA(cudaMallocAsync(&tmp, sizeof(double) * (2 * tF + tN), s));
+    LF_CUDA(cudaMemcpyAsync(tmp, sfA.data(), sizeof(double) * 3 * F, cudaMemcpyHostToDevice, s));
+    LF_CUDA(cudaMemcpyAsync(tmp + tF, cfA.data(), sizeof(double) * 3 * F, cudaMemcpyHostToDevice, s));
+    LF_CUDA(cudaMemcpyAsync(tmp + 2 * tF, cA.data(), sizeof(double) * tN, cudaMemcpyHostToDevice, s));
+    GeomDev &g = M->geo;
+    g.n = n;
+    g.F = F;
+    g.B = B;
+    double *w = A.alloc<double>(F), *corr = A.alloc<double>(3 * (size_t)F), *SfS = A.alloc<double>(3 * (size_t)F);
+    launch_weights_corr(s, F, owner, nbr, tmp, tmp + tF, tmp + 2 * tF, magSf, delta, w, corr, SfS);
+    LF_CUDA(cudaFreeAsync(tmp, s));
+    double *bSf = A.alloc<double>(3 * (size_t)B);
+    LF_CUDA(cudaMemcpyAsync(bSf, bsf.data(), sizeof(double) * 3 * B, cudaMemcpyHostToDevice, s));
+    std::vector<int32_t> selAll(B);
+    for (int32_t i = 0; i < B; ++i) selAll[i] = i;
+    int32_t *abStart, *abFace;
+    group_cells(selAll, abStart, abFace);
+    g.w = w;
+    g.corr = corr;
+    g.Sf = SfS;
+    g.bSf = bSf;
+    g.abStart = abStart;
+    g.abFace = abFace;
+    M->gradS = A.alloc<double>(3 * (size_t)n);
+    M->lapSrc = A.alloc<double>(n);
+    M->T0 = A.alloc<double>(n);
+    LF_CUDA(cudaStreamSynchronize(s));
+  }
 
   // ------------------------------------------ ELL slices for the solve
   // K = max faces per side (3 on hex meshes); built when 1 <= K <= 4 and the

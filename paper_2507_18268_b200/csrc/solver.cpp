@@ -191,8 +191,22 @@ static void sum_psi(lf_mesh *M, const double *psi) {
   allreduce(M, M->ws.lsum->p1, M->ws.gsum->p1, 2);
 }
 
+void require_corrected(const lf_mesh *M) {
+  LF_REQUIRE(M->hasGeom, "the non-orthogonal path needs the full geometry (lf_mesh_desc.sf/cf/c)");
+  LF_REQUIRE(M->nproc == 0, "the non-orthogonal path does not support processor patches");
+}
+
+// gradS <- fvc::grad(x); lapSrc <- explicit non-orthogonal laplacian source
+// of that gradient (two gathers, stream-ordered).
+void correction_source(lf_mesh *M, double DT, const double *x) {
+  lf_context *ctx = M->ctx;
+  ctx->launch(LF_K_NONORTH, [&] { launch_grad(ctx->stream, M->Lasm, M->md, M->geo, x, M->gradS, nullptr); });
+  ctx->launch(LF_K_NONORTH,
+              [&] { launch_lap_corr(ctx->stream, M->Lasm, M->md, M->geo, DT, M->gradS, M->lapSrc); });
+}
+
 void solve_loop(lf_mesh *M, const lf_solver_controls *c, double *psi, bool fromAssembly,
-                const lf_laplacian_params *p, lf_solver_perf *out) {
+                const lf_laplacian_params *p, lf_solver_perf *out, const double *T0, const double *lapSrc) {
   lf_context *ctx = M->ctx;
   cudaStream_t s = ctx->stream;
   const Workspace &ws = M->ws;
@@ -203,7 +217,7 @@ void solve_loop(lf_mesh *M, const lf_solver_controls *c, double *psi, bool fromA
   if (host_halo(M)) exchange_field(M, psi, ws.recvT);
   if (fromAssembly) {
     ctx->launch(LF_K_ASSEMBLE, [&] {
-      launch_assemble(s, M->Lasm, M->md, M->ld, p->DT, 1.0 / p->dt, psi, ws.recvT, true, ws);
+      launch_assemble(s, M->Lasm, M->md, M->ld, p->DT, 1.0 / p->dt, psi, ws.recvT, true, ws, T0, lapSrc);
     });
   } else {
     ctx->launch(LF_K_SETUP, [&] { launch_pcg_setup(s, M->Lsetup, M->md, M->ld, ws.recvT, ws); });

@@ -23,7 +23,8 @@ STATUS = {0: "LF_OK", 1: "LF_ERR_INVALID_ARG", 2: "LF_ERR_STATE", 3: "LF_ERR_OOM
           4: "LF_ERR_CUDA", 5: "LF_ERR_NCCL", 6: "LF_ERR_INTERNAL"}
 PATCH_TYPES = {"fixedValue": 0, "zeroGradient": 1, "processor": 2}
 FIELD_T, FIELD_PATCH_VALUE = 0, 1
-KERNELS = {"assemble": 0, "setup": 1, "phase1": 2, "phase2": 3, "amul": 4, "sumpsi": 5, "pack": 6, "pcg": 7}
+KERNELS = {"assemble": 0, "setup": 1, "phase1": 2, "phase2": 3, "amul": 4, "sumpsi": 5, "pack": 6, "pcg": 7,
+           "nonorth": 8}
 OPTIONS = {"persistent": 0, "graphs": 1}
 
 
@@ -36,18 +37,19 @@ class LfoamError(RuntimeError):
 class PatchDesc(C.Structure):
     _fields_ = [("type", C.c_int), ("n_faces", C.c_int32), ("face_cells", C.c_void_p),
                 ("mag_sf", C.c_void_p), ("delta_coeffs", C.c_void_p), ("value", C.c_void_p),
-                ("neighb_rank", C.c_int32)]
+                ("neighb_rank", C.c_int32), ("sf", C.c_void_p)]
 
 
 class MeshDesc(C.Structure):
     _fields_ = [("n_cells", C.c_int32), ("n_faces", C.c_int32), ("n_patches", C.c_int32),
                 ("owner", C.c_void_p), ("neighbour", C.c_void_p), ("mag_sf", C.c_void_p),
                 ("delta_coeffs", C.c_void_p), ("V", C.c_void_p), ("patches", C.POINTER(PatchDesc)),
-                ("renumber", C.c_int32)]
+                ("renumber", C.c_int32), ("sf", C.c_void_p), ("cf", C.c_void_p), ("c", C.c_void_p)]
 
 
 class Params(C.Structure):
-    _fields_ = [("DT", C.c_double), ("dt", C.c_double)]
+    _fields_ = [("DT", C.c_double), ("dt", C.c_double), ("corrected", C.c_int32),
+                ("n_non_orth_correctors", C.c_int32)]
 
 
 class Controls(C.Structure):
@@ -85,6 +87,7 @@ SIGNATURES = {
     "field_get": (C.c_int, [_vp, C.c_int, _i32, _vp, _i64, C.c_int]),
     "laplacian_assemble": (C.c_int, [_vp, C.POINTER(Params), C.POINTER(_vp)]),
     "lf_ldu_export": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
+    "lf_fvc_grad": (C.c_int, [_vp, _vp, _vp, _vp]),
     "ldu_amul": (C.c_int, [_vp, _vp, _vp]),
     "pcg_solve": (C.c_int, [_vp, _vp, C.POINTER(Controls), C.POINTER(Perf)]),
     "laplacianFoam_step": (C.c_int, [_vp, C.POINTER(Params), C.POINTER(Controls), _i32, C.POINTER(Perf)]),
@@ -125,6 +128,10 @@ def _check(st: int):
 
 def _host(a, dtype):
     return np.ascontiguousarray(a, dtype=dtype)
+
+
+def _vec3(a):
+    return None if a is None else np.ascontiguousarray(a, dtype=np.float64).reshape(-1, 3)
 
 
 def _ptr(a):
@@ -215,8 +222,12 @@ class Mesh:
     n_cells, owner, neighbour, mag_sf, delta, V, patches[type, face_cells,
     mag_sf, delta, value, neighb_rank])."""
 
-    def __init__(self, ctx: Context, m, renumber: bool = False):
+    def __init__(self, ctx: Context, m, renumber: bool = False, geometry: Optional[bool] = None):
+        """geometry: pass the full geometry (Sf, Cf, C, patch Sf) for the
+        non-orthogonal correction path; default: when the description has it."""
         self.ctx = ctx
+        if geometry is None:
+            geometry = getattr(m, "Sf", None) is not None
         keep = []
         own = _host(m.owner, np.int32); nb = _host(m.neighbour, np.int32)
         ms = _host(m.mag_sf, np.float64); de = _host(m.delta, np.float64); V = _host(m.V, np.float64)
@@ -227,13 +238,18 @@ class Mesh:
         for i, p in enumerate(m.patches):
             fc = _host(p.face_cells, np.int32); pm = _host(p.mag_sf, np.float64)
             pd = _host(p.delta, np.float64); pv = _host(p.value, np.float64)
-            keep += [fc, pm, pd, pv]
+            psf = _vec3(getattr(p, "Sf", None)) if geometry else None
+            keep += [fc, pm, pd, pv, psf]
             pds[i] = PatchDesc(PATCH_TYPES[p.type], fc.shape[0], _ptr(fc), _ptr(pm), _ptr(pd), _ptr(pv),
-                               int(getattr(p, "neighb_rank", -1)))
+                               int(getattr(p, "neighb_rank", -1)), _ptr(psf))
             self.patch_sizes.append(int(fc.shape[0]))
             self.patch_types.append(p.type)
+        g = [None, None, None]
+        if geometry:
+            g = [_vec3(m.Sf), _vec3(m.Cf), _vec3(m.C)]  # a missing one -> NULL -> INVALID_ARG
+            keep += g
         desc = MeshDesc(int(m.n_cells), int(own.shape[0]), len(m.patches), _ptr(own), _ptr(nb), _ptr(ms),
-                        _ptr(de), _ptr(V), pds, 1 if renumber else 0)
+                        _ptr(de), _ptr(V), pds, 1 if renumber else 0, _ptr(g[0]), _ptr(g[1]), _ptr(g[2]))
         h = C.c_void_p()
         _check(lib().mesh_create(ctx.h, C.byref(desc), C.byref(h)))
         self.h = h
@@ -297,16 +313,34 @@ class Mesh:
         _check(lib().lf_permute(self.h, 1 if to_internal else 0, _ptr(x), _ptr(y)))
 
     # ------------------------------------------------------------ ops
-    def assemble(self, DT: float = 1.0, dt: float = 0.2) -> "Ldu":
+    def assemble(self, DT: float = 1.0, dt: float = 0.2, corrected: bool = False) -> "Ldu":
         h = C.c_void_p()
-        _check(lib().laplacian_assemble(self.h, C.byref(Params(DT, dt)), C.byref(h)))
+        _check(lib().laplacian_assemble(self.h, C.byref(Params(DT, dt, int(corrected), 0)), C.byref(h)))
         return Ldu(self, h)
 
-    def step(self, n_steps: int, DT: float = 1.0, dt: float = 0.2, **ctl) -> List[Dict]:
-        perfs = (Perf * max(n_steps, 1))()
-        _check(lib().laplacianFoam_step(self.h, C.byref(Params(DT, dt)), C.byref(controls(**ctl)),
-                                        n_steps, perfs))
-        return [perfs[i].as_dict() for i in range(n_steps)]
+    def step(self, n_steps: int, DT: float = 1.0, dt: float = 0.2, corrected: bool = False,
+             n_non_orth_correctors: int = 0, **ctl) -> List[Dict]:
+        """n_steps time steps; one perf dict per solve (n_steps * (1 +
+        n_non_orth_correctors) when corrected)."""
+        nsol = n_steps * (1 + (n_non_orth_correctors if corrected else 0))
+        perfs = (Perf * max(nsol, 1))()
+        prm = Params(DT, dt, int(corrected), int(n_non_orth_correctors))
+        _check(lib().laplacianFoam_step(self.h, C.byref(prm), C.byref(controls(**ctl)), n_steps, perfs))
+        return [perfs[i].as_dict() for i in range(nsol)]
+
+    def fvc_grad(self, x, grad=None, bgrad=None):
+        """grad(x) (gaussGrad, linear) into device grad[n_cells, 3] and, if
+        given, the corrected boundary gradient bgrad[n_boundary_faces, 3];
+        internal numbering.  Returns grad."""
+        import torch
+        _check_dev(x, self.n_cells)
+        if grad is None:
+            grad = torch.empty((self.n_cells, 3), dtype=torch.float64, device=x.device)
+        _check_dev(grad, 3 * self.n_cells)
+        if bgrad is not None:
+            _check_dev(bgrad, 3 * self.n_bfaces)
+        _check(lib().lf_fvc_grad(self.h, _ptr(x), _ptr(grad), _ptr(bgrad)))
+        return grad
 
     def close(self):
         if getattr(self, "h", None):
