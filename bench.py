@@ -49,6 +49,10 @@ def parse():
     ap.add_argument("--mode", default="persistent", choices=["persistent", "graphs", "direct"],
                     help="PCG loop execution (single rank): one cooperative launch per solve, "
                          "CUDA-graph replays of per-phase launches, or direct launches")
+    ap.add_argument("--corrected", type=int, default=-1,
+                    help=">= 0: SURVEY §8(f) row 1 workload — the config's cells sheared and graded "
+                         "(meshgen.skewed_config_mesh), Gauss linear corrected laplacian with this many "
+                         "extra non-orthogonal correctors per step")
     return ap.parse_args()
 
 
@@ -59,9 +63,18 @@ def dist_env():
     return ws, rank, local
 
 
-def workload_name(cfg):
+def workload_name(cfg, corrected=-1):
     c = meshgen.CONFIGS[cfg]
-    return f"cube{c['N']}^3{'-permuted' if c['permuted'] else ''}"
+    base = f"cube{c['N']}^3{'-permuted' if c['permuted'] else ''}"
+    return base if corrected < 0 else f"skewed-{base}-corrected-{corrected}corr"
+
+
+def workload_mesh(cfg, corrected=-1):
+    return meshgen.config_mesh(cfg) if corrected < 0 else meshgen.skewed_config_mesh(cfg)
+
+
+def step_kw(corrected):
+    return {} if corrected < 0 else {"corrected": True, "n_non_orth_correctors": corrected}
 
 
 # ------------------------------------------------------------------ clocks
@@ -129,20 +142,27 @@ def ncu_traffic(cfg, kernel):
 
 
 # --------------------------------------------------------------- oracle arm
-def oracle_rate(mesh, T0, steps):
+def _oracle_steps(om, T0, steps, corrected, **kw):
+    import oracle
+    if corrected < 0:
+        return oracle.laplacian_foam(om, T0, steps, DT=DT, dt=DELTA_T, tol=TOL, **kw)
+    return oracle.laplacian_foam_corrected(om, T0, steps, n_corr=corrected, DT=DT, dt=DELTA_T, tol=TOL, **kw)
+
+
+def oracle_rate(mesh, T0, steps, corrected=-1):
     import oracle
     om = oracle.OMesh(mesh)
     t0 = time.perf_counter()
-    _, _, perfs = oracle.laplacian_foam(om, T0, steps, DT=DT, dt=DELTA_T, tol=TOL)
+    _, _, perfs = _oracle_steps(om, T0, steps, corrected)
     dt = time.perf_counter() - t0
     return mesh.n_cells * steps / dt, dt, perfs
 
 
-def oracle_rate_capped(mesh, T0, max_iter):
+def oracle_rate_capped(mesh, T0, max_iter, corrected=-1):
     import oracle
     om = oracle.OMesh(mesh)
     t0 = time.perf_counter()
-    _, _, perfs = oracle.laplacian_foam(om, T0, 1, DT=DT, dt=DELTA_T, tol=TOL, max_iter=max_iter)
+    _, _, perfs = _oracle_steps(om, T0, 1, corrected, max_iter=max_iter)
     dt = time.perf_counter() - t0
     return mesh.n_cells / dt, dt, perfs
 
@@ -152,20 +172,20 @@ def run_reference(args):
     if rank != 0:
         return
     cfg = args.config
-    mesh = meshgen.config_mesh(cfg)
+    mesh = workload_mesh(cfg, args.corrected)
     T0 = meshgen.canonical_field(mesh)
     K = min(args.steps, 20)
     W = min(args.warmup, 1)
     if W:
-        oracle_rate(mesh, T0, W)
-    rate, secs, perfs = oracle_rate(mesh, T0, K)
+        oracle_rate(mesh, T0, W, args.corrected)
+    rate, secs, perfs = oracle_rate(mesh, T0, K, args.corrected)
     its = [p["n_iterations"] for p in perfs]
-    sample = (f"first {K} laplacianFoam steps of {workload_name(cfg)} (of --steps {args.steps}); "
+    sample = (f"first {K} laplacianFoam steps of {workload_name(cfg, args.corrected)} (of --steps {args.steps}); "
               f"single-threaded C oracle, PCG iterations/step {min(its)}-{max(its)}")
     line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus,
             "steps": K, "warmup": W, "ms_per_step": secs / K * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_name(cfg), "n_cells": mesh.n_cells, "global_batch": 1,
+            "config": {"workload": workload_name(cfg, args.corrected), "n_cells": mesh.n_cells, "global_batch": 1,
                        "seq_len": 0, "parallelism": "cpu-1core"},
             "cpu_baseline": {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
             "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -195,7 +215,10 @@ def run_ours(args):
     ctx.set_option("graphs", args.mode != "direct")
 
     cfg = args.config
-    gmesh = meshgen.config_mesh(cfg)
+    if args.corrected >= 0 and ws > 1:
+        raise SystemExit("--corrected: single rank only (the corrected path has no processor patches)")
+    gmesh = workload_mesh(cfg, args.corrected)
+    kw = step_kw(args.corrected)
     n_global = gmesh.n_cells
     T0g = meshgen.canonical_field(gmesh)
     if ws > 1:
@@ -229,7 +252,7 @@ def run_ours(args):
 
     # warm-up (W >= 3 steps), then reset to step 0 of the case
     mesh.set_T(T0)
-    mesh.step(max(args.warmup, 3), DT, DELTA_T, tol=TOL)
+    mesh.step(max(args.warmup, 3), DT, DELTA_T, tol=TOL, **kw)
 
     def timed_pass(instrument=False):
         mesh.set_T(T0)
@@ -241,7 +264,7 @@ def run_ours(args):
             flush.fill_(float(k))          # L2 flush, outside the events
             a, b = ev[k]
             a.record(stream)
-            perfs += mesh.step(1, DT, DELTA_T, tol=TOL)
+            perfs += mesh.step(1, DT, DELTA_T, tol=TOL, **kw)
             b.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -263,6 +286,10 @@ def run_ours(args):
     n_p2, ms_p2 = ctx.kernel_stats("phase2")
     n_as, ms_as = ctx.kernel_stats("assemble")
     n_pcg, ms_pcg = ctx.kernel_stats("pcg")
+    n_no, ms_no = ctx.kernel_stats("nonorth")
+    B_local = sum(p.n_faces for p in m.patches)
+    # grad gather (40n + 40F + 37B) + correction gather (40n + 48F), per pass
+    bytes_no_pass = 80 * n_local + 88 * F_local + 37 * B_local
     iters = sum(p["n_iterations"] for p in perfs_i)
     bytes_p1 = 56 * n_local + 16 * F_local          # per full phase-1 launch
     bytes_p2 = 40 * n_local
@@ -278,7 +305,7 @@ def run_ours(args):
         total_bytes = bytes_p1 * iters
         k_launches, k_ms = n_p1, ms_p1
     achieved = total_bytes / (k_ms / 1e3) / 1e9 if k_ms > 0 else None
-    traffic = ncu_traffic(cfg, kernel) if ws == 1 else None
+    traffic = ncu_traffic(cfg if args.corrected < 0 else f"{cfg}-corr{args.corrected}", kernel) if ws == 1 else None
 
     # e2e through the public API with host buffers (pinned), copies inside the region
     T0h = torch.from_numpy(np.ascontiguousarray(T0)).pin_memory()
@@ -292,7 +319,7 @@ def run_ours(args):
         a, b = ev[k]
         a.record(stream)
         mesh.set_T(T0h.numpy() if k == 0 else Th.numpy())   # H2D of this step's input state
-        mesh.step(1, DT, DELTA_T, tol=TOL)
+        mesh.step(1, DT, DELTA_T, tol=TOL, **kw)
         mesh.get_T(Th.numpy())                              # D2H of this step's result
         b.record(stream)
     torch.cuda.synchronize()
@@ -306,21 +333,22 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        full = meshgen.config_mesh(cfg)
+        full = workload_mesh(cfg, args.corrected)
         its_gpu = sum(p["n_iterations"] for p in perfs) / len(perfs)
         if n_global <= 2_000_000:
             steps = args.cpu_steps or 2
-            rate, secs, po = oracle_rate(full, meshgen.canonical_field(full), steps)
-            sample = (f"first {steps} laplacianFoam steps of {workload_name(cfg)} "
+            rate, secs, po = oracle_rate(full, meshgen.canonical_field(full), steps, args.corrected)
+            sample = (f"first {steps} laplacianFoam steps of {workload_name(cfg, args.corrected)} "
                       f"({secs:.1f} s, PCG iterations {[p['n_iterations'] for p in po]})")
         else:
             # bounded sample: step 0 truncated to `cap` PCG iterations, scaled to
             # the GPU run's mean iterations per step (the oracle does the same
             # work per iteration; assembly is counted once)
             cap = max(2, int(20 * 8e6 / n_global))
-            _, secs, po = oracle_rate_capped(full, meshgen.canonical_field(full), cap)
-            rate = n_global / (secs * its_gpu / po[0]["n_iterations"])
-            sample = (f"step 0 of {workload_name(cfg)} capped at {po[0]['n_iterations']} PCG iterations "
+            _, secs, po = oracle_rate_capped(full, meshgen.canonical_field(full), cap, args.corrected)
+            its_cpu = sum(p["n_iterations"] for p in po) / len(po)
+            rate = n_global / (secs * its_gpu / its_cpu)
+            sample = (f"step 0 of {workload_name(cfg, args.corrected)} capped at {po[0]['n_iterations']} PCG iterations "
                       f"({secs:.1f} s), scaled to {its_gpu:.1f} iterations/step (projected)")
         cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample}
 
@@ -330,7 +358,7 @@ def run_ours(args):
         "warmup": max(args.warmup, 3), "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "weak" if ws == 1 else "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": workload_name(cfg), "n_cells": n_global, "steps_per_run": args.steps,
+        "config": {"workload": workload_name(cfg, args.corrected), "n_cells": n_global, "steps_per_run": args.steps,
                    "global_batch": 1, "seq_len": 0, "parallelism": "1gpu" if ws == 1 else f"domain{ws}-{args.transport}",
                    "renumber": args.renumber, "mode": args.mode,
                    "l2": "flushed between timed steps (256 MiB write)", "tol": TOL,
@@ -348,6 +376,10 @@ def run_ours(args):
                      "phase2": {"achieved": bytes_p2 * iters / (ms_p2 / 1e3) / 1e9 if ms_p2 > 0 else None,
                                 "avg_launch_ms": ms_p2 / max(n_p2, 1), "share_of_step": ms_p2 / inst_ms},
                      "assemble": {"avg_launch_ms": ms_as / max(n_as, 1), "share_of_step": ms_as / inst_ms},
+                     "nonorth": ({"achieved": bytes_no_pass * (n_no // 2) / (ms_no / 1e3) / 1e9,
+                                  "bytes_per_pass": bytes_no_pass, "launches": n_no,
+                                  "avg_launch_ms": ms_no / n_no, "share_of_step": ms_no / inst_ms}
+                                 if n_no > 0 and ms_no > 0 else None),
                      "instrumented_ms_per_step": inst_ms / args.steps},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * n_local,

@@ -396,3 +396,17 @@ def config_mesh(cfg: int) -> Mesh:
     c = CONFIGS[cfg]
     m = block_mesh(c["N"])
     return permute_mesh(m) if c["permuted"] else m
+
+
+# Skewed variant of a config (SURVEY §8(f) row 1 workload): the same N^3
+# cells sheared by A = [[1, .3, .2], [0, 1, .1], [0, 0, 1]] and graded so the
+# largest/smallest cell width ratio is 2 along x and y (weights != 1/2).
+SKEW_SHEAR = (0.3, 0.2, 0.1)
+
+
+def skewed_config_mesh(cfg: int) -> Mesh:
+    c = CONFIGS[cfg]
+    N = c["N"]
+    r = 2.0 ** (1.0 / max(N - 1, 1))
+    m = skewed_block_mesh(N, N, N, shear=SKEW_SHEAR, grading=(r, 1.0 / r, 1.0))
+    return permute_mesh(m) if c["permuted"] else m
