@@ -53,6 +53,9 @@ def parse():
                     help=">= 0: SURVEY §8(f) row 1 workload — the config's cells sheared and graded "
                          "(meshgen.skewed_config_mesh), Gauss linear corrected laplacian with this many "
                          "extra non-orthogonal correctors per step")
+    ap.add_argument("--dt-field", action="store_true",
+                    help="SURVEY §8(f) row 2 workload: two-material DT field (meshgen.layered_dt_field, "
+                         "ratio 10) on the config mesh with full geometry (skewed with --corrected)")
     return ap.parse_args()
 
 
@@ -63,14 +66,26 @@ def dist_env():
     return ws, rank, local
 
 
-def workload_name(cfg, corrected=-1):
+def workload_name(cfg, corrected=-1, dt_field=False):
     c = meshgen.CONFIGS[cfg]
     base = f"cube{c['N']}^3{'-permuted' if c['permuted'] else ''}"
-    return base if corrected < 0 else f"skewed-{base}-corrected-{corrected}corr"
+    name = base if corrected < 0 else f"skewed-{base}-corrected-{corrected}corr"
+    return name + ("-layeredDT" if dt_field else "")
 
 
-def workload_mesh(cfg, corrected=-1):
-    return meshgen.config_mesh(cfg) if corrected < 0 else meshgen.skewed_config_mesh(cfg)
+def workload_mesh(cfg, corrected=-1, dt_field=False):
+    import dataclasses
+    if corrected >= 0:
+        m = meshgen.skewed_config_mesh(cfg)
+    elif dt_field:
+        m = meshgen.with_geometry(meshgen.block_mesh(meshgen.CONFIGS[cfg]["N"]))
+        if meshgen.CONFIGS[cfg]["permuted"]:
+            m = meshgen.permute_mesh(m)
+    else:
+        return meshgen.config_mesh(cfg)
+    if dt_field:
+        m = dataclasses.replace(m, DT_field=meshgen.layered_dt_field(m))
+    return m
 
 
 def step_kw(corrected):
@@ -172,7 +187,7 @@ def run_reference(args):
     if rank != 0:
         return
     cfg = args.config
-    mesh = workload_mesh(cfg, args.corrected)
+    mesh = workload_mesh(cfg, args.corrected, args.dt_field)
     T0 = meshgen.canonical_field(mesh)
     K = min(args.steps, 20)
     W = min(args.warmup, 1)
@@ -180,12 +195,12 @@ def run_reference(args):
         oracle_rate(mesh, T0, W, args.corrected)
     rate, secs, perfs = oracle_rate(mesh, T0, K, args.corrected)
     its = [p["n_iterations"] for p in perfs]
-    sample = (f"first {K} laplacianFoam steps of {workload_name(cfg, args.corrected)} (of --steps {args.steps}); "
+    sample = (f"first {K} laplacianFoam steps of {workload_name(cfg, args.corrected, args.dt_field)} (of --steps {args.steps}); "
               f"single-threaded C oracle, PCG iterations/step {min(its)}-{max(its)}")
     line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus,
             "steps": K, "warmup": W, "ms_per_step": secs / K * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_name(cfg, args.corrected), "n_cells": mesh.n_cells, "global_batch": 1,
+            "config": {"workload": workload_name(cfg, args.corrected, args.dt_field), "n_cells": mesh.n_cells, "global_batch": 1,
                        "seq_len": 0, "parallelism": "cpu-1core"},
             "cpu_baseline": {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
             "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -217,7 +232,7 @@ def run_ours(args):
     cfg = args.config
     if args.corrected >= 0 and ws > 1:
         raise SystemExit("--corrected: single rank only (the corrected path has no processor patches)")
-    gmesh = workload_mesh(cfg, args.corrected)
+    gmesh = workload_mesh(cfg, args.corrected, args.dt_field)
     kw = step_kw(args.corrected)
     n_global = gmesh.n_cells
     T0g = meshgen.canonical_field(gmesh)
@@ -305,7 +320,8 @@ def run_ours(args):
         total_bytes = bytes_p1 * iters
         k_launches, k_ms = n_p1, ms_p1
     achieved = total_bytes / (k_ms / 1e3) / 1e9 if k_ms > 0 else None
-    traffic = ncu_traffic(cfg if args.corrected < 0 else f"{cfg}-corr{args.corrected}", kernel) if ws == 1 else None
+    tkey = f"{cfg}{'' if args.corrected < 0 else f'-corr{args.corrected}'}{'-dt' if args.dt_field else ''}"
+    traffic = ncu_traffic(tkey, kernel) if ws == 1 else None
 
     # e2e through the public API with host buffers (pinned), copies inside the region
     T0h = torch.from_numpy(np.ascontiguousarray(T0)).pin_memory()
@@ -333,12 +349,12 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        full = workload_mesh(cfg, args.corrected)
+        full = workload_mesh(cfg, args.corrected, args.dt_field)
         its_gpu = sum(p["n_iterations"] for p in perfs) / len(perfs)
         if n_global <= 2_000_000:
             steps = args.cpu_steps or 2
             rate, secs, po = oracle_rate(full, meshgen.canonical_field(full), steps, args.corrected)
-            sample = (f"first {steps} laplacianFoam steps of {workload_name(cfg, args.corrected)} "
+            sample = (f"first {steps} laplacianFoam steps of {workload_name(cfg, args.corrected, args.dt_field)} "
                       f"({secs:.1f} s, PCG iterations {[p['n_iterations'] for p in po]})")
         else:
             # bounded sample: step 0 truncated to `cap` PCG iterations, scaled to
@@ -348,7 +364,7 @@ def run_ours(args):
             _, secs, po = oracle_rate_capped(full, meshgen.canonical_field(full), cap, args.corrected)
             its_cpu = sum(p["n_iterations"] for p in po) / len(po)
             rate = n_global / (secs * its_gpu / its_cpu)
-            sample = (f"step 0 of {workload_name(cfg, args.corrected)} capped at {po[0]['n_iterations']} PCG iterations "
+            sample = (f"step 0 of {workload_name(cfg, args.corrected, args.dt_field)} capped at {po[0]['n_iterations']} PCG iterations "
                       f"({secs:.1f} s), scaled to {its_gpu:.1f} iterations/step (projected)")
         cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample}
 
@@ -358,7 +374,7 @@ def run_ours(args):
         "warmup": max(args.warmup, 3), "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "weak" if ws == 1 else "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": workload_name(cfg, args.corrected), "n_cells": n_global, "steps_per_run": args.steps,
+        "config": {"workload": workload_name(cfg, args.corrected, args.dt_field), "n_cells": n_global, "steps_per_run": args.steps,
                    "global_batch": 1, "seq_len": 0, "parallelism": "1gpu" if ws == 1 else f"domain{ws}-{args.transport}",
                    "renumber": args.renumber, "mode": args.mode,
                    "l2": "flushed between timed steps (256 MiB write)", "tol": TOL,

@@ -167,6 +167,13 @@ LF_API lf_status lf_permute(const lf_mesh *mesh, int to_internal, const double *
 /* --------------------------------------------------------------- fields */
 typedef enum {
   LF_FIELD_T = 0,            /* cell values, n = n_cells, patch = -1            */
+  LF_FIELD_DT = 2,           /* spatially varying diffusivity DT (cell values > 0, n =
+                                n_cells, patch = -1).  Setting it
+                                computes the face diffusivities once, on the device:
+                                gamma_f = w (DT_P - DT_N) + DT_N with the geometric
+                                weights, boundary DT[faceCell] (reading A38).
+                                Needs the full geometry and no processor patches;
+                                used by solves with lf_laplacian_params.variable_DT. */
   LF_FIELD_PATCH_VALUE = 1   /* boundary values of patch `patch`, n = n_faces.
                                 fixedValue: T_b (set/get).  zeroGradient: get
                                 returns T[faceCells] (correctBoundaryConditions);
@@ -190,6 +197,9 @@ typedef struct {
                           step (simple.correctNonOrthogonal()); each pass
                           re-evaluates the correction from the current T and solves
                           again from it, ddt keeping T0 of the step (0 = one pass) */
+  int32_t variable_DT; /* 1: the laplacian's diffusivity is the LF_FIELD_DT cell field
+                          (gammaMagSf = gamma_f |Sf| in place of DT |Sf|; DT ignored);
+                          LF_ERR_STATE if that field was never set */
 } lf_laplacian_params;
 
 typedef struct lf_ldu lf_ldu;   /* owned by its mesh, reused every step */

@@ -64,6 +64,8 @@ class Mesh:
     C: Optional[np.ndarray] = None
     affine: Optional[np.ndarray] = None       # 3x3 map applied to the unit block (skewed meshes)
     grid_lines: Optional[tuple] = None        # graded blocks: grid-line coordinates per axis
+    # spatially varying diffusivity: DT per cell, or None (uniform DT)
+    DT_field: Optional[np.ndarray] = None
 
     @property
     def n_faces(self) -> int:
@@ -270,6 +272,10 @@ def permute_mesh(mesh: Mesh, cell_seed: int = 1, face_seed: int = 2) -> Mesh:
         C[new_of_old] = mesh.C
         geo = dict(Sf=mesh.Sf[fperm] * sgn, Cf=mesh.Cf[fperm].copy(), C=C, affine=mesh.affine,
                    grid_lines=mesh.grid_lines)
+    if mesh.DT_field is not None:
+        DTf = np.empty_like(mesh.DT_field)
+        DTf[new_of_old] = mesh.DT_field
+        geo["DT_field"] = DTf
     return Mesh(n, owner, neighbour, mesh.mag_sf[fperm], mesh.delta[fperm], V, patches,
                 dims=mesh.dims, extent=mesh.extent,
                 old_of_new=base[old_of_new].astype(np.int32), face_old_of_new=fperm, **geo)
@@ -410,3 +416,11 @@ def skewed_config_mesh(cfg: int) -> Mesh:
     r = 2.0 ** (1.0 / max(N - 1, 1))
     m = skewed_block_mesh(N, N, N, shear=SKEW_SHEAR, grading=(r, 1.0 / r, 1.0))
     return permute_mesh(m) if c["permuted"] else m
+
+
+def layered_dt_field(mesh: Mesh, ratio: float = 10.0) -> np.ndarray:
+    """Two-material diffusivity (SURVEY §8(f) row 2 workload): DT = 1 below
+    the mid-plane z = 1/2 of the generating block, 1/ratio above."""
+    nx, ny, nz = mesh.dims
+    k = mesh.block_labels() // (nx * ny)
+    return np.where(k < nz // 2, 1.0, 1.0 / ratio)

@@ -43,7 +43,8 @@ class _Mesh(C.Structure):
                 ("mag_sf", C.c_void_p), ("delta", C.c_void_p), ("V", C.c_void_p),
                 ("patch_type", C.c_void_p), ("patch_start", C.c_void_p), ("b_cells", C.c_void_p),
                 ("b_mag_sf", C.c_void_p), ("b_delta", C.c_void_p),
-                ("Sf", C.c_void_p), ("Cf", C.c_void_p), ("C", C.c_void_p), ("b_Sf", C.c_void_p)]
+                ("Sf", C.c_void_p), ("Cf", C.c_void_p), ("C", C.c_void_p), ("b_Sf", C.c_void_p),
+                ("gamma", C.c_void_p), ("b_gamma", C.c_void_p)]
 
 
 class Perf(C.Structure):
@@ -82,6 +83,7 @@ def lib():
         _lib.orc_grad.argtypes = [C.POINTER(_Mesh), vp, vp, vp, vp]
         _lib.orc_grad_bc.argtypes = [C.POINTER(_Mesh), vp, vp, vp, vp]
         _lib.orc_lap_correction.argtypes = [C.POINTER(_Mesh), C.c_double, vp, vp, vp, vp]
+        _lib.orc_face_gamma.argtypes = [C.POINTER(_Mesh), vp, vp, vp, vp]
         _lib.orc_laplacian_foam_corrected.argtypes = [C.POINTER(_Mesh), C.c_double, C.c_double, vp, vp,
                                                       C.c_int32, C.c_int32, C.c_double, C.c_double,
                                                       C.c_int32, C.c_int32, C.POINTER(Perf)]
@@ -125,7 +127,20 @@ class OMesh:
                        _p(self.owner), _p(self.neighbour), _p(self.mag_sf), _p(self.delta),
                        _p(self.V), _p(self.patch_type), _p(self.patch_start), _p(self.b_cells),
                        _p(self.b_mag_sf), _p(self.b_delta), _p(self.Sf), _p(self.Cf), _p(self.C),
-                       _p(self.b_Sf))
+                       _p(self.b_Sf), None, None)
+        # spatially varying DT (mesh.DT_field): face
+        # diffusivities by linear interpolation with the geometric weights
+        self.DT_field = getattr(mesh, "DT_field", None)
+        self.gamma = self.b_gamma = None
+        if self.DT_field is not None:
+            if not self.has_geometry:
+                raise ValueError("a DT field needs the full geometry (interpolation weights)")
+            self.DT_field = np.ascontiguousarray(self.DT_field, dtype=np.float64)
+            w = np.zeros(self.n_faces)
+            lib().orc_weights(C.byref(self.s), _p(w))
+            self.gamma, self.b_gamma = np.zeros(self.n_faces), np.zeros(self.n_bfaces)
+            lib().orc_face_gamma(C.byref(self.s), _p(w), _p(self.DT_field), _p(self.gamma), _p(self.b_gamma))
+            self.s.gamma, self.s.b_gamma = _p(self.gamma), _p(self.b_gamma)
 
     @property
     def has_geometry(self):
@@ -313,3 +328,14 @@ def laplacian_foam_corrected(mesh, T0, n_steps, n_corr=1, DT=1.0, dt=0.2, tol=1e
     if rc:
         raise MemoryError
     return T, bv, [perfs[i].as_dict() for i in range(n_steps * (n_corr + 1))]
+
+
+def face_gamma(mesh, DT_field):
+    """Face / boundary diffusivities of a cell DT field (linear interpolation
+    with the weights of P:321-334; boundary DT[faceCell])."""
+    om = _om(mesh)
+    _need_geom(om)
+    w = weights(om)
+    g, gb = np.zeros(om.n_faces), np.zeros(om.n_bfaces)
+    lib().orc_face_gamma(C.byref(om.s), _p(w), _p(np.ascontiguousarray(DT_field, np.float64)), _p(g), _p(gb))
+    return g, gb

@@ -51,6 +51,11 @@ typedef struct {
     const double *Sf, *Cf;                 /* [n_faces][3] */
     const double *C;                       /* [n_cells][3] */
     const double *b_Sf;                    /* [n_bfaces][3] */
+    /* spatially varying DT (optional, NULL = the scalar DT argument): the
+     * face diffusivity gamma_f (linear interpolation of the cell field,
+     * orc_face_gamma) and its boundary values */
+    const double *gamma;                   /* [n_faces] */
+    const double *b_gamma;                 /* [n_bfaces] */
 } orc_mesh;
 
 typedef struct {
@@ -110,7 +115,8 @@ int orc_assemble(const orc_mesh *m, double DT, double dt, const double *T0,
         source[c] = (rDeltaT * T0[c]) * m->V[c];        /* S[c] */
     }
     for (f = 0; f < m->n_faces; f++) {                 /* file order */
-        double u = m->delta[f] * (DT * m->mag_sf[f]);
+        double g = m->gamma ? m->gamma[f] : DT;         /* gammaMagSf = gamma_f*magSf */
+        double u = m->delta[f] * (g * m->mag_sf[f]);
         upper[f] = -u;
         L[m->owner[f]] -= u;
         L[m->neighbour[f]] -= u;
@@ -121,7 +127,7 @@ int orc_assemble(const orc_mesh *m, double DT, double dt, const double *T0,
         int32_t t = m->patch_type[p];
         for (i = m->patch_start[p]; i < m->patch_start[p + 1]; i++) {
             int32_t cc = m->b_cells[i];
-            double gms = DT * m->b_mag_sf[i];
+            double gms = (m->b_gamma ? m->b_gamma[i] : DT) * m->b_mag_sf[i];
             double a = gms * m->b_delta[i];
             if (t == ORC_FIXED_VALUE) {
                 double bc = gms * (m->b_delta[i] * b_value[i]);
@@ -442,7 +448,7 @@ void orc_lap_correction(const orc_mesh *m, double DT, const double *w, const dou
             const double gf = w[f] * (grad[3 * P + k] - grad[3 * N + k]) + grad[3 * N + k];
             cs += corr[3 * f + k] * gf;
         }
-        flux = (DT * m->mag_sf[f]) * cs;
+        flux = ((m->gamma ? m->gamma[f] : DT) * m->mag_sf[f]) * cs;
         lapSrc[P] += flux;   /* surfaceIntegrate: owner +, neighbour - */
         lapSrc[N] -= flux;
     }
@@ -496,4 +502,17 @@ int orc_laplacian_foam_corrected(const orc_mesh *m, double DT, double dt, double
     free(diag); free(source); free(upper); free(w); free(corr); free(grad); free(lapSrc); free(T0);
     free(b_int); free(b_bnd);
     return rc;
+}
+
+/* Spatially varying DT: the laplacian's face
+ * diffusivity is the linear interpolate of the cell field,
+ * gamma_f = lambda*(DT_P - DT_N) + DT_N (Listing "dotInterpolate loop" form,
+ * P:293-299, with the weights of P:321-334); on boundary faces the field's
+ * patch value, DT[faceCell] (zeroGradient DT, reading A38). */
+void orc_face_gamma(const orc_mesh *m, const double *w, const double *DTc, double *gamma, double *b_gamma)
+{
+    int32_t f, i;
+    for (f = 0; f < m->n_faces; f++)
+        gamma[f] = w[f] * (DTc[m->owner[f]] - DTc[m->neighbour[f]]) + DTc[m->neighbour[f]];
+    for (i = 0; i < m->n_bfaces; i++) b_gamma[i] = DTc[m->b_cells[i]];
 }

@@ -1,5 +1,6 @@
 // C ABI entry points (include/lfoam.h).  Every call catches everything and
 // maps it to an lf_status; nothing throws or aborts across the boundary.
+#include <cmath>
 #include <cstdio>
 
 #include "host.h"
@@ -255,6 +256,32 @@ lf_status field_set(lf_mesh *M, lf_field f, int32_t patch, const double *v, int6
         launch_permute(s, M->n, M->cellPerm, M->scratch, M->T, false);
       }
       M->sumPsiValid = false;
+    } else if (f == LF_FIELD_DT) {
+      LF_REQUIRE(patch == -1, "patch must be -1 for LF_FIELD_DT");
+      LF_REQUIRE(n == M->n, "n must equal n_cells");
+      LF_REQUIRE(M->hasGeom, "a DT field needs the full geometry (interpolation weights)");
+      LF_REQUIRE(M->nproc == 0, "a DT field is not supported with processor patches");
+      if (!on_device)
+        for (int64_t i = 0; i < n; ++i)
+          LF_REQUIRE(v[i] > 0.0 && std::isfinite(v[i]), "DT must be > 0 and finite");
+      if (!M->DTc) {
+        M->DTc = M->arena.alloc<double>(M->n);
+        M->gammaF = M->arena.alloc<double>(M->F);
+        M->gammaB = M->arena.alloc<double>(M->B);
+      }
+      if (!M->renumbered) {
+        LF_CUDA(cudaMemcpyAsync(M->DTc, v, sizeof(double) * n, kind, s));
+      } else {
+        LF_CUDA(cudaMemcpyAsync(M->scratch, v, sizeof(double) * n, kind, s));
+        launch_permute(s, M->n, M->cellPerm, M->scratch, M->DTc, false);
+      }
+      M->ctx->launch(LF_K_NONORTH, [&] {
+        launch_face_gamma(s, M->md, M->geo, M->ownerInt, M->bCell, M->DTc, M->gammaF, M->gammaB);
+      });
+      M->mdVar = M->md;
+      M->mdVar.gammaF = M->gammaF;
+      M->mdVar.gammaB = M->gammaB;
+      M->dtSet = true;
     } else if (f == LF_FIELD_PATCH_VALUE) {
       LF_REQUIRE(patch >= 0 && patch < M->nPatches, "patch out of range");
       const int32_t off = M->patchStart[patch], cnt = M->patchStart[patch + 1] - off;
@@ -282,6 +309,16 @@ lf_status field_get(const lf_mesh *Mc, lf_field f, int32_t patch, double *v, int
         LF_CUDA(cudaMemcpyAsync(v, M->T, sizeof(double) * n, kind, s));
       } else {
         launch_permute(s, M->n, M->cellPerm, M->T, M->scratch, true);
+        LF_CUDA(cudaMemcpyAsync(v, M->scratch, sizeof(double) * n, kind, s));
+      }
+    } else if (f == LF_FIELD_DT) {
+      LF_REQUIRE(patch == -1, "patch must be -1 for LF_FIELD_DT");
+      LF_REQUIRE(n == M->n, "n must equal n_cells");
+      if (!M->dtSet) throw Error{LF_ERR_STATE, "the DT field was never set"};
+      if (!M->renumbered) {
+        LF_CUDA(cudaMemcpyAsync(v, M->DTc, sizeof(double) * n, kind, s));
+      } else {
+        launch_permute(s, M->n, M->cellPerm, M->DTc, M->scratch, true);
         LF_CUDA(cudaMemcpyAsync(v, M->scratch, sizeof(double) * n, kind, s));
       }
     } else if (f == LF_FIELD_PATCH_VALUE) {
@@ -315,15 +352,16 @@ lf_status laplacian_assemble(lf_mesh *M, const lf_laplacian_params *p, lf_ldu **
     LF_REQUIRE(p->DT > 0.0 && p->dt > 0.0, "DT and dt must be > 0");
     lf_context *ctx = M->ctx;
     cudaStream_t s = ctx->stream;
+    const MeshDev &md = mesh_for(M, p);
     const double *lapSrc = nullptr;
     if (p->corrected) {
       require_corrected(M);
-      correction_source(M, p->DT, M->T);
+      correction_source(M, md, p->DT, M->T);
       lapSrc = M->lapSrc;
     }
     field_halo(M, M->T);
     ctx->launch(LF_K_ASSEMBLE, [&] {
-      launch_assemble(s, M->Lasm, M->md, M->ld, p->DT, 1.0 / p->dt, M->T, M->ws.recvT, false, M->ws, nullptr,
+      launch_assemble(s, M->Lasm, md, M->ld, p->DT, 1.0 / p->dt, M->T, M->ws.recvT, false, M->ws, nullptr,
                       lapSrc);
     });
     M->ldu.assembled = true;
@@ -412,6 +450,7 @@ lf_status laplacianFoam_step(lf_mesh *M, const lf_laplacian_params *p, const lf_
       require_corrected(M);
       LF_REQUIRE(p->n_non_orth_correctors >= 0, "n_non_orth_correctors must be >= 0");
     }
+    const MeshDev &md = mesh_for(M, p);  // validates variable_DT up front
     if (n_steps == 0) return;
     upload_controls(M, c, M->T);
     if (!p->corrected) {
@@ -429,7 +468,7 @@ lf_status laplacianFoam_step(lf_mesh *M, const lf_laplacian_params *p, const lf_
       if (keepT0)
         LF_CUDA(cudaMemcpyAsync(M->T0, M->T, sizeof(double) * M->n, cudaMemcpyDeviceToDevice, M->ctx->stream));
       for (int32_t k = 0; k < passes; ++k) {
-        correction_source(M, p->DT, M->T);
+        correction_source(M, md, p->DT, M->T);
         solve_loop(M, c, M->T, true, p, per_step ? per_step + (int64_t)st * passes + k : nullptr,
                    keepT0 ? M->T0 : nullptr, M->lapSrc);
         M->ldu.assembled = true;

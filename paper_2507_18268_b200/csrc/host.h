@@ -109,6 +109,10 @@ struct lf_mesh {
   double *gradS = nullptr;   // [3][n] fvc::grad(T), SoA
   double *lapSrc = nullptr;  // [n] explicit laplacian correction source
   double *T0 = nullptr;      // [n] old-time T of the current step (correctors)
+  // spatially varying DT (LF_FIELD_DT): cell field and face diffusivities
+  double *DTc = nullptr, *gammaF = nullptr, *gammaB = nullptr;
+  bool dtSet = false;
+  lf::MeshDev mdVar{};       // md with gammaF/gammaB set (variable_DT solves)
   ~lf_mesh();
 };
 
@@ -118,8 +122,10 @@ void solve_loop(lf_mesh *M, const lf_solver_controls *c, double *psi, bool fromA
                 const lf_laplacian_params *p, lf_solver_perf *out, const double *T0 = nullptr,
                 const double *lapSrc = nullptr);
 // nonorth path (solver.cpp): gradS <- grad(x), lapSrc <- correction of gradS
-void correction_source(lf_mesh *M, double DT, const double *x);
+void correction_source(lf_mesh *M, const MeshDev &md, double DT, const double *x);
 void require_corrected(const lf_mesh *M);
+// the MeshDev a solve with params p assembles with (variable DT or not)
+const MeshDev &mesh_for(const lf_mesh *M, const lf_laplacian_params *p);
 void halo_exchange(lf_mesh *M, const double *send, double *recv);
 void field_halo(lf_mesh *M, const double *x);
 // p2p.cpp

@@ -405,7 +405,7 @@ __global__ void __launch_bounds__(BS, LF_MINB)
     const int l0 = m.losortStart[c], l1 = m.losortStart[c + 1];
     for (int j = l0; j < l1; ++j) {
       const int f = m.losort[j];
-      const double u = __dmul_rn(m.delta[f], __dmul_rn(DT, m.magSf[f]));
+      const double u = __dmul_rn(m.delta[f], __dmul_rn(m.gammaF ? m.gammaF[f] : DT, m.magSf[f]));
       L = __dsub_rn(L, u);
       if (SETUP) {
         sOff = fma(-u, T[m.losortOwner[j]], sOff);
@@ -414,7 +414,7 @@ __global__ void __launch_bounds__(BS, LF_MINB)
     }
     const int o0 = m.ownerStart[c], o1 = m.ownerStart[c + 1];
     for (int i = o0; i < o1; ++i) {
-      const double u = __dmul_rn(m.delta[i], __dmul_rn(DT, m.magSf[i]));
+      const double u = __dmul_rn(m.delta[i], __dmul_rn(m.gammaF ? m.gammaF[i] : DT, m.magSf[i]));
       a.upper[i] = -u;
       if (m.K > 0) a.upperE[(i - o0) * m.ldE + c] = -u;
       L = __dsub_rn(L, u);
@@ -431,7 +431,7 @@ __global__ void __launch_bounds__(BS, LF_MINB)
     const int b0 = m.bcStart[c], b1 = m.bcStart[c + 1];
     for (int k = b0; k < b1; ++k) {
       const int i = m.bcFace[k];
-      const double gms = __dmul_rn(DT, m.bMagSf[i]);
+      const double gms = __dmul_rn(m.gammaB ? m.gammaB[i] : DT, m.bMagSf[i]);
       const double aa = __dmul_rn(gms, m.bDelta[i]);
       d = __dadd_rn(d, aa);
       a.bInt[i] = aa;

@@ -90,6 +90,9 @@ struct MeshDev {
   // slot k of cell c at k*n + c.  See kernels.cu header.
   int32_t K, ldE;  // ldE: slab stride (n rounded up to 4: 16-byte aligned slabs)
   const int32_t *nbrE, *loE;
+  // spatially varying DT (§8(f) row 2): face / boundary diffusivities, or
+  // null (the scalar DT argument of the kernels)
+  const double *gammaF, *gammaB;
 };
 
 struct LduDev {
@@ -159,6 +162,8 @@ void launch_grad(cudaStream_t s, const Launch &L, const MeshDev &m, const GeomDe
                  double *gradS, double *gradA);
 void launch_grad_bc(cudaStream_t s, const MeshDev &m, const GeomDev &g, const int32_t *bCell,
                     const double *x, const double *gradS, double *bgradA);
+void launch_face_gamma(cudaStream_t s, const MeshDev &m, const GeomDev &g, const int32_t *owner,
+                       const int32_t *bCell, const double *DTc, double *gammaF, double *gammaB);
 void launch_lap_corr(cudaStream_t s, const Launch &L, const MeshDev &m, const GeomDev &g, double DT,
                      const double *gradS, double *lapSrc);
 void launch_pcg_setup(cudaStream_t s, const Launch &L, const MeshDev &m, const LduDev &a,

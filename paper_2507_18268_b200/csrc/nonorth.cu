@@ -153,7 +153,7 @@ __device__ __forceinline__ double face_flux(const GeomDev &g, const MeshDev &m, 
     const double gP = gradS[(size_t)k * n + P], gN = gradS[(size_t)k * n + N];
     cs = add(cs, mul(g.corr[(size_t)k * F + f], add(mul(w, sub(gP, gN)), gN)));
   }
-  return mul(mul(DT, m.magSf[f]), cs);
+  return mul(mul(m.gammaF ? m.gammaF[f] : DT, m.magSf[f]), cs);
 }
 
 // Explicit non-orthogonal part of gaussLaplacianScheme::fvmLaplacian:
@@ -171,6 +171,23 @@ __global__ void __launch_bounds__(NB) k_lap_corr(MeshDev m, GeomDev g, double DT
       acc = add(acc, face_flux(g, m, DT, f, gradS, c, m.nbr[f]));
     const double V = m.V[c];
     lapSrc[c] = -mul(V, dvd(acc, V));
+  }
+}
+
+// Face diffusivity of a cell DT field (§8(f) row 2): linear interpolation
+// gamma_f = w (DT_P - DT_N) + DT_N (P:293-299 with the weights of P:321-334),
+// boundary faces DT[faceCell].
+__global__ void __launch_bounds__(NB) k_face_gamma(int32_t F, int32_t B, const int32_t *__restrict__ owner,
+                                                   const int32_t *__restrict__ nbr, const int32_t *__restrict__ bCell,
+                                                   const double *__restrict__ w, const double *__restrict__ DTc,
+                                                   double *__restrict__ gammaF, double *__restrict__ gammaB) {
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < F + B; i += gridDim.x * blockDim.x) {
+    if (i < F) {
+      const double dN = DTc[nbr[i]];
+      gammaF[i] = add(mul(w[i], sub(DTc[owner[i]], dN)), dN);
+    } else {
+      gammaB[i - F] = DTc[bCell[i - F]];
+    }
   }
 }
 
@@ -196,6 +213,13 @@ void launch_grad_bc(cudaStream_t s, const MeshDev &m, const GeomDev &g, const in
                     const double *x, const double *gradS, double *bgradA) {
   if (g.B <= 0) return;
   k_grad_bc<<<grid_for(g.B), NB, 0, s>>>(m, g, bCell, x, gradS, bgradA);
+}
+
+void launch_face_gamma(cudaStream_t s, const MeshDev &m, const GeomDev &g, const int32_t *owner,
+                       const int32_t *bCell, const double *DTc, double *gammaF, double *gammaB) {
+  if (g.F + g.B <= 0) return;
+  k_face_gamma<<<grid_for((int64_t)g.F + g.B), NB, 0, s>>>(g.F, g.B, owner, m.nbr, bCell, g.w, DTc, gammaF,
+                                                             gammaB);
 }
 
 void launch_lap_corr(cudaStream_t s, const Launch &L, const MeshDev &m, const GeomDev &g, double DT,

@@ -198,11 +198,19 @@ void require_corrected(const lf_mesh *M) {
 
 // gradS <- fvc::grad(x); lapSrc <- explicit non-orthogonal laplacian source
 // of that gradient (two gathers, stream-ordered).
-void correction_source(lf_mesh *M, double DT, const double *x) {
+void correction_source(lf_mesh *M, const MeshDev &md, double DT, const double *x) {
   lf_context *ctx = M->ctx;
-  ctx->launch(LF_K_NONORTH, [&] { launch_grad(ctx->stream, M->Lasm, M->md, M->geo, x, M->gradS, nullptr); });
+  ctx->launch(LF_K_NONORTH, [&] { launch_grad(ctx->stream, M->Lasm, md, M->geo, x, M->gradS, nullptr); });
   ctx->launch(LF_K_NONORTH,
-              [&] { launch_lap_corr(ctx->stream, M->Lasm, M->md, M->geo, DT, M->gradS, M->lapSrc); });
+              [&] { launch_lap_corr(ctx->stream, M->Lasm, md, M->geo, DT, M->gradS, M->lapSrc); });
+}
+
+const MeshDev &mesh_for(const lf_mesh *M, const lf_laplacian_params *p) {
+  if (p && p->variable_DT) {
+    if (!M->dtSet) throw Error{LF_ERR_STATE, "variable_DT: set the DT field first (field_set LF_FIELD_DT)"};
+    return M->mdVar;
+  }
+  return M->md;
 }
 
 void solve_loop(lf_mesh *M, const lf_solver_controls *c, double *psi, bool fromAssembly,
@@ -217,7 +225,8 @@ void solve_loop(lf_mesh *M, const lf_solver_controls *c, double *psi, bool fromA
   if (host_halo(M)) exchange_field(M, psi, ws.recvT);
   if (fromAssembly) {
     ctx->launch(LF_K_ASSEMBLE, [&] {
-      launch_assemble(s, M->Lasm, M->md, M->ld, p->DT, 1.0 / p->dt, psi, ws.recvT, true, ws, T0, lapSrc);
+      launch_assemble(s, M->Lasm, mesh_for(M, p), M->ld, p->DT, 1.0 / p->dt, psi, ws.recvT, true, ws, T0,
+                      lapSrc);
     });
   } else {
     ctx->launch(LF_K_SETUP, [&] { launch_pcg_setup(s, M->Lsetup, M->md, M->ld, ws.recvT, ws); });

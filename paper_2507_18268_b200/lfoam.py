@@ -22,7 +22,7 @@ LF_OK = 0
 STATUS = {0: "LF_OK", 1: "LF_ERR_INVALID_ARG", 2: "LF_ERR_STATE", 3: "LF_ERR_OOM",
           4: "LF_ERR_CUDA", 5: "LF_ERR_NCCL", 6: "LF_ERR_INTERNAL"}
 PATCH_TYPES = {"fixedValue": 0, "zeroGradient": 1, "processor": 2}
-FIELD_T, FIELD_PATCH_VALUE = 0, 1
+FIELD_T, FIELD_PATCH_VALUE, FIELD_DT = 0, 1, 2
 KERNELS = {"assemble": 0, "setup": 1, "phase1": 2, "phase2": 3, "amul": 4, "sumpsi": 5, "pack": 6, "pcg": 7,
            "nonorth": 8}
 OPTIONS = {"persistent": 0, "graphs": 1}
@@ -49,7 +49,7 @@ class MeshDesc(C.Structure):
 
 class Params(C.Structure):
     _fields_ = [("DT", C.c_double), ("dt", C.c_double), ("corrected", C.c_int32),
-                ("n_non_orth_correctors", C.c_int32)]
+                ("n_non_orth_correctors", C.c_int32), ("variable_DT", C.c_int32)]
 
 
 class Controls(C.Structure):
@@ -258,6 +258,9 @@ class Mesh:
         self.n_faces = int(own.shape[0])
         self.n_bfaces = int(sum(self.patch_sizes))
         self.renumber = renumber
+        self.variable_dt = False
+        if getattr(m, "DT_field", None) is not None:
+            self.set_DT_field(m.DT_field)
 
     def info(self):
         n, F, B, b = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int64()
@@ -300,6 +303,22 @@ class Mesh:
         _check(lib().field_get(self.h, FIELD_T, -1, _ptr(a), self.n_cells, 0))
         return a
 
+    def set_DT_field(self, v):
+        """Spatially varying DT (cell values, caller numbering); later solves
+        use it unless called with variable_DT=False."""
+        if _is_device(v):
+            _check_dev(v, self.n_cells)
+            _check(lib().field_set(self.h, FIELD_DT, -1, _ptr(v), self.n_cells, 1))
+        else:
+            a = _host(v, np.float64)
+            _check(lib().field_set(self.h, FIELD_DT, -1, _ptr(a), a.shape[0], 0))
+        self.variable_dt = True
+
+    def get_DT_field(self):
+        a = np.zeros(self.n_cells)
+        _check(lib().field_get(self.h, FIELD_DT, -1, _ptr(a), self.n_cells, 0))
+        return a
+
     def set_patch_value(self, patch: int, v):
         a = _host(v, np.float64)
         _check(lib().field_set(self.h, FIELD_PATCH_VALUE, patch, _ptr(a), a.shape[0], 0))
@@ -313,18 +332,23 @@ class Mesh:
         _check(lib().lf_permute(self.h, 1 if to_internal else 0, _ptr(x), _ptr(y)))
 
     # ------------------------------------------------------------ ops
-    def assemble(self, DT: float = 1.0, dt: float = 0.2, corrected: bool = False) -> "Ldu":
+    def _var(self, variable_DT):
+        return int(self.variable_dt if variable_DT is None else variable_DT)
+
+    def assemble(self, DT: float = 1.0, dt: float = 0.2, corrected: bool = False,
+                 variable_DT: Optional[bool] = None) -> "Ldu":
         h = C.c_void_p()
-        _check(lib().laplacian_assemble(self.h, C.byref(Params(DT, dt, int(corrected), 0)), C.byref(h)))
+        prm = Params(DT, dt, int(corrected), 0, self._var(variable_DT))
+        _check(lib().laplacian_assemble(self.h, C.byref(prm), C.byref(h)))
         return Ldu(self, h)
 
     def step(self, n_steps: int, DT: float = 1.0, dt: float = 0.2, corrected: bool = False,
-             n_non_orth_correctors: int = 0, **ctl) -> List[Dict]:
+             n_non_orth_correctors: int = 0, variable_DT: Optional[bool] = None, **ctl) -> List[Dict]:
         """n_steps time steps; one perf dict per solve (n_steps * (1 +
         n_non_orth_correctors) when corrected)."""
         nsol = n_steps * (1 + (n_non_orth_correctors if corrected else 0))
         perfs = (Perf * max(nsol, 1))()
-        prm = Params(DT, dt, int(corrected), int(n_non_orth_correctors))
+        prm = Params(DT, dt, int(corrected), int(n_non_orth_correctors), self._var(variable_DT))
         _check(lib().laplacianFoam_step(self.h, C.byref(prm), C.byref(controls(**ctl)), n_steps, perfs))
         return [perfs[i].as_dict() for i in range(nsol)]
 
