@@ -16,11 +16,13 @@ from .cube import (Mesh, Patch, block_mesh, permute_mesh, sine_field, canonical_
                    cosine_field, multimode_field, random_field, hot_plate,
                    cube_counts, mesh_points_faces, CONFIGS, config_mesh,
                    skewed_block_mesh, with_geometry, PATCH_NAMES,
-                   skewed_config_mesh, SKEW_SHEAR, layered_dt_field)
+                   skewed_config_mesh, SKEW_SHEAR, layered_dt_field,
+                   PROTOCOL_MESHES, PROTOCOL, protocol_mesh)
 
 __all__ = ["Mesh", "Patch", "block_mesh", "permute_mesh", "sine_field", "canonical_field",
            "CANONICAL_AMPLITUDE",
            "cosine_field", "multimode_field", "random_field", "hot_plate",
            "cube_counts", "mesh_points_faces", "CONFIGS", "config_mesh",
            "skewed_block_mesh", "with_geometry", "PATCH_NAMES",
-           "skewed_config_mesh", "SKEW_SHEAR", "layered_dt_field"]
+           "skewed_config_mesh", "SKEW_SHEAR", "layered_dt_field",
+           "PROTOCOL_MESHES", "PROTOCOL", "protocol_mesh"]

@@ -424,3 +424,17 @@ def layered_dt_field(mesh: Mesh, ratio: float = 10.0) -> np.ndarray:
     nx, ny, nz = mesh.dims
     k = mesh.block_labels() // (nx * ny)
     return np.where(k < nz // 2, 1.0, 1.0 / ratio)
+
+
+# Paper protocol (Table 1 meshes: 100 s
+# of simulated time at dt = 0.2 s, PCG + diagonal, 5 repeats): the hot plate
+# with a diffusivity small enough that the transient spans the whole 100 s
+# (slowest mode e^{-pi^2 DT t}: ~ e^{-1} at t = 100 s for DT = 1e-3), so no
+# step degenerates (reading A30).
+PROTOCOL_MESHES = {"S": 100, "M": 200, "L": 300, "XL": 400}
+PROTOCOL = dict(DT=1e-3, dt=0.2, steps=500, repeats=5)
+
+
+def protocol_mesh(name_or_N) -> Mesh:
+    N = PROTOCOL_MESHES.get(name_or_N, name_or_N) if isinstance(name_or_N, str) else int(name_or_N)
+    return hot_plate(N)

@@ -488,3 +488,26 @@ def test_reading_A30_normfactor_floor():
     ref = g ** 100 * c
     assert np.max(np.abs(T - ref)) <= 1e-8 * np.max(np.abs(ref))
     assert min(p["n_iterations"] for p in perfs) >= 15
+
+
+def test_protocol_hot_plate_is_one_dimensional():
+    """SURVEY §8(f) row 4 workload: the 3-D hot plate with zeroGradient y/z
+    walls equals the 1-D implicit-Euler two-point solution (banded direct
+    solve) on every x-line."""
+    from scipy.linalg import solve_banded
+    pr = meshgen.PROTOCOL
+    N, steps = 8, 40
+    m = meshgen.protocol_mesh(N)
+    T, _, _ = oracle.laplacian_foam(m, np.zeros(m.n_cells), steps, DT=pr["DT"], dt=pr["dt"], tol=1e-14)
+    h = 1.0 / N
+    a, ab = pr["DT"] / h, 2 * pr["DT"] / h
+    band = np.zeros((3, N))
+    band[0, 1:] = band[2, :-1] = -a
+    band[1] = h / pr["dt"] + 2 * a
+    band[1, 0] = band[1, -1] = h / pr["dt"] + a + ab
+    t = np.zeros(N)
+    for _ in range(steps):
+        b = h / pr["dt"] * t
+        b[0] += ab
+        t = solve_banded((1, 1), band, b)
+    assert np.max(np.abs(T.reshape(-1, N) - t)) < 1e-12
