@@ -17,7 +17,8 @@ from .cube import (Mesh, Patch, block_mesh, permute_mesh, sine_field, canonical_
                    cube_counts, mesh_points_faces, CONFIGS, config_mesh,
                    skewed_block_mesh, with_geometry, PATCH_NAMES,
                    skewed_config_mesh, SKEW_SHEAR, layered_dt_field,
-                   PROTOCOL_MESHES, PROTOCOL, protocol_mesh)
+                   PROTOCOL_MESHES, PROTOCOL, protocol_mesh,
+                   relabel_mesh, colour_order, colour_mesh)
 
 __all__ = ["Mesh", "Patch", "block_mesh", "permute_mesh", "sine_field", "canonical_field",
            "CANONICAL_AMPLITUDE",
@@ -25,4 +26,5 @@ __all__ = ["Mesh", "Patch", "block_mesh", "permute_mesh", "sine_field", "canonic
            "cube_counts", "mesh_points_faces", "CONFIGS", "config_mesh",
            "skewed_block_mesh", "with_geometry", "PATCH_NAMES",
            "skewed_config_mesh", "SKEW_SHEAR", "layered_dt_field",
-           "PROTOCOL_MESHES", "PROTOCOL", "protocol_mesh"]
+           "PROTOCOL_MESHES", "PROTOCOL", "protocol_mesh",
+           "relabel_mesh", "colour_order", "colour_mesh"]

@@ -281,6 +281,71 @@ def permute_mesh(mesh: Mesh, cell_seed: int = 1, face_seed: int = 2) -> Mesh:
                 old_of_new=base[old_of_new].astype(np.int32), face_old_of_new=fperm, **geo)
 
 
+def relabel_mesh(mesh: Mesh, old_of_new: np.ndarray) -> Mesh:
+    """The same mesh with cell i of the result = cell old_of_new[i] of
+    `mesh`; faces relabelled owner = min, neighbour = max (LDU convention)
+    and re-sorted upper-triangular (owner, then neighbour) as OpenFOAM's
+    renumberMesh leaves them."""
+    n = mesh.n_cells
+    old_of_new = np.asarray(old_of_new, dtype=np.int64)
+    new_of_old = np.empty(n, dtype=np.int64)
+    new_of_old[old_of_new] = np.arange(n)
+    a, b = new_of_old[mesh.owner], new_of_old[mesh.neighbour]
+    lo, hi = np.minimum(a, b), np.maximum(a, b)
+    fperm = np.lexsort((hi, lo))
+    owner, neighbour = lo[fperm].astype(np.int32), hi[fperm].astype(np.int32)
+    patches = [dataclasses.replace(p, face_cells=new_of_old[p.face_cells].astype(np.int32))
+               for p in mesh.patches]
+    geo = {}
+    if mesh.Sf is not None:
+        sgn = np.where(a > b, -1.0, 1.0)[fperm][:, None]
+        geo = dict(Sf=mesh.Sf[fperm] * sgn, Cf=mesh.Cf[fperm].copy(), C=mesh.C[old_of_new],
+                   affine=mesh.affine, grid_lines=mesh.grid_lines)
+    if mesh.DT_field is not None:
+        geo["DT_field"] = mesh.DT_field[old_of_new]
+    base = mesh.block_labels()
+    face_base = (mesh.face_old_of_new if mesh.face_old_of_new is not None
+                 else np.arange(mesh.n_faces, dtype=np.int64))
+    return Mesh(n, owner, neighbour, mesh.mag_sf[fperm], mesh.delta[fperm], mesh.V[old_of_new], patches,
+                dims=mesh.dims, extent=mesh.extent, old_of_new=base[old_of_new].astype(np.int32),
+                face_old_of_new=face_base[fperm], **geo)
+
+
+def colour_order(mesh: Mesh) -> np.ndarray:
+    """Greedy first-fit colouring in label order — colour(c) = the smallest
+    colour not used by a lower-labelled neighbour — and the cells sorted by
+    (colour, label): returns old_of_new.  Under this numbering every colour
+    is a contiguous block with no internal coupling, so the sequential DIC
+    loops run in #colours parallel levels (2 on a structured hex block,
+    where the colour is the parity of i+j+k).  Pure Python loop: meant for
+    test-sized meshes; the library's renumber = 2 does the same in C++."""
+    n = mesh.n_cells
+    a = np.concatenate([mesh.owner, mesh.neighbour]).astype(np.int64)
+    b = np.concatenate([mesh.neighbour, mesh.owner]).astype(np.int64)
+    sel = b < a                       # b is a lower neighbour of a
+    a, b = a[sel], b[sel]
+    idx = np.argsort(a, kind="stable")
+    a, b = a[idx], b[idx]
+    start = np.searchsorted(a, np.arange(n + 1))
+    col = np.zeros(n, dtype=np.int64)
+    bl = b.tolist()
+    st = start.tolist()
+    cl = [0] * n
+    for c in range(n):
+        used = {cl[j] for j in bl[st[c]:st[c + 1]]}
+        k = 0
+        while k in used:
+            k += 1
+        cl[c] = k
+    col[:] = cl
+    return np.argsort(col, kind="stable")
+
+
+def colour_mesh(mesh: Mesh) -> Mesh:
+    """The multicolour numbering of `mesh` (colour_order + relabel_mesh)."""
+    return relabel_mesh(mesh, colour_order(mesh))
+
+
 # ----------------------------------------------------------------- fields
 def sine_field(mesh: Mesh, k=(1, 1, 1), amp: float = 1.0) -> np.ndarray:
     """T0 = amp * prod_d sin(k_d pi x_d / L_d) at cell centres (reading A6)."""

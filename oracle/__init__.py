@@ -26,6 +26,9 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "lfoam_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 _TYPES = {"fixedValue": 0, "zeroGradient": 1, "processor": 2}
+# preconditioners (OpenFOAM fvSolution names): diagonal (the paper's),
+# DIC
+PRECONDITIONERS = {"diagonal": 0, "DIC": 1}
 
 
 def build(force: bool = False) -> str:
@@ -77,6 +80,12 @@ def lib():
         _lib.orc_laplacian_foam.argtypes = [C.POINTER(_Mesh), C.c_double, C.c_double, vp, vp,
                                             C.c_int32, C.c_double, C.c_double, C.c_int32,
                                             C.c_int32, GSUM, HALO, vp, C.POINTER(Perf)]
+        _lib.orc_pcg_p.argtypes = [C.POINTER(_Mesh), vp, vp, vp, vp, vp, C.c_double, C.c_double,
+                                   C.c_int32, C.c_int32, C.c_int32, GSUM, HALO, vp, C.POINTER(Perf)]
+        _lib.orc_laplacian_foam_p.argtypes = [C.POINTER(_Mesh), C.c_double, C.c_double, vp, vp,
+                                              C.c_int32, C.c_double, C.c_double, C.c_int32,
+                                              C.c_int32, C.c_int32, GSUM, HALO, vp, C.POINTER(Perf)]
+        _lib.orc_dic.argtypes = [C.POINTER(_Mesh), vp, vp, vp, vp, vp]
         _lib.orc_patch_values.argtypes = [C.POINTER(_Mesh), vp, vp]
         _lib.orc_weights.argtypes = [C.POINTER(_Mesh), vp]
         _lib.orc_corr_vectors.argtypes = [C.POINTER(_Mesh), vp]
@@ -219,36 +228,51 @@ def _callbacks(gsum: Optional[Callable], halo: Optional[Callable], n_cells: int,
 
 
 def pcg(mesh, sys: dict, psi: np.ndarray, tol=1e-10, rel_tol=0.0, max_iter=1000, min_iter=0,
-        gsum=None, halo=None):
-    """OpenFOAM PCG (diagonal preconditioner). Returns (psi, perf dict)."""
+        gsum=None, halo=None, precond="diagonal"):
+    """OpenFOAM PCG (diagonal or DIC preconditioner). Returns (psi, perf dict)."""
     om = _om(mesh)
     psi = np.array(psi, dtype=np.float64, copy=True)
     perf = Perf()
     g, h = _callbacks(gsum, halo, om.n_cells, om.n_bfaces)
     bc = sys.get("boundary_coeffs")
     bc = np.zeros(om.n_bfaces) if bc is None else np.ascontiguousarray(bc, np.float64)
-    rc = lib().orc_pcg(C.byref(om.s), _p(np.ascontiguousarray(sys["diag"], np.float64)),
-                       _p(np.ascontiguousarray(sys["upper"], np.float64)), _p(bc),
-                       _p(np.ascontiguousarray(sys["source"], np.float64)), _p(psi),
-                       tol, rel_tol, max_iter, min_iter, g, h, None, C.byref(perf))
+    rc = lib().orc_pcg_p(C.byref(om.s), _p(np.ascontiguousarray(sys["diag"], np.float64)),
+                         _p(np.ascontiguousarray(sys["upper"], np.float64)), _p(bc),
+                         _p(np.ascontiguousarray(sys["source"], np.float64)), _p(psi),
+                         tol, rel_tol, max_iter, min_iter, PRECONDITIONERS[precond], g, h, None,
+                         C.byref(perf))
     if rc:
         raise MemoryError
     return psi, perf.as_dict()
 
 
 def laplacian_foam(mesh, T0, n_steps, DT=1.0, dt=0.2, tol=1e-10, rel_tol=0.0, max_iter=1000,
-                   min_iter=0, gsum=None, halo=None, b_value=None):
+                   min_iter=0, gsum=None, halo=None, b_value=None, precond="diagonal"):
     """Listing 1 time loop. Returns (T, b_value, [perf dicts])."""
     om = _om(mesh)
     T = np.array(T0, dtype=np.float64, copy=True)
     bv = np.array(om.b_value if b_value is None else b_value, dtype=np.float64, copy=True)
     perfs = (Perf * max(n_steps, 1))()
     g, h = _callbacks(gsum, halo, om.n_cells, om.n_bfaces)
-    rc = lib().orc_laplacian_foam(C.byref(om.s), DT, dt, _p(T), _p(bv), n_steps, tol, rel_tol,
-                                  max_iter, min_iter, g, h, None, perfs)
+    rc = lib().orc_laplacian_foam_p(C.byref(om.s), DT, dt, _p(T), _p(bv), n_steps, tol, rel_tol,
+                                    max_iter, min_iter, PRECONDITIONERS[precond], g, h, None, perfs)
     if rc:
         raise MemoryError
     return T, bv, [perfs[i].as_dict() for i in range(n_steps)]
+
+
+def dic(mesh, diag, upper, r=None):
+    """OpenFOAM DICPreconditioner: the reciprocal DIC
+    diagonal rD and, if r is given, w = M^-1 r.  Returns (rD, w or None)."""
+    om = _om(mesh)
+    rD = np.zeros(om.n_cells)
+    w = None if r is None else np.zeros(om.n_cells)
+    rr = None if r is None else np.ascontiguousarray(r, np.float64)
+    rc = lib().orc_dic(C.byref(om.s), _p(np.ascontiguousarray(diag, np.float64)),
+                       _p(np.ascontiguousarray(upper, np.float64)), _p(rr), _p(rD), _p(w))
+    if rc:
+        raise MemoryError
+    return rD, w
 
 
 def self_halo(mesh):

@@ -21,6 +21,8 @@
  *   - lduMatrix::Amul with processor interfaces (y -= bc*x_remote).
  *   - OpenFOAM PCG + diagonal preconditioner (§5.1, §6): L1
  *     residual / normFactor, strict '<' (reading A9), singularity 1e-300.
+ *   - OpenFOAM DIC preconditioner, face-loop form over
+ *     the upper-triangular face order (reading A39).
  *   - CSR cell->face grouping (§5.2): the plain definition — a
  *     stable counting sort (items grouped by key, ties in input order,
  *     starts = exclusive scan of counts with the total appended, A13/A14).
@@ -203,14 +205,98 @@ static int converged(double res, double init, double tol, double rel_tol)
     return res < tol || (rel_tol > 0.0 && res < rel_tol * init);
 }
 
-/* ------------------------------------------------------------------ PCG */
-/* OpenFOAM PCG::scalarSolve with diagonalPreconditioner, SURVEY §8(c.1)
- * "PCG" block, step by step in its order. */
-int orc_pcg(const orc_mesh *m, const double *diag, const double *upper,
-            const double *b_bnd, const double *source, double *psi,
-            double tol, double rel_tol, int32_t max_iter, int32_t min_iter,
-            orc_gsum_fn gsum_fn, orc_halo_fn halo_fn, void *ctx, orc_perf *perf)
+/* ------------------------------------------------------------------ DIC */
+/* DIC preconditioner ("DIC/DILU (the usual laplacianFoam
+ * fvSolution choice [OF])"; OpenFOAM DICPreconditioner), in OpenFOAM's own
+ * face-loop form.  lduAddressing keeps faces in upper-triangular order
+ * (lower address l < upper address u, sorted by l then u); the loops below
+ * run over that order (reading A39: the oracle sorts a copy of the faces,
+ * so any input face order/orientation gives the OpenFOAM result).
+ *   calcReciprocalD:  rD = diag; for f: rD[u] -= upper_f*upper_f/rD[l];
+ *                     rD = 1/rD
+ *   precondition:     wA = rD*rA;
+ *                     for f ascending:  wA[u] -= rD[u]*upper_f*wA[l];
+ *                     for f descending: wA[l] -= rD[l]*upper_f*wA[u]
+ * i.e. wA = M^-1 rA with M = (D*+L) D*^-1 (D*+U), D* = 1/rD (incomplete
+ * Cholesky with no fill: diag(M) = diag(A), M = A on A's pattern).
+ * Processor interfaces do not enter (OpenFOAM's DIC is processor-local). */
+typedef struct {
+    int32_t l, u, f;
+} orc_face3;
+
+static int face3_cmp(const void *a, const void *b)
 {
+    const orc_face3 *x = (const orc_face3 *)a, *y = (const orc_face3 *)b;
+    if (x->l != y->l) return x->l < y->l ? -1 : 1;
+    if (x->u != y->u) return x->u < y->u ? -1 : 1;
+    return x->f < y->f ? -1 : (x->f > y->f);
+}
+
+static orc_face3 *upper_triangular_faces(const orc_mesh *m)
+{
+    int32_t f, F = m->n_faces;
+    orc_face3 *t = (orc_face3 *)malloc(sizeof(orc_face3) * (size_t)(F > 0 ? F : 1));
+    if (!t) return NULL;
+    for (f = 0; f < F; f++) {
+        int32_t a = m->owner[f], b = m->neighbour[f];
+        t[f].l = a < b ? a : b;
+        t[f].u = a < b ? b : a;
+        t[f].f = f;
+    }
+    qsort(t, (size_t)F, sizeof(orc_face3), face3_cmp);
+    return t;
+}
+
+static void dic_rD(const orc_mesh *m, const orc_face3 *t, const double *diag,
+                   const double *upper, double *rD)
+{
+    int32_t c, k;
+    for (c = 0; c < m->n_cells; c++) rD[c] = diag[c];
+    for (k = 0; k < m->n_faces; k++) {
+        double a = upper[t[k].f];
+        rD[t[k].u] -= a * a / rD[t[k].l];
+    }
+    for (c = 0; c < m->n_cells; c++) rD[c] = 1.0 / rD[c];
+}
+
+static void dic_precondition(const orc_mesh *m, const orc_face3 *t, const double *rD,
+                             const double *upper, const double *rA, double *wA)
+{
+    int32_t c, k;
+    for (c = 0; c < m->n_cells; c++) wA[c] = rD[c] * rA[c];
+    for (k = 0; k < m->n_faces; k++)
+        wA[t[k].u] -= rD[t[k].u] * upper[t[k].f] * wA[t[k].l];
+    for (k = m->n_faces - 1; k >= 0; k--)
+        wA[t[k].l] -= rD[t[k].l] * upper[t[k].f] * wA[t[k].u];
+}
+
+/* rD_out[n] (reciprocal DIC diagonal) and, if rA != NULL, wA = M^-1 rA. */
+int orc_dic(const orc_mesh *m, const double *diag, const double *upper,
+            const double *rA, double *rD_out, double *wA)
+{
+    orc_face3 *t = upper_triangular_faces(m);
+    if (!t) return 2;
+    dic_rD(m, t, diag, upper, rD_out);
+    if (rA) dic_precondition(m, t, rD_out, upper, rA, wA);
+    free(t);
+    return 0;
+}
+
+#define ORC_PRECOND_DIAGONAL 0
+#define ORC_PRECOND_DIC 1
+
+/* ------------------------------------------------------------------ PCG */
+/* OpenFOAM PCG::scalarSolve, SURVEY §8(c.1) "PCG" block, step by step in
+ * its order; precond = ORC_PRECOND_DIAGONAL (diagonalPreconditioner, the
+ * paper's choice P:608) or ORC_PRECOND_DIC (DICPreconditioner, above; built
+ * where OpenFOAM constructs the preconditioner, once per solve). */
+int orc_pcg_p(const orc_mesh *m, const double *diag, const double *upper,
+              const double *b_bnd, const double *source, double *psi,
+              double tol, double rel_tol, int32_t max_iter, int32_t min_iter,
+              int32_t precond,
+              orc_gsum_fn gsum_fn, orc_halo_fn halo_fn, void *ctx, orc_perf *perf)
+{
+    orc_face3 *t = NULL;
     int32_t n = m->n_cells, c;
     size_t nn = (size_t)(n > 0 ? n : 1), nb = (size_t)(m->n_bfaces > 0 ? m->n_bfaces : 1);
     double *wA = (double *)calloc(nn, sizeof(double));
@@ -249,11 +335,20 @@ int orc_pcg(const orc_mesh *m, const double *diag, const double *upper,
     perf->final_residual = perf->initial_residual;
 
     if (min_iter > 0 || !converged(perf->final_residual, perf->initial_residual, tol, rel_tol)) {
-        for (c = 0; c < n; c++) rD[c] = 1.0 / diag[c];
+        if (precond == ORC_PRECOND_DIC) {
+            t = upper_triangular_faces(m);
+            if (!t) return 2;
+            dic_rD(m, t, diag, upper, rD);
+        } else {
+            for (c = 0; c < n; c++) rD[c] = 1.0 / diag[c];
+        }
         wArA = 1e20; /* OpenFOAM solverPerformance::great_ */
         do {
             wArAold = wArA;
-            for (c = 0; c < n; c++) wA[c] = rD[c] * rA[c];          /* precondition */
+            if (precond == ORC_PRECOND_DIC)                           /* precondition */
+                dic_precondition(m, t, rD, upper, rA, wA);
+            else
+                for (c = 0; c < n; c++) wA[c] = rD[c] * rA[c];
             s[0] = 0.0;
             for (c = 0; c < n; c++) s[0] += wA[c] * rA[c];
             gsum(gsum_fn, ctx, s, 1);
@@ -288,8 +383,17 @@ int orc_pcg(const orc_mesh *m, const double *diag, const double *upper,
     }
     perf->n_iterations = it;
     perf->converged = converged(perf->final_residual, perf->initial_residual, tol, rel_tol);
-    free(wA); free(rA); free(pA); free(rD); free(tmp); free(xr);
+    free(wA); free(rA); free(pA); free(rD); free(tmp); free(xr); free(t);
     return 0;
+}
+
+int orc_pcg(const orc_mesh *m, const double *diag, const double *upper,
+            const double *b_bnd, const double *source, double *psi,
+            double tol, double rel_tol, int32_t max_iter, int32_t min_iter,
+            orc_gsum_fn gsum_fn, orc_halo_fn halo_fn, void *ctx, orc_perf *perf)
+{
+    return orc_pcg_p(m, diag, upper, b_bnd, source, psi, tol, rel_tol, max_iter, min_iter,
+                     ORC_PRECOND_DIAGONAL, gsum_fn, halo_fn, ctx, perf);
 }
 
 /* correctBoundaryConditions for the patch values (a6): zeroGradient
@@ -307,11 +411,11 @@ void orc_patch_values(const orc_mesh *m, const double *T, double *b_value)
 /* ------------------------------------------------------- laplacianFoam */
 /* Listing 1: for each step: assemble TEqn from T0 = T, solve
  * with psi = T (initial guess = old T), correct boundary values. */
-int orc_laplacian_foam(const orc_mesh *m, double DT, double dt, double *T,
-                       double *b_value, int32_t n_steps, double tol,
-                       double rel_tol, int32_t max_iter, int32_t min_iter,
-                       orc_gsum_fn gsum_fn, orc_halo_fn halo_fn, void *ctx,
-                       orc_perf *perf)
+int orc_laplacian_foam_p(const orc_mesh *m, double DT, double dt, double *T,
+                         double *b_value, int32_t n_steps, double tol,
+                         double rel_tol, int32_t max_iter, int32_t min_iter,
+                         int32_t precond, orc_gsum_fn gsum_fn, orc_halo_fn halo_fn,
+                         void *ctx, orc_perf *perf)
 {
     size_t nn = (size_t)(m->n_cells > 0 ? m->n_cells : 1);
     size_t nf = (size_t)(m->n_faces > 0 ? m->n_faces : 1);
@@ -327,12 +431,22 @@ int orc_laplacian_foam(const orc_mesh *m, double DT, double dt, double *T,
     for (s = 0; s < n_steps && rc == 0; s++) {
         rc = orc_assemble(m, DT, dt, T, b_value, diag, upper, source, b_int, b_bnd);
         if (rc == 0)
-            rc = orc_pcg(m, diag, upper, b_bnd, source, T, tol, rel_tol, max_iter,
-                         min_iter, gsum_fn, halo_fn, ctx, &perf[s]);
+            rc = orc_pcg_p(m, diag, upper, b_bnd, source, T, tol, rel_tol, max_iter,
+                           min_iter, precond, gsum_fn, halo_fn, ctx, &perf[s]);
         orc_patch_values(m, T, b_value);
     }
     free(diag); free(source); free(upper); free(b_int); free(b_bnd);
     return rc;
+}
+
+int orc_laplacian_foam(const orc_mesh *m, double DT, double dt, double *T,
+                       double *b_value, int32_t n_steps, double tol,
+                       double rel_tol, int32_t max_iter, int32_t min_iter,
+                       orc_gsum_fn gsum_fn, orc_halo_fn halo_fn, void *ctx,
+                       orc_perf *perf)
+{
+    return orc_laplacian_foam_p(m, DT, dt, T, b_value, n_steps, tol, rel_tol, max_iter,
+                                min_iter, ORC_PRECOND_DIAGONAL, gsum_fn, halo_fn, ctx, perf);
 }
 
 /* ================================================================ *
