@@ -45,7 +45,11 @@ def parse():
     ap.add_argument("--cpu-steps", type=int, default=0, help="oracle steps for cpu_baseline (0 = auto)")
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
                     help="N>1 data path: peer memory (CUDA IPC over NVLink, fused into the kernels) or NCCL")
-    ap.add_argument("--renumber", type=int, default=0, help="1: RCM renumbering inside mesh_create")
+    ap.add_argument("--renumber", type=int, default=-1,
+                    help="0 none, 1 RCM, 2 multicolour (default: 2 with --precond DIC, else 0)")
+    ap.add_argument("--precond", default="diagonal", choices=["diagonal", "DIC"],
+                    help="PCG preconditioner: the paper's diagonal (P:608), or SURVEY §8(f) row 3's DIC "
+                         "(level-scheduled sweeps; 2 levels under the multicolour numbering)")
     ap.add_argument("--mode", default="persistent", choices=["persistent", "graphs", "direct"],
                     help="PCG loop execution (single rank): one cooperative launch per solve, "
                          "CUDA-graph replays of per-phase launches, or direct launches")
@@ -66,11 +70,11 @@ def dist_env():
     return ws, rank, local
 
 
-def workload_name(cfg, corrected=-1, dt_field=False):
+def workload_name(cfg, corrected=-1, dt_field=False, precond="diagonal"):
     c = meshgen.CONFIGS[cfg]
     base = f"cube{c['N']}^3{'-permuted' if c['permuted'] else ''}"
     name = base if corrected < 0 else f"skewed-{base}-corrected-{corrected}corr"
-    return name + ("-layeredDT" if dt_field else "")
+    return name + ("-layeredDT" if dt_field else "") + ("" if precond == "diagonal" else f"-{precond}")
 
 
 def workload_mesh(cfg, corrected=-1, dt_field=False):
@@ -88,8 +92,11 @@ def workload_mesh(cfg, corrected=-1, dt_field=False):
     return m
 
 
-def step_kw(corrected):
-    return {} if corrected < 0 else {"corrected": True, "n_non_orth_correctors": corrected}
+def step_kw(corrected, precond="diagonal"):
+    kw = {} if corrected < 0 else {"corrected": True, "n_non_orth_correctors": corrected}
+    if precond != "diagonal":
+        kw["precond"] = precond
+    return kw
 
 
 # ------------------------------------------------------------------ clocks
@@ -161,23 +168,24 @@ def _oracle_steps(om, T0, steps, corrected, **kw):
     import oracle
     if corrected < 0:
         return oracle.laplacian_foam(om, T0, steps, DT=DT, dt=DELTA_T, tol=TOL, **kw)
+    kw.pop("precond", None)
     return oracle.laplacian_foam_corrected(om, T0, steps, n_corr=corrected, DT=DT, dt=DELTA_T, tol=TOL, **kw)
 
 
-def oracle_rate(mesh, T0, steps, corrected=-1):
+def oracle_rate(mesh, T0, steps, corrected=-1, precond="diagonal"):
     import oracle
     om = oracle.OMesh(mesh)
     t0 = time.perf_counter()
-    _, _, perfs = _oracle_steps(om, T0, steps, corrected)
+    _, _, perfs = _oracle_steps(om, T0, steps, corrected, precond=precond)
     dt = time.perf_counter() - t0
     return mesh.n_cells * steps / dt, dt, perfs
 
 
-def oracle_rate_capped(mesh, T0, max_iter, corrected=-1):
+def oracle_rate_capped(mesh, T0, max_iter, corrected=-1, precond="diagonal"):
     import oracle
     om = oracle.OMesh(mesh)
     t0 = time.perf_counter()
-    _, _, perfs = _oracle_steps(om, T0, 1, corrected, max_iter=max_iter)
+    _, _, perfs = _oracle_steps(om, T0, 1, corrected, max_iter=max_iter, precond=precond)
     dt = time.perf_counter() - t0
     return mesh.n_cells / dt, dt, perfs
 
@@ -187,24 +195,33 @@ def run_reference(args):
     if rank != 0:
         return
     cfg = args.config
-    mesh = workload_mesh(cfg, args.corrected, args.dt_field)
+    mesh = oracle_numbering(workload_mesh(cfg, args.corrected, args.dt_field), args.renumber)
     T0 = meshgen.canonical_field(mesh)
     K = min(args.steps, 20)
     W = min(args.warmup, 1)
     if W:
-        oracle_rate(mesh, T0, W, args.corrected)
-    rate, secs, perfs = oracle_rate(mesh, T0, K, args.corrected)
+        oracle_rate(mesh, T0, W, args.corrected, args.precond)
+    rate, secs, perfs = oracle_rate(mesh, T0, K, args.corrected, args.precond)
     its = [p["n_iterations"] for p in perfs]
-    sample = (f"first {K} laplacianFoam steps of {workload_name(cfg, args.corrected, args.dt_field)} (of --steps {args.steps}); "
+    wname = workload_name(cfg, args.corrected, args.dt_field, args.precond)
+    sample = (f"first {K} laplacianFoam steps of {wname} (of --steps {args.steps}); "
               f"single-threaded C oracle, PCG iterations/step {min(its)}-{max(its)}")
     line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus,
             "steps": K, "warmup": W, "ms_per_step": secs / K * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_name(cfg, args.corrected, args.dt_field), "n_cells": mesh.n_cells, "global_batch": 1,
-                       "seq_len": 0, "parallelism": "cpu-1core"},
+            "config": {"workload": wname, "n_cells": mesh.n_cells, "global_batch": 1,
+                       "seq_len": 0, "parallelism": "cpu-1core", "precond": args.precond,
+                       "renumber": args.renumber},
             "cpu_baseline": {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
             "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def oracle_numbering(mesh, renumber):
+    """The numbering the library solves in, for the oracle arm: the DIC
+    recurrences depend on it (renumber = 2: meshgen's multicolour numbering,
+    the same first-fit rule as mesh_create's); the diagonal method does not."""
+    return meshgen.colour_mesh(mesh) if renumber == 2 else mesh
 
 
 # ----------------------------------------------------------------- GPU arm
@@ -230,10 +247,13 @@ def run_ours(args):
     ctx.set_option("graphs", args.mode != "direct")
 
     cfg = args.config
+    wname = workload_name(cfg, args.corrected, args.dt_field, args.precond)
     if args.corrected >= 0 and ws > 1:
         raise SystemExit("--corrected: single rank only (the corrected path has no processor patches)")
     gmesh = workload_mesh(cfg, args.corrected, args.dt_field)
-    kw = step_kw(args.corrected)
+    kw = step_kw(args.corrected, args.precond)
+    if args.precond != "diagonal" and ws > 1:
+        raise SystemExit("--precond DIC: single rank only (the DIC is processor-local; no halo variant yet)")
     n_global = gmesh.n_cells
     T0g = meshgen.canonical_field(gmesh)
     if ws > 1:
@@ -250,7 +270,7 @@ def run_ours(args):
     else:
         m, T0 = gmesh, T0g
     del gmesh
-    mesh = P.Mesh(ctx, m, renumber=bool(args.renumber))
+    mesh = P.Mesh(ctx, m, renumber=args.renumber)
     if ws > 1 and args.transport == "p2p":
         hs = [None] * ws
         dist.all_gather_object(hs, mesh.p2p_export())
@@ -301,6 +321,7 @@ def run_ours(args):
     n_p2, ms_p2 = ctx.kernel_stats("phase2")
     n_as, ms_as = ctx.kernel_stats("assemble")
     n_pcg, ms_pcg = ctx.kernel_stats("pcg")
+    n_dic, ms_dic = ctx.kernel_stats("pcg_dic")
     n_no, ms_no = ctx.kernel_stats("nonorth")
     B_local = sum(p.n_faces for p in m.patches)
     # grad gather (40n + 40F + 37B) + correction gather (40n + 48F), per pass
@@ -309,7 +330,17 @@ def run_ours(args):
     bytes_p1 = 56 * n_local + 16 * F_local          # per full phase-1 launch
     bytes_p2 = 40 * n_local
     peak, peak_kind = measured_peak()
-    if n_pcg > 0:
+    if n_dic > 0:
+        # persistent DIC solve: per iteration the Amul phase
+        # (56n + 16F) + r update and both sweeps (r, q, rD read, r and w
+        # written: 40n; coefficient + label per face per sweep: 24F); per
+        # launch the factor (diag read, rD written, 16n + 12F), the set-up
+        # sweeps (24n + 24F) and the final psi flush (24n)
+        kernel = "k_pcg_dic"
+        total_bytes = (iters * (96 * n_local + 40 * F_local)
+                       + n_dic * (64 * n_local + 36 * F_local))
+        k_launches, k_ms = n_dic, ms_dic
+    elif n_pcg > 0:
         # persistent whole-solve kernel: per launch = its iterations x (96n + 16F)
         # + the final flush pass (psi, p_old read, psi written: 24n)
         kernel = "k_pcg_persistent"
@@ -320,7 +351,8 @@ def run_ours(args):
         total_bytes = bytes_p1 * iters
         k_launches, k_ms = n_p1, ms_p1
     achieved = total_bytes / (k_ms / 1e3) / 1e9 if k_ms > 0 else None
-    tkey = f"{cfg}{'' if args.corrected < 0 else f'-corr{args.corrected}'}{'-dt' if args.dt_field else ''}"
+    tkey = (f"{cfg}{'' if args.corrected < 0 else f'-corr{args.corrected}'}{'-dt' if args.dt_field else ''}"
+            f"{'' if args.precond == 'diagonal' else '-' + args.precond.lower()}")
     traffic = ncu_traffic(tkey, kernel) if ws == 1 else None
 
     # e2e through the public API with host buffers (pinned), copies inside the region
@@ -349,22 +381,22 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        full = workload_mesh(cfg, args.corrected, args.dt_field)
+        full = oracle_numbering(workload_mesh(cfg, args.corrected, args.dt_field), args.renumber)
         its_gpu = sum(p["n_iterations"] for p in perfs) / len(perfs)
         if n_global <= 2_000_000:
             steps = args.cpu_steps or 2
-            rate, secs, po = oracle_rate(full, meshgen.canonical_field(full), steps, args.corrected)
-            sample = (f"first {steps} laplacianFoam steps of {workload_name(cfg, args.corrected, args.dt_field)} "
+            rate, secs, po = oracle_rate(full, meshgen.canonical_field(full), steps, args.corrected, args.precond)
+            sample = (f"first {steps} laplacianFoam steps of {wname} "
                       f"({secs:.1f} s, PCG iterations {[p['n_iterations'] for p in po]})")
         else:
             # bounded sample: step 0 truncated to `cap` PCG iterations, scaled to
             # the GPU run's mean iterations per step (the oracle does the same
             # work per iteration; assembly is counted once)
             cap = max(2, int(20 * 8e6 / n_global))
-            _, secs, po = oracle_rate_capped(full, meshgen.canonical_field(full), cap, args.corrected)
+            _, secs, po = oracle_rate_capped(full, meshgen.canonical_field(full), cap, args.corrected, args.precond)
             its_cpu = sum(p["n_iterations"] for p in po) / len(po)
             rate = n_global / (secs * its_gpu / its_cpu)
-            sample = (f"step 0 of {workload_name(cfg, args.corrected, args.dt_field)} capped at {po[0]['n_iterations']} PCG iterations "
+            sample = (f"step 0 of {wname} capped at {po[0]['n_iterations']} PCG iterations "
                       f"({secs:.1f} s), scaled to {its_gpu:.1f} iterations/step (projected)")
         cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample}
 
@@ -374,9 +406,9 @@ def run_ours(args):
         "warmup": max(args.warmup, 3), "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "weak" if ws == 1 else "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": workload_name(cfg, args.corrected, args.dt_field), "n_cells": n_global, "steps_per_run": args.steps,
+        "config": {"workload": wname, "n_cells": n_global, "steps_per_run": args.steps,
                    "global_batch": 1, "seq_len": 0, "parallelism": "1gpu" if ws == 1 else f"domain{ws}-{args.transport}",
-                   "renumber": args.renumber, "mode": args.mode,
+                   "renumber": args.renumber, "mode": args.mode, "precond": args.precond,
                    "l2": "flushed between timed steps (256 MiB write)", "tol": TOL,
                    "pcg_iterations_per_step": {"min": min(its), "max": max(its), "mean": sum(its) / len(its)}},
         "roofline": {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": peak,
@@ -413,6 +445,8 @@ def run_ours(args):
 
 def main():
     args = parse()
+    if args.renumber < 0:
+        args.renumber = 2 if args.precond != "diagonal" else 0
     if args.impl == "reference":
         run_reference(args)
     else:

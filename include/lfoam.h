@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define LF_VERSION 1
+#define LF_VERSION 2
 
 #if defined(__GNUC__)
 #define LF_API __attribute__((visibility("default")))
@@ -105,7 +105,12 @@ typedef struct {
   const double *V;             /* host [n_cells] > 0                                        */
   const lf_patch_desc *patches;/* host [n_patches]                                          */
   int32_t renumber;            /* 0 keep numbering; 1 reverse Cuthill-McKee inside the
-                                  library (fields still speak the caller's numbering)      */
+                                  library; 2 multicolour: greedy first-fit colouring in cell
+                                  order (colour = smallest not used by a lower-labelled
+                                  neighbour), cells renumbered colour by colour, ascending
+                                  label within a colour — the numbering under which the DIC
+                                  sweeps run in #colours parallel levels (2 on hex blocks).
+                                  Fields still speak the caller's numbering.              */
   /* Full geometry (all NULL, or all set together with every non-empty patch's
    * sf; c != NULL marks a geometry mesh, sf/cf may be NULL only if n_faces == 0): the
    * non-orthogonal correction path (fvc::grad and the
@@ -235,11 +240,33 @@ LF_API lf_status lf_ldu_export(const lf_ldu *sys, double *diag, double *upper, d
 LF_API lf_status ldu_amul(const lf_ldu *sys, const double *x_dev, double *y_dev);
 
 /* ---------------------------------------------------------------- PCG */
+/* Preconditioners (OpenFOAM fvSolution names).
+ *   LF_PRECOND_DIAGONAL  rD = 1/diag, w = rD r — the paper's choice.
+ *   LF_PRECOND_DIC       OpenFOAM DICPreconditioner:
+ *                        rD = diag; for faces in upper-triangular order
+ *                        rD[u] -= upper^2/rD[l]; rD = 1/rD;  w = rD r;
+ *                        forward  for f ascending:  w[u] -= rD[u] upper_f w[l];
+ *                        backward for f descending: w[l] -= rD[l] upper_f w[u].
+ *                        Exact OpenFOAM semantics on any numbering: the sweeps
+ *                        run level by level (a cell's level = 1 + the largest
+ *                        level of its lower neighbours), so the parallel depth
+ *                        is the number of levels — 2 on a hex block numbered
+ *                        with renumber = 2, 3N-2 on the natural N^3 numbering.
+ *                        Single rank, no processor patches (else INVALID_ARG);
+ *                        runs in the persistent solver whatever LF_OPT_PERSISTENT
+ *                        says; cells may have at most 8 neighbours.
+ *   LF_PRECOND_DILU      OpenFOAM DILUPreconditioner; on this symmetric matrix
+ *                        (lower == upper) its recurrences are DIC's term for
+ *                        term, so it runs the DIC kernels. */
+typedef enum { LF_PRECOND_DIAGONAL = 0, LF_PRECOND_DIC = 1, LF_PRECOND_DILU = 2 } lf_preconditioner;
+
 typedef struct {
   double tolerance;   /* absolute on the normalised L1 residual (1e-10)   */
   double rel_tol;     /* 0 = off                                          */
   int32_t max_iter;   /* 1000 (OpenFOAM default)                          */
   int32_t min_iter;   /* 0                                                */
+  int32_t preconditioner;  /* lf_preconditioner; 0 (zero-initialised) = diagonal */
+  int32_t reserved;   /* 0                                                */
 } lf_solver_controls;
 
 typedef struct {
@@ -247,11 +274,22 @@ typedef struct {
   int32_t n_iterations, converged, singular, reserved;
 } lf_solver_perf;
 
-/* OpenFOAM PCG with diagonal preconditioner:
+/* w = M^-1 r for the preconditioner of the assembled system (the call PCG
+ * makes once per iteration): r_dev, w_dev device [n_cells] in internal
+ * numbering, must not alias; rD_dev: device [n_cells] receives the
+ * reciprocal (DIC) diagonal, or NULL.  Stream-ordered.  Errors as pcg_solve. */
+LF_API lf_status ldu_precondition(const lf_ldu *sys, int32_t preconditioner, const double *r_dev,
+                                  double *w_dev, double *rD_dev);
+
+/* OpenFOAM PCG, preconditioner from c:
  * psi_dev (device [n_cells], internal numbering) is the initial guess and
- * receives the solution.  Two fused kernels per iteration; alpha, beta and
- * the stopping rule are evaluated on the device.  Returns once *out is on
- * the host.  Non-convergence and singularity are LF_OK with flags set. */
+ * receives the solution.  Two fused kernels per iteration (diagonal) or one
+ * persistent launch per solve; alpha, beta and the stopping rule are
+ * evaluated on the device.  With DIC the preconditioner is rebuilt from the
+ * current coefficients at every solve (as OpenFOAM constructs it per solve).
+ * Returns once *out is on the host.  Non-convergence and singularity are
+ * LF_OK with flags set; an unknown preconditioner or DIC on a mesh with
+ * processor patches / more than 8 neighbours per cell is INVALID_ARG. */
 LF_API lf_status pcg_solve(lf_ldu *sys, double *psi_dev, const lf_solver_controls *c, lf_solver_perf *out);
 
 /* n_steps laplacianFoam time steps on the mesh's T field: each step
@@ -270,7 +308,9 @@ typedef enum {
   LF_K_AMUL = 4, LF_K_SUMPSI = 5, LF_K_PACK = 6,
   LF_K_PCG = 7,      /* persistent whole-solve kernel (single rank, no processor patches) */
   LF_K_NONORTH = 8,  /* gradient / non-orthogonal correction kernels (lf_fvc_grad, corrected) */
-  LF_K_COUNT = 9
+  LF_K_PCG_DIC = 9,  /* persistent whole-solve kernel with the DIC preconditioner */
+  LF_K_PRECOND = 10, /* standalone preconditioner kernels (ldu_precondition, DIC set-up) */
+  LF_K_COUNT = 11
 } lf_kernel_kind;
 
 /* Execution options of a context (all default 1):

@@ -430,6 +430,17 @@ lf_status lf_fvc_grad(lf_mesh *M, const double *x, double *grad, double *bgrad) 
 }
 
 // ------------------------------------------------------------------- PCG
+lf_status ldu_precondition(const lf_ldu *sys, int32_t precond, const double *r, double *w, double *rD) {
+  lf_mesh *M = sys ? sys->mesh : nullptr;
+  return guard([&] {
+    LF_REQUIRE(sys && M && r && w, "NULL argument");
+    LF_REQUIRE(r != w && r != rD && w != rD, "r, w and rD must not alias");
+    LF_REQUIRE(sys->assembled, "ldu not assembled");
+    LF_REQUIRE(precond >= LF_PRECOND_DIAGONAL && precond <= LF_PRECOND_DILU, "unknown preconditioner");
+    precondition(M, precond, r, w, rD);
+  }, M);
+}
+
 lf_status pcg_solve(lf_ldu *sys, double *psi, const lf_solver_controls *c, lf_solver_perf *out) {
   lf_mesh *M = sys ? sys->mesh : nullptr;
   return guard([&] {

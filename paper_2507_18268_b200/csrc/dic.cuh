@@ -1,0 +1,411 @@
+// DIC preconditioner kernels — included by kernels.cu
+// (same translation unit: shares the grid barrier / reduction helpers).
+//
+// OpenFOAM's DICPreconditioner is three sequential face loops over the
+// upper-triangular face order (include/lfoam.h, LF_PRECOND_DIC):
+//   calcReciprocalD  rD[u] -= upper_f^2 / rD[l]           (f ascending)
+//   forward          w[u]  -= rD[u] upper_f w[l]           (f ascending)
+//   backward         w[l]  -= rD[l] upper_f w[u]           (f descending)
+// A cell's value is final once all its lower (forward) / upper (backward)
+// neighbours are, so the loops parallelise over LEVELS: level(c) = 0 without
+// lower neighbours, else 1 + max level of them.  Cells of one level are
+// independent; levels are separated by grid barriers inside one persistent
+// launch.  Each cell gathers its neighbours' contributions in exactly the
+// sequential order (lower neighbours ascending = ascending face id; upper
+// neighbours descending), with explicit _rn operations (no FMA), so rD and
+// the preconditioned vector are bitwise those of the face loops.
+//
+// Level 0 needs no forward pass: its forward value is rD_c r_c, which the
+// forward passes of higher levels recompute at the neighbour (bit L0 of the
+// row label) from the not-yet-updated r and q — so a solve with L levels
+// costs 2L-2 grid barriers per preconditioner application plus one for the
+// Amul phase: 3 per iteration on a 2-colour numbering (renumber = 2).
+//
+// Row layout: full-row ELL (DicDev / LduDev.symU), every access coalesced;
+// coefficients written by the assembly kernel.
+
+// Plain grid barrier of the persistent kernels (no reduction): same
+// protocol as grid_reduce_sync (acq_rel arrival, release by the last block,
+// ld.acquire spin that also invalidates the SM's L1).
+__device__ __forceinline__ void grid_barrier(unsigned *bar) {
+  __shared__ int amLastB;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned gen = ld_acquire(bar + 1);
+    unsigned t;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(t) : "l"(bar) : "memory");
+    amLastB = (t == gridDim.x - 1);
+    if (amLastB) {
+      bar[0] = 0u;
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar + 1) : "memory");
+    } else {
+      const unsigned long long t0 = gtime_ns();
+      unsigned tries = 0;
+      while (ld_acquire(bar + 1) == gen) {
+        __nanosleep(32);
+        spin_check(t0, tries);
+      }
+    }
+  }
+  __syncthreads();
+}
+
+template <int KS>
+struct SymRow {
+  int lab[KS];
+  double u[KS];
+};
+
+template <int KS>
+__device__ __forceinline__ void load_row(const DicDev &d, const LduDev &a, int c, SymRow<KS> &R) {
+#pragma unroll
+  for (int k = 0; k < KS; ++k) {
+    R.lab[k] = __ldg(d.symN + k * d.ldS + c);
+    R.u[k] = __ldg(a.symU + k * d.ldS + c);
+  }
+}
+
+__device__ __forceinline__ int sym_cell(int lab) { return lab & (DIC_L0BIT - 1); }
+
+// calcReciprocalD for a cell on level >= 1 (its lower neighbours are final)
+template <int KS>
+__device__ __forceinline__ void dic_factor_cell(const DicDev &d, const LduDev &a, int c) {
+  SymRow<KS> R;
+  load_row<KS>(d, a, c, R);
+  double rdu = a.diag[c];
+#pragma unroll
+  for (int k = 0; k < KS; ++k) {
+    const int lab = R.lab[k];
+    if (lab >= 0 && sym_cell(lab) < c) {
+      const int j = sym_cell(lab);
+      const double dj = (lab & DIC_L0BIT) ? a.diag[j] : d.rDu[j];
+      rdu = __dsub_rn(rdu, __ddiv_rn(__dmul_rn(R.u[k], R.u[k]), dj));
+    }
+  }
+  d.rDu[c] = rdu;
+  d.rD[c] = __ddiv_rn(1.0, rdu);
+}
+
+// r of a cell after this iteration's update (upd) — identical operation
+// wherever it is evaluated
+__device__ __forceinline__ double r_new(const double *r, const double *q, bool upd, double alpha, int j) {
+  return upd ? fma(-alpha, q[j], r[j]) : r[j];
+}
+
+// Forward pass of a cell on level >= 1.  Writes r (upd) and the forward w;
+// returns r_c.
+template <int KS>
+__device__ __forceinline__ double dic_forward_cell(const DicDev &d, const LduDev &a, int c, double *r,
+                                                   const double *q, double *w, bool upd, double alpha,
+                                                   double &wOut) {
+  SymRow<KS> R;
+  load_row<KS>(d, a, c, R);
+  const double rc = r_new(r, q, upd, alpha, c);
+  if (upd) r[c] = rc;
+  const double rd = d.rD[c];
+  double wv = __dmul_rn(rd, rc);
+#pragma unroll
+  for (int k = 0; k < KS; ++k) {
+    const int lab = R.lab[k];
+    if (lab >= 0 && sym_cell(lab) < c) {
+      const int j = sym_cell(lab);
+      const double wj = (lab & DIC_L0BIT) ? __dmul_rn(d.rD[j], r_new(r, q, upd, alpha, j)) : w[j];
+      wv = __dsub_rn(wv, __dmul_rn(__dmul_rn(rd, R.u[k]), wj));
+    }
+  }
+  w[c] = wv;
+  wOut = wv;
+  return rc;
+}
+
+// Backward pass of a cell on level l (l == 0: r update and forward value
+// here).  Writes the final w; returns r_c.
+template <int KS>
+__device__ __forceinline__ double dic_backward_cell(const DicDev &d, const LduDev &a, int c, bool level0,
+                                                    double *r, const double *q, double *w, bool upd,
+                                                    double alpha, double &wOut) {
+  SymRow<KS> R;
+  load_row<KS>(d, a, c, R);
+  const double rd = d.rD[c];
+  double rc, wv;
+  if (level0) {
+    rc = r_new(r, q, upd, alpha, c);
+    if (upd) r[c] = rc;
+    wv = __dmul_rn(rd, rc);
+  } else {
+    rc = r[c];
+    wv = w[c];
+  }
+#pragma unroll
+  for (int k = KS - 1; k >= 0; --k) {
+    const int lab = R.lab[k];
+    if (lab >= 0 && sym_cell(lab) > c)
+      wv = __dsub_rn(wv, __dmul_rn(__dmul_rn(rd, R.u[k]), w[sym_cell(lab)]));
+  }
+  w[c] = wv;
+  wOut = wv;
+  return rc;
+}
+
+__device__ __forceinline__ int level_cell(const DicDev &d, int t) { return d.contig ? t : __ldg(d.lvlCells + t); }
+
+// One application of the preconditioner inside the persistent kernel (upd:
+// fused r -= alpha q), ending in the reducing barrier that publishes
+// {sum|r|, sum w.r} to out[0..1].
+template <int KS>
+__device__ __forceinline__ void dic_apply(const DicDev &d, const LduDev &a, double *r, const double *q,
+                                          double *w, bool upd, double alpha, unsigned *bar,
+                                          double *partials, double *out, const P2PDev &nop) {
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+  const int L = d.L;
+  double v[2] = {0.0, 0.0};
+  for (int l = 1; l < L; ++l) {
+    const int t1 = __ldg(d.lvlStart + l + 1);
+    for (int t = __ldg(d.lvlStart + l) + gtid; t < t1; t += stride) {
+      const int c = level_cell(d, t);
+      double wc;
+      const double rc = dic_forward_cell<KS>(d, a, c, r, q, w, upd, alpha, wc);
+      v[0] += fabs(rc);
+      if (l == L - 1) v[1] = fma(wc, rc, v[1]);  // no upper neighbours: final
+    }
+    grid_barrier(bar);
+  }
+  for (int l = L >= 2 ? L - 2 : 0; l >= 0; --l) {
+    const int t1 = __ldg(d.lvlStart + l + 1);
+    for (int t = __ldg(d.lvlStart + l) + gtid; t < t1; t += stride) {
+      const int c = level_cell(d, t);
+      double wc;
+      const double rc = dic_backward_cell<KS>(d, a, c, l == 0, r, q, w, upd, alpha, wc);
+      if (l == 0) v[0] += fabs(rc);
+      v[1] = fma(wc, rc, v[1]);
+    }
+    if (l > 0) grid_barrier(bar);
+  }
+  grid_reduce_sync<2>(v, partials, bar, out, nop LF_DBG_ARG(0));
+}
+
+// ------------------------------------------------ persistent DIC PCG solve
+// The diagonal persistent kernel's state machine (k_pcg_persistent) with
+// the preconditioner application replaced by the level sweeps:
+//   set-up:    DIC factor (L-1 passes), w = M^-1 r (2L-2 barriers), sum w.r
+//   iteration: phase 1 (p, q = A p over full rows, sum p.q, deferred psi)
+//              | r -= alpha q fused into the sweeps, w = M^-1 r, sum|r|, sum w.r
+// Single rank, no processor patches (the DIC is processor-local in OpenFOAM;
+// the halo variant is future work).
+template <int KS>
+__global__ void __launch_bounds__(BS, LF_MINB_P)
+    k_pcg_dic(MeshDev m, LduDev a, DicDev d, Workspace ws, unsigned *bar) {
+  PcgCtl *ctl = ws.ctl;
+  if (ctl->stop) return;
+  const P2PDev &nop = ws.p2p;  // P == 0: single rank (set by launch_pcg_dic)
+  struct St {
+    double nf, initRes, finRes, wArA, alpha, beta;
+    int k, cont, singular;
+  };
+  __shared__ St st;
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+  const int L = d.L;
+  double *psi = ctl->psi;
+  double *r = ws.r, *w = ws.w, *q = ws.q;
+
+  if (threadIdx.x == 0) {
+    st.k = ctl->it;
+    st.nf = ctl->normFactor;
+    st.initRes = ctl->initRes;
+    st.finRes = ctl->finRes;
+    st.wArA = ctl->wArA;
+    st.alpha = ctl->alpha;
+    st.singular = 0;
+    // OpenFOAM: iterate if minIter > 0 || !checkConvergence (set-up sums)
+    st.nf = __ldcg(&ws.gsum->setup[0]) + 1e-20;
+    st.initRes = __ldcg(&ws.gsum->setup[1]) / st.nf;
+    st.finRes = st.initRes;
+    st.cont = ctl->minIter > 0 || !conv(st.finRes, st.initRes, ctl);
+  }
+  __syncthreads();
+  if (st.cont) {
+    // ---- calcReciprocalD: levels 0 and 1 in one pass (level 1 reads only
+    // diag of level-0 cells), then one pass per level
+    for (int l = 0; l < L; ++l) {
+      if (l >= 2) grid_barrier(bar);
+      const int t1 = __ldg(d.lvlStart + l + 1);
+      for (int t = __ldg(d.lvlStart + l) + gtid; t < t1; t += stride) {
+        const int c = level_cell(d, t);
+        if (l == 0)
+          d.rD[c] = __ddiv_rn(1.0, a.diag[c]);
+        else
+          dic_factor_cell<KS>(d, a, c);
+      }
+    }
+    grid_barrier(bar);
+    dic_apply<KS>(d, a, r, q, w, false, 0.0, bar, ws.partials, ws.gsum->p2, nop);  // w = M^-1 r (set-up)
+  }
+  for (;;) {
+    if (threadIdx.x == 0) {
+      if (st.k == 0) {
+        st.wArA = st.cont ? __ldcg(&ws.gsum->p2[1]) : 0.0;
+        st.beta = 0.0;
+      } else {
+        st.finRes = __ldcg(&ws.gsum->p2[0]) / st.nf;
+        st.cont = (st.k < ctl->maxIter && !conv(st.finRes, st.initRes, ctl)) || st.k < ctl->minIter;
+        const double wn = __ldcg(&ws.gsum->p2[1]);
+        st.beta = wn / st.wArA;
+        st.wArA = wn;
+      }
+    }
+    __syncthreads();
+    const int k = st.k;
+    const bool first = (k == 0), cont = st.cont != 0;
+    const double beta = st.beta, alpha = st.alpha;
+    const double *pold = (k & 1) ? ws.p[0] : ws.p[1];
+    double *pnew = (k & 1) ? ws.p[1] : ws.p[0];
+    // ---- phase 1: flush psi, p = w + beta p_old, q = A p (full rows), sums
+    double v1[2] = {0.0, 0.0};
+    for (int c = gtid; c < m.n; c += stride) {
+      double ps = psi[c];
+      if (!first) {
+        ps = fma(alpha, pold[c], ps);
+        psi[c] = ps;
+      }
+      v1[1] += ps;
+      if (cont) {
+        SymRow<KS> R;
+        load_row<KS>(d, a, c, R);
+        const double pc = first ? w[c] : fma(beta, pold[c], w[c]);
+        pnew[c] = pc;
+        double pn[KS];
+#pragma unroll
+        for (int kk = 0; kk < KS; ++kk) {
+          const int j = sym_cell(R.lab[kk]);
+          pn[kk] = R.lab[kk] >= 0 ? (first ? w[j] : fma(beta, pold[j], w[j])) : 0.0;
+        }
+        double qc = a.diag[c] * pc;
+#pragma unroll
+        for (int kk = 0; kk < KS; ++kk)
+          if (R.lab[kk] >= 0) qc = fma(R.u[kk], pn[kk], qc);
+        q[c] = qc;
+        v1[0] = fma(pc, qc, v1[0]);
+      }
+    }
+    grid_reduce_sync<2>(v1, ws.partials, bar, ws.gsum->p1, nop LF_DBG_ARG(0));
+    if (!cont) break;
+    if (threadIdx.x == 0) {
+      const double pq = __ldcg(&ws.gsum->p1[0]);
+      st.singular = fabs(pq) / st.nf < 1e-300;
+      if (!st.singular) st.alpha = st.wArA / pq;
+    }
+    __syncthreads();
+    if (st.singular) break;
+    // ---- r -= alpha q, w = M^-1 r, sum|r|, sum w.r
+    dic_apply<KS>(d, a, r, q, w, true, st.alpha, bar, ws.partials, ws.gsum->p2, nop);
+    if (threadIdx.x == 0) ++st.k;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    ctl->it = st.k;
+    ctl->stop = 1;
+    ctl->singular = st.singular;
+    ctl->converged = conv(st.finRes, st.initRes, ctl) ? 1 : 0;
+    ctl->normFactor = st.nf;
+    ctl->initRes = st.initRes;
+    ctl->finRes = st.finRes;
+    ctl->wArA = st.wArA;
+    ctl->alpha = st.alpha;
+  }
+}
+
+int dic_grid(int device, int KS) {
+  int sms = 0, nb = 0;
+  LF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  const void *fn = KS <= 6 ? (const void *)k_pcg_dic<6> : (const void *)k_pcg_dic<8>;
+  LF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, BS, 0));
+  return sms * (nb < 1 ? 1 : nb);
+}
+
+void launch_pcg_dic(cudaStream_t s, int grid, const MeshDev &m, const LduDev &a, const DicDev &d,
+                    const Workspace &ws, unsigned *bar) {
+  Workspace w1 = ws;
+  w1.p2p.P = 0;  // single rank: the reductions exchange nothing
+  void *args[] = {(void *)&m, (void *)&a, (void *)&d, (void *)&w1, (void *)&bar};
+  const void *fn = d.KS <= 6 ? (const void *)k_pcg_dic<6> : (const void *)k_pcg_dic<8>;
+  LF_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(BS), args, 0, s));
+}
+
+// ------------------------------------------- full-row coefficients (fill)
+// symU from upper for a system assembled before the DIC rows existed (the
+// assembly kernel writes them directly afterwards).  Slot order: the
+// neighbour-side faces (losort order), then the owned faces.
+__global__ void k_sym_fill(MeshDev m, LduDev a) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < m.n; c += gridDim.x * blockDim.x) {
+    const int l0 = m.losortStart[c], l1 = m.losortStart[c + 1];
+    const int o0 = m.ownerStart[c], o1 = m.ownerStart[c + 1];
+    for (int j = l0; j < l1; ++j) a.symU[(j - l0) * a.ldS + c] = a.upper[m.losort[j]];
+    for (int i = o0; i < o1; ++i) a.symU[((l1 - l0) + (i - o0)) * a.ldS + c] = a.upper[i];
+  }
+}
+
+void launch_sym_fill(cudaStream_t s, const Launch &L, const MeshDev &m, const LduDev &a) {
+  k_sym_fill<<<L.grid, BS, 0, s>>>(m, a);
+}
+
+// ------------------------------------------------ standalone level passes
+template <int KS>
+__global__ void k_dic_factor_level(LduDev a, DicDev d, int l) {
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+  const int lo = l, hi = l == 0 ? min(1, d.L - 1) : l;
+  for (int ll = lo; ll <= hi; ++ll) {
+    const int t1 = d.lvlStart[ll + 1];
+    for (int t = d.lvlStart[ll] + gtid; t < t1; t += stride) {
+      const int c = level_cell(d, t);
+      if (ll == 0)
+        d.rD[c] = __ddiv_rn(1.0, a.diag[c]);
+      else
+        dic_factor_cell<KS>(d, a, c);
+    }
+  }
+}
+
+template <int KS>
+__global__ void k_dic_sweep_level(LduDev a, DicDev d, int l, int forward, const double *r, double *w) {
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+  const int t1 = d.lvlStart[l + 1];
+  for (int t = d.lvlStart[l] + gtid; t < t1; t += stride) {
+    const int c = level_cell(d, t);
+    double wc;
+    // r is read only (no update): the const_cast is never written through
+    if (forward)
+      dic_forward_cell<KS>(d, a, c, const_cast<double *>(r), nullptr, w, false, 0.0, wc);
+    else
+      dic_backward_cell<KS>(d, a, c, l == 0, const_cast<double *>(r), nullptr, w, false, 0.0, wc);
+  }
+}
+
+void launch_dic_factor_level(cudaStream_t s, const Launch &L, const MeshDev &m, const LduDev &a,
+                             const DicDev &d, int l) {
+  (void)m;
+  if (d.KS <= 6)
+    k_dic_factor_level<6><<<L.grid, BS, 0, s>>>(a, d, l);
+  else
+    k_dic_factor_level<8><<<L.grid, BS, 0, s>>>(a, d, l);
+}
+
+void launch_dic_sweep_level(cudaStream_t s, const Launch &L, const MeshDev &m, const LduDev &a,
+                            const DicDev &d, int l, bool forward, const double *r, double *w) {
+  (void)m;
+  if (d.KS <= 6)
+    k_dic_sweep_level<6><<<L.grid, BS, 0, s>>>(a, d, l, forward ? 1 : 0, r, w);
+  else
+    k_dic_sweep_level<8><<<L.grid, BS, 0, s>>>(a, d, l, forward ? 1 : 0, r, w);
+}
+
+// diagonalPreconditioner: w = (1/diag) r (rD = 1/diag, then rD*r, as
+// OpenFOAM); r == null: w = rD
+__global__ void k_diag_precondition(int32_t n, const double *__restrict__ diag, const double *__restrict__ r,
+                                    double *__restrict__ w) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x)
+    w[c] = r ? (1.0 / diag[c]) * r[c] : 1.0 / diag[c];
+}
+
+void launch_diag_precondition(cudaStream_t s, const Launch &L, int32_t n, const double *diag,
+                              const double *r, double *w) {
+  k_diag_precondition<<<L.grid, BS, 0, s>>>(n, diag, r, w);
+}

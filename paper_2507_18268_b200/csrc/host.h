@@ -113,6 +113,12 @@ struct lf_mesh {
   double *DTc = nullptr, *gammaF = nullptr, *gammaB = nullptr;
   bool dtSet = false;
   lf::MeshDev mdVar{};       // md with gammaF/gammaB set (variable_DT solves)
+  // DIC preconditioner: levels + full-row ELL, built on
+  // first use (precond.cpp)
+  bool dicBuilt = false;
+  lf::DicDev dic{};
+  int dicGrid = 0;            // co-resident grid of k_pcg_dic
+  std::vector<int32_t> hLvlStart;  // host copy of the level starts
   ~lf_mesh();
 };
 
@@ -134,4 +140,10 @@ void p2p_export(lf_mesh *M, void *handle);
 void p2p_connect(lf_mesh *M, int nranks, int rank, const void *handles);
 void allreduce(lf_mesh *M, const double *local, double *global, size_t count);
 void upload_controls(lf_mesh *M, const lf_solver_controls *c, double *psi);
+// precond.cpp
+void ensure_dic(lf_mesh *M);  // build the DIC levels / rows (once), fill symU if assembled
+void require_dic(const lf_mesh *M);  // INVALID_ARG where the DIC kernels cannot run
+void precondition(lf_mesh *M, int precond, const double *r, double *w, double *rD);
+// mesh.cpp: resident grid with equal grid-stride trips per block
+int balanced_grid(int64_t n, int g0);
 }  // namespace lf

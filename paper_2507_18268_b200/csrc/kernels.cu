@@ -406,6 +406,7 @@ __global__ void __launch_bounds__(BS, LF_MINB)
     for (int j = l0; j < l1; ++j) {
       const int f = m.losort[j];
       const double u = __dmul_rn(m.delta[f], __dmul_rn(m.gammaF ? m.gammaF[f] : DT, m.magSf[f]));
+      if (a.symU) a.symU[(j - l0) * a.ldS + c] = -u;  // full-row copy (DIC)
       L = __dsub_rn(L, u);
       if (SETUP) {
         sOff = fma(-u, T[m.losortOwner[j]], sOff);
@@ -417,6 +418,7 @@ __global__ void __launch_bounds__(BS, LF_MINB)
       const double u = __dmul_rn(m.delta[i], __dmul_rn(m.gammaF ? m.gammaF[i] : DT, m.magSf[i]));
       a.upper[i] = -u;
       if (m.K > 0) a.upperE[(i - o0) * m.ldE + c] = -u;
+      if (a.symU) a.symU[((l1 - l0) + (i - o0)) * a.ldS + c] = -u;
       L = __dsub_rn(L, u);
       if (SETUP) {
         sOff = fma(-u, T[m.nbr[i]], sOff);
@@ -1262,6 +1264,9 @@ void sort_pairs_u64(cudaStream_t s, uint64_t *keys, int32_t *vals, int64_t m, in
 void sort_pairs_i32(cudaStream_t s, int32_t *keys, int32_t *vals, int64_t m, int end_bit) {
   sort_pairs<int32_t>(s, keys, vals, m, end_bit);
 }
+
+// ----------------------------------------------------- DIC preconditioner
+#include "dic.cuh"
 
 // ------------------------------------------------------------- occupancy
 int occupancy_grid(int kernel_id, int device) {

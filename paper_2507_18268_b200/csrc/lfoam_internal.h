@@ -64,6 +64,7 @@ struct PcgCtl {
   double normFactor, initRes, finRes;
   double wArA, alpha;
   int32_t it, stop, converged, singular;
+  int32_t precond;      // lf_preconditioner of the current solve (host side)
 };
 
 // Global sums consumed by the next launch (after the allreduce in multi-GPU).
@@ -99,6 +100,24 @@ struct LduDev {
   double *upperE;  // [K*n] ELL copy of upper (owner side), 0 in padding
   double *diag, *upper, *source;
   double *bInt, *bBnd;  // per flat boundary face: internalCoeffs, boundaryCoeffs
+  double *symU;    // [KS*ldS] full-row ELL coefficients (DIC meshes), or null
+  int32_t ldS;     // its slab stride
+};
+
+// DIC preconditioner (dic.cuh), built on first use.
+// Full-row ELL: slot k of cell c at k*ldS + c holds its k-th neighbour in
+// ascending label order (lower neighbours, then upper) — for upper-triangular
+// face order that is the order of the faces in OpenFOAM's sequential loops.
+// Label bit 30 marks a neighbour on level 0; empty slots are -1.
+constexpr int DIC_L0BIT = 1 << 30;
+struct DicDev {
+  int32_t L;               // number of levels (>= 1)
+  int32_t contig;          // 1: level l = cells [lvlStart[l], lvlStart[l+1])
+  const int32_t *lvlStart; // [L+1] device
+  const int32_t *lvlCells; // [n] cells ordered by level (null when contig)
+  int32_t KS, ldS;         // row width (6 or 8) and slab stride
+  const int32_t *symN;     // [KS*ldS]
+  double *rD, *rDu;        // reciprocal DIC diagonal; unreciprocated (levels >= 1)
 };
 
 // ---------------------------------------------------------------- kernels
@@ -178,6 +197,19 @@ int persistent_grid(int device, int K);
 bool persistent_chunked();
 void launch_pcg_persistent(cudaStream_t s, int grid, const MeshDev &m, const LduDev &a,
                            const Workspace &ws, unsigned *bar);
+// DIC (dic.cuh)
+int dic_grid(int device, int KS);  // co-resident grid of the DIC solve kernel
+void launch_pcg_dic(cudaStream_t s, int grid, const MeshDev &m, const LduDev &a, const DicDev &d,
+                    const Workspace &ws, unsigned *bar);
+void launch_sym_fill(cudaStream_t s, const Launch &L, const MeshDev &m, const LduDev &a);
+// standalone level passes (ldu_precondition): factor pass l (0 = levels 0 and
+// 1), forward level l >= 1, backward level l; w = M^-1 r without r update
+void launch_dic_factor_level(cudaStream_t s, const Launch &L, const MeshDev &m, const LduDev &a,
+                             const DicDev &d, int l);
+void launch_dic_sweep_level(cudaStream_t s, const Launch &L, const MeshDev &m, const LduDev &a,
+                            const DicDev &d, int l, bool forward, const double *r, double *w);
+void launch_diag_precondition(cudaStream_t s, const Launch &L, int32_t n, const double *diag,
+                              const double *r, double *w);
 void launch_pack_x(cudaStream_t s, int32_t nsend, const int32_t *cells, const double *x,
                    double *buf);
 void launch_permute(cudaStream_t s, int32_t n, const int32_t *idx, const double *in, double *out,

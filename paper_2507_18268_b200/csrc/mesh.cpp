@@ -81,6 +81,49 @@ static std::vector<int32_t> rcm_order(int32_t n, int32_t F, const int32_t *own, 
   return order;
 }
 
+// Greedy first-fit colouring in label order (renumber = 2): colour(c) = the
+// smallest colour not used by a lower-labelled neighbour.  Returns order[i]
+// = caller label of internal cell i, cells sorted by (colour, label): every
+// colour class is a contiguous, dependency-free block — the DIC levels.
+static std::vector<int32_t> colour_order(int32_t n, int32_t F, const int32_t *own, const int32_t *nbr) {
+  std::vector<int32_t> start(n + 1, 0), adj(2 * (size_t)F);
+  for (int32_t f = 0; f < F; ++f) {
+    start[own[f] + 1]++;
+    start[nbr[f] + 1]++;
+  }
+  for (int32_t c = 0; c < n; ++c) start[c + 1] += start[c];
+  std::vector<int32_t> fill(start.begin(), start.end() - 1);
+  int32_t maxDeg = 0;
+  for (int32_t c = 0; c < n; ++c) maxDeg = std::max(maxDeg, start[c + 1] - start[c]);
+  for (int32_t f = 0; f < F; ++f) {
+    adj[fill[own[f]]++] = nbr[f];
+    adj[fill[nbr[f]]++] = own[f];
+  }
+  std::vector<int32_t> col(n, 0), stamp(maxDeg + 2, -1);
+  int32_t nCol = 1;
+  for (int32_t c = 0; c < n; ++c) {
+    for (int32_t k = start[c]; k < start[c + 1]; ++k)
+      if (adj[k] < c) stamp[col[adj[k]]] = c;
+    int32_t k = 0;
+    while (stamp[k] == c) ++k;
+    col[c] = k;
+    nCol = std::max(nCol, k + 1);
+  }
+  std::vector<int32_t> cnt(nCol + 1, 0), order(n);
+  for (int32_t c = 0; c < n; ++c) cnt[col[c] + 1]++;
+  for (int32_t k = 0; k < nCol; ++k) cnt[k + 1] += cnt[k];
+  for (int32_t c = 0; c < n; ++c) order[cnt[col[c]]++] = c;
+  return order;
+}
+
+int balanced_grid(int64_t n, int g0) {
+  const int BSZ = kernel_block_size();
+  const int need = (int)((n + BSZ - 1) / BSZ);
+  if (need <= g0) return std::max(1, need);
+  const int T = (need + g0 - 1) / g0;
+  return (need + T - 1) / T;
+}
+
 static void validate(const lf_mesh_desc *d, int rank) {
   LF_REQUIRE(d != nullptr, "desc is NULL");
   LF_REQUIRE(d->n_cells >= 1, "n_cells must be >= 1");
@@ -89,6 +132,7 @@ static void validate(const lf_mesh_desc *d, int rank) {
   LF_REQUIRE(d->n_faces == 0 || (d->owner && d->neighbour && d->mag_sf && d->delta_coeffs),
              "owner/neighbour/mag_sf/delta_coeffs required");
   LF_REQUIRE(d->V != nullptr, "V required");
+  LF_REQUIRE(d->renumber >= 0 && d->renumber <= 2, "renumber must be 0, 1 (RCM) or 2 (colour)");
   LF_REQUIRE(d->n_patches == 0 || d->patches, "patches required");
   const int32_t n = d->n_cells;
   for (int32_t f = 0; f < d->n_faces; ++f) {
@@ -160,7 +204,8 @@ static void build_mesh(lf_context *ctx, const lf_mesh_desc *d, lf_mesh *M) {
   // ---------------------------------------------- optional renumbering
   std::vector<int32_t> iperm;  // caller -> internal
   if (d->renumber) {
-    std::vector<int32_t> order = rcm_order(n, F, d->owner, d->neighbour);
+    std::vector<int32_t> order = d->renumber == 2 ? colour_order(n, F, d->owner, d->neighbour)
+                                                  : rcm_order(n, F, d->owner, d->neighbour);
     iperm.assign(n, 0);
     for (int32_t i = 0; i < n; ++i) iperm[order[i]] = i;
     M->renumbered = true;

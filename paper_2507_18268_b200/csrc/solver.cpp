@@ -48,6 +48,9 @@ void upload_controls(lf_mesh *M, const lf_solver_controls *c, double *psi) {
   LF_REQUIRE(c != nullptr, "controls is NULL");
   LF_REQUIRE(c->tolerance >= 0.0 && c->rel_tol >= 0.0, "tolerances must be >= 0");
   LF_REQUIRE(c->max_iter >= 0 && c->min_iter >= 0, "max_iter/min_iter must be >= 0");
+  LF_REQUIRE(c->preconditioner >= LF_PRECOND_DIAGONAL && c->preconditioner <= LF_PRECOND_DILU,
+             "unknown preconditioner");
+  if (c->preconditioner != LF_PRECOND_DIAGONAL) require_dic(M);
   PcgCtl *h = M->hctl;
   std::memset(h, 0, sizeof(PcgCtl));
   h->tol = c->tolerance;
@@ -56,6 +59,7 @@ void upload_controls(lf_mesh *M, const lf_solver_controls *c, double *psi) {
   h->minIter = c->min_iter;
   h->nTotal = M->nTotal;
   h->psi = psi;
+  h->precond = c->preconditioner;
   h->stop = 1;  // nothing runs until a setup kernel resets it
   LF_CUDA(cudaMemcpyAsync(M->ws.ctl, h, sizeof(PcgCtl), cudaMemcpyHostToDevice, M->ctx->stream));
   // the pinned mirror is read by the copy engine asynchronously: wait before reuse
@@ -152,7 +156,15 @@ static void run_iterations(lf_mesh *M, lf_solver_perf *out) {
   const int64_t bound = (int64_t)std::max(maxIter, minIter) + 2;
   int64_t launched = 0;
   int chunk = M->lastIters >= 0 ? M->lastIters + 1 : 8;
-  if (ctx->persistent && !ctx->comm && !host_halo(M)) {
+  if (M->hctl->precond != LF_PRECOND_DIAGONAL) {
+    // DIC (DILU = DIC on this symmetric matrix): one persistent launch with
+    // the level-scheduled sweeps (single rank, checked in upload_controls)
+    ctx->launch(LF_K_PCG_DIC, [&] { launch_pcg_dic(s, M->dicGrid, M->md, M->ld, M->dic, M->ws, M->gridBar); });
+    LF_CUDA(cudaMemcpyAsync(M->hctl, M->ws.ctl, sizeof(PcgCtl), cudaMemcpyDeviceToHost, s));
+    LF_CUDA(cudaStreamSynchronize(s));
+    ctx->harvest();
+    chunk = 0;
+  } else if (ctx->persistent && !ctx->comm && !host_halo(M)) {
     // no host-side halo (single rank, or peer-memory transport): the whole
     // loop in one cooperative launch
     ctx->launch(LF_K_PCG, [&] { launch_pcg_persistent(s, M->persistentGrid, M->md, M->ld, M->ws, M->gridBar); });
@@ -219,6 +231,7 @@ void solve_loop(lf_mesh *M, const lf_solver_controls *c, double *psi, bool fromA
   cudaStream_t s = ctx->stream;
   const Workspace &ws = M->ws;
   const bool psiIsT = (psi == M->T);
+  if (M->hctl->precond != LF_PRECOND_DIAGONAL) ensure_dic(M);  // before the assembly writes the rows
   // sum(psi) for normFactor; with the peer-memory transport the same launch
   // puts psi at the processor-face cells into the neighbours' recvT
   if (!(psiIsT && M->sumPsiValid) || M->p2pConnected) sum_psi(M, psi);

@@ -24,7 +24,11 @@ STATUS = {0: "LF_OK", 1: "LF_ERR_INVALID_ARG", 2: "LF_ERR_STATE", 3: "LF_ERR_OOM
 PATCH_TYPES = {"fixedValue": 0, "zeroGradient": 1, "processor": 2}
 FIELD_T, FIELD_PATCH_VALUE, FIELD_DT = 0, 1, 2
 KERNELS = {"assemble": 0, "setup": 1, "phase1": 2, "phase2": 3, "amul": 4, "sumpsi": 5, "pack": 6, "pcg": 7,
-           "nonorth": 8}
+           "nonorth": 8, "pcg_dic": 9, "precond": 10}
+# lf_preconditioner (OpenFOAM fvSolution names)
+PRECONDITIONERS = {"diagonal": 0, "DIC": 1, "DILU": 2}
+# lf_mesh_desc.renumber
+RENUMBER = {False: 0, True: 1, 0: 0, 1: 1, 2: 2, "none": 0, "rcm": 1, "colour": 2}
 OPTIONS = {"persistent": 0, "graphs": 1}
 
 
@@ -54,7 +58,8 @@ class Params(C.Structure):
 
 class Controls(C.Structure):
     _fields_ = [("tolerance", C.c_double), ("rel_tol", C.c_double),
-                ("max_iter", C.c_int32), ("min_iter", C.c_int32)]
+                ("max_iter", C.c_int32), ("min_iter", C.c_int32),
+                ("preconditioner", C.c_int32), ("reserved", C.c_int32)]
 
 
 class Perf(C.Structure):
@@ -89,6 +94,7 @@ SIGNATURES = {
     "lf_ldu_export": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "lf_fvc_grad": (C.c_int, [_vp, _vp, _vp, _vp]),
     "ldu_amul": (C.c_int, [_vp, _vp, _vp]),
+    "ldu_precondition": (C.c_int, [_vp, _i32, _vp, _vp, _vp]),
     "pcg_solve": (C.c_int, [_vp, _vp, C.POINTER(Controls), C.POINTER(Perf)]),
     "laplacianFoam_step": (C.c_int, [_vp, C.POINTER(Params), C.POINTER(Controls), _i32, C.POINTER(Perf)]),
     "lf_set_instrumentation": (C.c_int, [_vp, C.c_int]),
@@ -144,6 +150,13 @@ def _ptr(a):
 
 def _is_device(a) -> bool:
     return not isinstance(a, np.ndarray) and getattr(a, "is_cuda", False)
+
+
+def _device_sync():
+    """Order torch's work and the library stream around a call on device
+    vectors (the context may own a private stream): device-wide sync."""
+    import torch
+    torch.cuda.synchronize()
 
 
 def _check_dev(t, n):
@@ -213,8 +226,8 @@ class Context:
             pass
 
 
-def controls(tol=1e-10, rel_tol=0.0, max_iter=1000, min_iter=0) -> Controls:
-    return Controls(tol, rel_tol, max_iter, min_iter)
+def controls(tol=1e-10, rel_tol=0.0, max_iter=1000, min_iter=0, precond="diagonal") -> Controls:
+    return Controls(tol, rel_tol, max_iter, min_iter, PRECONDITIONERS[precond], 0)
 
 
 class Mesh:
@@ -222,9 +235,11 @@ class Mesh:
     n_cells, owner, neighbour, mag_sf, delta, V, patches[type, face_cells,
     mag_sf, delta, value, neighb_rank])."""
 
-    def __init__(self, ctx: Context, m, renumber: bool = False, geometry: Optional[bool] = None):
-        """geometry: pass the full geometry (Sf, Cf, C, patch Sf) for the
-        non-orthogonal correction path; default: when the description has it."""
+    def __init__(self, ctx: Context, m, renumber=False, geometry: Optional[bool] = None):
+        """renumber: False/0 keep, True/1/"rcm" reverse Cuthill-McKee, 2/"colour"
+        multicolour (the DIC levels); geometry: pass the full geometry (Sf, Cf,
+        C, patch Sf) for the non-orthogonal correction path; default: when the
+        description has it."""
         self.ctx = ctx
         if geometry is None:
             geometry = getattr(m, "Sf", None) is not None
@@ -249,7 +264,7 @@ class Mesh:
             g = [_vec3(m.Sf), _vec3(m.Cf), _vec3(m.C)]  # a missing one -> NULL -> INVALID_ARG
             keep += g
         desc = MeshDesc(int(m.n_cells), int(own.shape[0]), len(m.patches), _ptr(own), _ptr(nb), _ptr(ms),
-                        _ptr(de), _ptr(V), pds, 1 if renumber else 0, _ptr(g[0]), _ptr(g[1]), _ptr(g[2]))
+                        _ptr(de), _ptr(V), pds, RENUMBER[renumber], _ptr(g[0]), _ptr(g[1]), _ptr(g[2]))
         h = C.c_void_p()
         _check(lib().mesh_create(ctx.h, C.byref(desc), C.byref(h)))
         self.h = h
@@ -289,6 +304,7 @@ class Mesh:
     def set_T(self, v):
         if _is_device(v):
             _check_dev(v, self.n_cells)
+            _device_sync()
             _check(lib().field_set(self.h, FIELD_T, -1, _ptr(v), self.n_cells, 1))
         else:
             a = _host(v, np.float64)
@@ -298,6 +314,7 @@ class Mesh:
         if out is not None and _is_device(out):
             _check_dev(out, self.n_cells)
             _check(lib().field_get(self.h, FIELD_T, -1, _ptr(out), self.n_cells, 1))
+            _device_sync()
             return out
         a = np.zeros(self.n_cells) if out is None else out
         _check(lib().field_get(self.h, FIELD_T, -1, _ptr(a), self.n_cells, 0))
@@ -363,7 +380,9 @@ class Mesh:
         _check_dev(grad, 3 * self.n_cells)
         if bgrad is not None:
             _check_dev(bgrad, 3 * self.n_bfaces)
+        _device_sync()
         _check(lib().lf_fvc_grad(self.h, _ptr(x), _ptr(grad), _ptr(bgrad)))
+        _device_sync()
         return grad
 
     def close(self):
@@ -394,11 +413,26 @@ class Ldu:
     def amul(self, x, y):
         _check_dev(x, self.mesh.n_cells)
         _check_dev(y, self.mesh.n_cells)
+        _device_sync()
         _check(lib().ldu_amul(self.h, _ptr(x), _ptr(y)))
+        _device_sync()
         return y
+
+    def precondition(self, r, w, precond: str = "DIC", rD=None):
+        """w = M^-1 r (device vectors, internal numbering); rD (optional
+        device vector) receives the reciprocal preconditioner diagonal."""
+        _check_dev(r, self.mesh.n_cells)
+        _check_dev(w, self.mesh.n_cells)
+        if rD is not None:
+            _check_dev(rD, self.mesh.n_cells)
+        _device_sync()
+        _check(lib().ldu_precondition(self.h, PRECONDITIONERS[precond], _ptr(r), _ptr(w), _ptr(rD)))
+        _device_sync()
+        return w
 
     def pcg_solve(self, psi, **ctl) -> Dict:
         _check_dev(psi, self.mesh.n_cells)
+        _device_sync()
         perf = Perf()
         _check(lib().pcg_solve(self.h, _ptr(psi), C.byref(controls(**ctl)), C.byref(perf)))
         return perf.as_dict()

@@ -43,8 +43,36 @@ def test_binding_matches_header(libpath):
     import paper_2507_18268_b200 as P
     assert sorted(P.SIGNATURES) == header_functions()
     L = P.lib()  # loads on a CPU-only box (CUDA runtime is linked statically)
-    assert L.lf_version() == 1
+    assert L.lf_version() == 2
     assert L.lf_status_string(1) == b"LF_ERR_INVALID_ARG"
+
+
+def test_binding_struct_layouts(tmp_path):
+    """ctypes structs have the C layout of include/lfoam.h (gcc sizeof/offsetof)."""
+    import ctypes as C
+
+    import paper_2507_18268_b200 as P
+    from paper_2507_18268_b200 import lfoam as B
+    checks = {"lf_solver_controls": (B.Controls, ["preconditioner", "reserved"]),
+              "lf_laplacian_params": (B.Params, ["variable_DT"]),
+              "lf_mesh_desc": (B.MeshDesc, ["renumber", "c"]),
+              "lf_patch_desc": (B.PatchDesc, ["neighb_rank", "sf"]),
+              "lf_solver_perf": (B.Perf, ["n_iterations", "reserved"])}
+    src = ['#include <stdio.h>', '#include <stddef.h>', '#include "lfoam.h"', "int main(void){"]
+    for name, (_, fields) in checks.items():
+        src.append(f'printf("{name} %zu\\n", sizeof({name}));')
+        for f in fields:
+            src.append(f'printf("{name}.{f} %zu\\n", offsetof({name}, {f}));')
+    src.append("return 0;}")
+    c = tmp_path / "layout.c"
+    c.write_text("\n".join(src))
+    exe = tmp_path / "layout"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(c), "-o", str(exe)])
+    got = dict(ln.split() for ln in subprocess.check_output([str(exe)], text=True).splitlines())
+    for name, (cls, fields) in checks.items():
+        assert int(got[name]) == C.sizeof(cls), name
+        for f in fields:
+            assert int(got[f"{name}.{f}"]) == getattr(cls, f).offset, (name, f)
 
 
 def test_kernels_built_for_sm100a(libpath):
@@ -70,6 +98,6 @@ def test_product_does_not_import_oracle():
     pkg = os.path.join(ROOT, "paper_2507_18268_b200")
     for dirpath, _, files in os.walk(pkg):
         for f in files:
-            if f.endswith((".py", ".cu", ".cpp", ".h")):
+            if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "liboracle" not in txt and "lfoam_oracle" not in txt, f
