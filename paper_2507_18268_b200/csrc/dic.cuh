@@ -24,6 +24,10 @@
 // Row layout: full-row ELL (DicDev / LduDev.symU), every access coalesced;
 // coefficients written by the assembly kernel.
 
+#ifndef LF_DIC_PAIR
+#define LF_DIC_PAIR 0    // 1: phase 1 interleaves the two colours (thread t: cell t of each).
+#endif                   // r1x: 100^3 3.37 vs 3.13 ms/step, 200^3 39.2 vs 39.9 -> off
+
 // Plain grid barrier of the persistent kernels (no reduction): same
 // protocol as grid_reduce_sync (acq_rel arrival, release by the last block,
 // ld.acquire spin that also invalidates the SM's L1).
@@ -184,6 +188,40 @@ __device__ __forceinline__ void dic_apply(const DicDev &d, const LduDev &a, doub
   grid_reduce_sync<2>(v, partials, bar, out, nop LF_DBG_ARG(0));
 }
 
+// Phase-1 work of one cell in the DIC solve: deferred psi update, p = w +
+// beta p_old, q = A p over the full row (ascending neighbour label = the
+// order of lduMatrix::Amul's face loop), partial sums {p.q, psi}.
+template <int KS>
+__device__ __forceinline__ void dic_amul_cell(const MeshDev &m, const LduDev &a, const DicDev &d, int c,
+                                              bool first, bool cont, double alpha, double beta, double *psi,
+                                              const double *w, const double *pold, double *pnew, double *q,
+                                              double (&v1)[2]) {
+  double ps = psi[c];
+  if (!first) {
+    ps = fma(alpha, pold[c], ps);
+    psi[c] = ps;
+  }
+  v1[1] += ps;
+  if (cont) {
+    SymRow<KS> R;
+    load_row<KS>(d, a, c, R);
+    const double pc = first ? w[c] : fma(beta, pold[c], w[c]);
+    pnew[c] = pc;
+    double pn[KS];
+#pragma unroll
+    for (int kk = 0; kk < KS; ++kk) {
+      const int j = sym_cell(R.lab[kk]);
+      pn[kk] = R.lab[kk] >= 0 ? (first ? w[j] : fma(beta, pold[j], w[j])) : 0.0;
+    }
+    double qc = a.diag[c] * pc;
+#pragma unroll
+    for (int kk = 0; kk < KS; ++kk)
+      if (R.lab[kk] >= 0) qc = fma(R.u[kk], pn[kk], qc);
+    q[c] = qc;
+    v1[0] = fma(pc, qc, v1[0]);
+  }
+}
+
 // ------------------------------------------------ persistent DIC PCG solve
 // The diagonal persistent kernel's state machine (k_pcg_persistent) with
 // the preconditioner application replaced by the level sweeps:
@@ -205,6 +243,7 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
   __shared__ St st;
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
   const int L = d.L;
+  const bool pair = LF_DIC_PAIR && d.contig && L == 2;  // two contiguous colours: interleave in phase 1
   double *psi = ctl->psi;
   double *r = ws.r, *w = ws.w, *q = ws.q;
 
@@ -259,33 +298,20 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
     const double beta = st.beta, alpha = st.alpha;
     const double *pold = (k & 1) ? ws.p[0] : ws.p[1];
     double *pnew = (k & 1) ? ws.p[1] : ws.p[0];
-    // ---- phase 1: flush psi, p = w + beta p_old, q = A p (full rows), sums
+    // ---- phase 1: flush psi, p = w + beta p_old, q = A p (full rows), sums.
+    // With two contiguous levels (multicolour numbering) thread t may handle
+    // cell t of each colour together (LF_DIC_PAIR), so a cell's gathers hit
+    // the lines its partner-colour neighbours just read.
     double v1[2] = {0.0, 0.0};
-    for (int c = gtid; c < m.n; c += stride) {
-      double ps = psi[c];
-      if (!first) {
-        ps = fma(alpha, pold[c], ps);
-        psi[c] = ps;
+    if (pair) {
+      const int n0 = __ldg(d.lvlStart + 1), n1 = m.n - n0, nt = max(n0, n1);
+      for (int t = gtid; t < nt; t += stride) {
+        if (t < n0) dic_amul_cell<KS>(m, a, d, t, first, cont, alpha, beta, psi, w, pold, pnew, q, v1);
+        if (t < n1) dic_amul_cell<KS>(m, a, d, n0 + t, first, cont, alpha, beta, psi, w, pold, pnew, q, v1);
       }
-      v1[1] += ps;
-      if (cont) {
-        SymRow<KS> R;
-        load_row<KS>(d, a, c, R);
-        const double pc = first ? w[c] : fma(beta, pold[c], w[c]);
-        pnew[c] = pc;
-        double pn[KS];
-#pragma unroll
-        for (int kk = 0; kk < KS; ++kk) {
-          const int j = sym_cell(R.lab[kk]);
-          pn[kk] = R.lab[kk] >= 0 ? (first ? w[j] : fma(beta, pold[j], w[j])) : 0.0;
-        }
-        double qc = a.diag[c] * pc;
-#pragma unroll
-        for (int kk = 0; kk < KS; ++kk)
-          if (R.lab[kk] >= 0) qc = fma(R.u[kk], pn[kk], qc);
-        q[c] = qc;
-        v1[0] = fma(pc, qc, v1[0]);
-      }
+    } else {
+      for (int c = gtid; c < m.n; c += stride)
+        dic_amul_cell<KS>(m, a, d, c, first, cont, alpha, beta, psi, w, pold, pnew, q, v1);
     }
     grid_reduce_sync<2>(v1, ws.partials, bar, ws.gsum->p1, nop LF_DBG_ARG(0));
     if (!cont) break;

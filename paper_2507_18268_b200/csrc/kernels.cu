@@ -34,13 +34,13 @@ namespace lf {
 // ---- tuning knobs (defaults = the shipped configuration; variants are built
 // with -D for measurements, see scripts/variants.py and profiles/)
 #ifndef LF_BS
-#define LF_BS 256        // threads per block
-#endif
+#define LF_BS 512        // threads per block (r1u sweep: 512 beats 256 by 2.4% at 100^3, 1.6% at
+#endif                   // 200^3 in the persistent solve — fewer arrivals per grid barrier)
 #ifndef LF_MINB
-#define LF_MINB 4        // __launch_bounds__ min blocks/SM (register cap 65536/(BS*MINB))
+#define LF_MINB 2        // __launch_bounds__ min blocks/SM (register cap 65536/(BS*MINB))
 #endif
 #ifndef LF_MINB_G
-#define LF_MINB_G 5      // same, for the row-gather kernels (phase 1, Amul, PCG setup)
+#define LF_MINB_G 2      // same, for the row-gather kernels (phase 1, Amul, PCG setup)
 #endif
 #ifndef LF_P2_UNROLL
 #define LF_P2_UNROLL 4   // cells per thread per grid-stride trip in phase 2
@@ -837,8 +837,8 @@ __device__ void grid_reduce_sync(double (&v)[NV], double *partials, unsigned *ba
 }
 
 #ifndef LF_MINB_P
-#define LF_MINB_P 4  // persistent kernel blocks/SM: 64 registers, no spills (r1o: 100^3
-                     // 3.39 ms/step vs 3.71 with 5 blocks/SM and 60 B of spills)
+#define LF_MINB_P 2  // persistent kernel blocks/SM (x512 threads): 64 registers, no spills
+                     // (r1o: 100^3 3.39 ms/step at 64 regs vs 3.71 with 60 B of spills)
 #endif
 #ifndef LF_TIMING
 #define LF_TIMING 0  // 1: per-phase / per-barrier times printed by the persistent kernel

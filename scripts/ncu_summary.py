@@ -82,7 +82,7 @@ def main(tag):
     tj_path = os.path.join(PROF, "ncu_traffic.json")
     tj = json.load(open(tj_path)) if os.path.exists(tj_path) else {}
     for rep in sorted(glob.glob(os.path.join(OUT, f"prof_{tag}_cfg*_k_*.ncu-rep"))):
-        m = re.search(r"cfg(\d+(?:-corr\d+)?(?:-dt)?)_(k_\w+)\.ncu-rep", rep)
+        m = re.search(r"cfg(\d+(?:-corr\d+)?(?:-dt)?(?:-dic)?)_(k_\w+)\.ncu-rep", rep)
         cfg, kern = m.group(1), m.group(2)
         det, rd, traffic = summarise(rep)
         lines.append(f"## config {cfg} — `{kern}`")
@@ -97,7 +97,7 @@ def main(tag):
             tj.setdefault(f"config{cfg}", {})[kern] = traffic
         lines.append("")
     for path in sorted(glob.glob(os.path.join(OUT, f"launches_{tag}_cfg*.csv"))):
-        cfg = re.search(r"cfg(\d+(?:-corr\d+)?(?:-dt)?)", path).group(1)
+        cfg = re.search(r"cfg(\d+(?:-corr\d+)?(?:-dt)?(?:-dic)?)", path).group(1)
         agg = launch_table(path)
         lines.append(f"## config {cfg} — launch list (`--metrics gpu__time_duration.sum,dram__bytes_*`)")
         lines.append("")

@@ -12,14 +12,11 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-# name -> (-D defines, bench --mode)
+# name -> (-D defines, bench --mode[, bench --precond])
 VARIANTS = {
+    "dic_p1": ([], "persistent", "DIC"),
+    "dic_p0": (["LF_DIC_PAIR=0"], "persistent", "DIC"),
     "persist": ([], "persistent"),
-    "graphs": ([], "graphs"),
-    "p_u1": (["LF_P2P_UNROLL=1"], "persistent"),
-    "p_pipe_m3": (["LF_P1_PIPE=1", "LF_MINB_P=3"], "persistent"),
-    "p_pipe_m4": (["LF_P1_PIPE=1", "LF_MINB_P=4"], "persistent"),
-    "p_pipe_m5": (["LF_P1_PIPE=1", "LF_MINB_P=5"], "persistent"),
 }
 
 
@@ -30,7 +27,7 @@ def libname(name):
 def build():
     from paper_2507_18268_b200 import build as B
     built = {}
-    for name, (defs, _) in VARIANTS.items():
+    for name, (defs, *_) in VARIANTS.items():
         key = tuple(defs)
         if key in built:  # same defines: reuse
             continue
@@ -40,7 +37,7 @@ def build():
 
 def lib_for(name):
     defs = tuple(VARIANTS[name][0])
-    for other, (d, _) in VARIANTS.items():
+    for other, (d, *_) in VARIANTS.items():
         if tuple(d) == defs:
             return libname(other)
 
@@ -48,10 +45,11 @@ def lib_for(name):
 def run(cfgs, steps=10):
     rows = []
     for cfg in cfgs:
-        for name, (_, mode) in VARIANTS.items():
+        for name, (_, mode, *pc) in VARIANTS.items():
             env = dict(os.environ, LFOAM_LIB=lib_for(name))
             r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", str(steps), "--warmup", "3",
-                                "--config", str(cfg), "--no-cpu-baseline", "--mode", mode],
+                                "--config", str(cfg), "--no-cpu-baseline", "--mode", mode,
+                                "--precond", pc[0] if pc else "diagonal"],
                                capture_output=True, text=True, env=env, timeout=1800)
             line = [l for l in r.stdout.splitlines() if l.startswith("{")]
             if not line:
