@@ -44,25 +44,26 @@ PAPER_GH200 = {"S": (0.56, 1.93, 6.78), "M": (2.04, 12.53, 50.83), "L": (5.90, 4
                "XL": (13.31, 144.92, 458.93)}
 
 
-def run_once(P, ctx, m, t_gen, steps, DT, dt, tol, write_interval):
+def run_once(P, ctx, m, t_gen, steps, DT, dt, tol, write_interval, precond="diagonal", renumber=0):
     import torch
     torch.cuda.synchronize()
     ctx.set_instrumentation(True)
     w0 = time.perf_counter()
-    mesh = P.Mesh(ctx, m)                       # "read initial data": upload + build
+    mesh = P.Mesh(ctx, m, renumber=renumber)    # "read initial data": upload + build
     mesh.set_T(np.zeros(m.n_cells))
     perfs = []
     tmp = tempfile.mkdtemp(prefix="lfoam_protocol_") if write_interval else None
     host = np.zeros(m.n_cells)
     for k in range(steps):
-        perfs += mesh.step(1, DT, dt, tol=tol)
+        perfs += mesh.step(1, DT, dt, tol=tol, precond=precond)
         if write_interval and (k + 1) % write_interval == 0:
             mesh.get_T(host)
             np.save(os.path.join(tmp, f"T_{k + 1}.npy"), host)
     T = mesh.get_T()
     wall = time.perf_counter() - w0
     asm = ctx.kernel_stats("assemble")[1] / 1e3
-    solver = sum(ctx.kernel_stats(k)[1] for k in ("pcg", "phase1", "phase2", "setup", "sumpsi", "pack")) / 1e3
+    solver = sum(ctx.kernel_stats(k)[1] for k in ("pcg", "pcg_dic", "precond", "phase1", "phase2", "setup",
+                                                   "sumpsi", "pack")) / 1e3
     ctx.set_instrumentation(False)
     mesh.close()
     if tmp:
@@ -83,6 +84,8 @@ def main():
     ap.add_argument("--tol", type=float, default=1e-10)
     ap.add_argument("--write-interval", type=int, default=0, help="write T to disk every K steps (0 = never)")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "protocol.md"))
+    ap.add_argument("--precond", default="diagonal", choices=["diagonal", "DIC"])
+    ap.add_argument("--renumber", type=int, default=-1, help="default: 2 (multicolour) with DIC, else 0")
     args = ap.parse_args()
 
     import torch
@@ -96,7 +99,8 @@ def main():
         t0 = time.perf_counter()
         mg = meshgen.protocol_mesh(name)          # host-side generator, not timed (no file I/O here)
         t_gen = time.perf_counter() - t0
-        runs = [run_once(P, ctx, mg, t_gen, args.steps, DT, dt, args.tol, args.write_interval)
+        rn = args.renumber if args.renumber >= 0 else (2 if args.precond != "diagonal" else 0)
+        runs = [run_once(P, ctx, mg, t_gen, args.steps, DT, dt, args.tol, args.write_interval, args.precond, rn)
                 for _ in range(args.repeats)]
         T, m = runs[-1]["T"], runs[-1]["m"]
         # 1-D check of the last run: every x-line equals the same profile
@@ -105,7 +109,7 @@ def main():
         line_spread = float(np.max(np.abs(prof - prof[0])))
         stat = lambda k: (statistics.mean(r[k] for r in runs), statistics.pstdev(r[k] for r in runs))
         row = {"mesh": f"Mesh-{name}", "N": m.dims[0], "n_cells": m.n_cells, "steps": args.steps,
-               "repeats": args.repeats, "DT": DT, "dt": dt, "tol": args.tol,
+               "repeats": args.repeats, "DT": DT, "dt": dt, "tol": args.tol, "precond": args.precond,
                "write_interval": args.write_interval,
                "assembly_s": stat("assembly_s"), "solver_s": stat("solver_s"),
                "execution_s": stat("execution_s"), "meshgen_s_host": stat("meshgen_s"),
@@ -119,7 +123,7 @@ def main():
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     with open(args.out, "w") as f:
         f.write("# Paper protocol on one B200 (SURVEY §8(f) row 4)\n\n")
-        f.write(f"Hot plate, DT = {DT}, dt = {dt} s, {args.steps} steps (100 s), PCG + diagonal, tol {args.tol}, "
+        f.write(f"Hot plate, DT = {DT}, dt = {dt} s, {args.steps} steps (100 s), PCG + {args.precond}, tol {args.tol}, "
                 f"{args.repeats} repeats (mean ± std), field writes every {args.write_interval or 'never'}.  "
                 "Assembly / Solver = summed CUDA-event kernel time; Execution = wall clock of "
                 "mesh_create + field_set + steps + field_get (the paper's 'Execution' includes reading "
