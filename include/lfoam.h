@@ -252,8 +252,11 @@ LF_API lf_status ldu_amul(const lf_ldu *sys, const double *x_dev, double *y_dev)
  *                        level of its lower neighbours), so the parallel depth
  *                        is the number of levels — 2 on a hex block numbered
  *                        with renumber = 2, 3N-2 on the natural N^3 numbering.
- *                        Single rank, no processor patches (else INVALID_ARG);
- *                        runs in the persistent solver whatever LF_OPT_PERSISTENT
+ *                        Processor-local like OpenFOAM's (interfaces do not enter
+ *                        the factor or the sweeps: block-Jacobi IC(0) across
+ *                        ranks); processor patches need the peer-memory
+ *                        transport (lf_p2p_*), not NCCL (else INVALID_ARG); runs
+ *                        in the persistent solver whatever LF_OPT_PERSISTENT
  *                        says; cells may have at most 8 neighbours.
  *   LF_PRECOND_DILU      OpenFOAM DILUPreconditioner; on this symmetric matrix
  *                        (lower == upper) its recurrences are DIC's term for
@@ -288,8 +291,8 @@ LF_API lf_status ldu_precondition(const lf_ldu *sys, int32_t preconditioner, con
  * evaluated on the device.  With DIC the preconditioner is rebuilt from the
  * current coefficients at every solve (as OpenFOAM constructs it per solve).
  * Returns once *out is on the host.  Non-convergence and singularity are
- * LF_OK with flags set; an unknown preconditioner or DIC on a mesh with
- * processor patches / more than 8 neighbours per cell is INVALID_ARG. */
+ * LF_OK with flags set; an unknown preconditioner, or DIC with NCCL
+ * processor patches / more than 8 neighbours per cell, is INVALID_ARG. */
 LF_API lf_status pcg_solve(lf_ldu *sys, double *psi_dev, const lf_solver_controls *c, lf_solver_perf *out);
 
 /* n_steps laplacianFoam time steps on the mesh's T field: each step

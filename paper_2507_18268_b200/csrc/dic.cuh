@@ -28,32 +28,6 @@
 #define LF_DIC_PAIR 0    // 1: phase 1 interleaves the two colours (thread t: cell t of each).
 #endif                   // r1x: 100^3 3.37 vs 3.13 ms/step, 200^3 39.2 vs 39.9 -> off
 
-// Plain grid barrier of the persistent kernels (no reduction): same
-// protocol as grid_reduce_sync (acq_rel arrival, release by the last block,
-// ld.acquire spin that also invalidates the SM's L1).
-__device__ __forceinline__ void grid_barrier(unsigned *bar) {
-  __shared__ int amLastB;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned gen = ld_acquire(bar + 1);
-    unsigned t;
-    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(t) : "l"(bar) : "memory");
-    amLastB = (t == gridDim.x - 1);
-    if (amLastB) {
-      bar[0] = 0u;
-      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar + 1) : "memory");
-    } else {
-      const unsigned long long t0 = gtime_ns();
-      unsigned tries = 0;
-      while (ld_acquire(bar + 1) == gen) {
-        __nanosleep(32);
-        spin_check(t0, tries);
-      }
-    }
-  }
-  __syncthreads();
-}
-
 template <int KS>
 struct SymRow {
   int lab[KS];
@@ -155,11 +129,14 @@ __device__ __forceinline__ int level_cell(const DicDev &d, int t) { return d.con
 
 // One application of the preconditioner inside the persistent kernel (upd:
 // fused r -= alpha q), ending in the reducing barrier that publishes
-// {sum|r|, sum w.r} to out[0..1].
-template <int KS>
-__device__ __forceinline__ void dic_apply(const DicDev &d, const LduDev &a, double *r, const double *q,
-                                          double *w, bool upd, double alpha, unsigned *bar,
-                                          double *partials, double *out, const P2PDev &nop) {
+// {sum|r|, sum w.r} to out[0..1].  HALO: each final w of a cell with
+// processor faces is stored into the neighbour ranks' recvW (peer memory),
+// ordered before the reduction's cross-rank exchange; the factor and the
+// sweeps themselves are processor-local, as OpenFOAM's DIC (reading A42).
+template <int KS, bool HALO>
+__device__ __forceinline__ void dic_apply(const MeshDev &m, const DicDev &d, const LduDev &a, double *r,
+                                          const double *q, double *w, bool upd, double alpha, unsigned *bar,
+                                          double *partials, double *out, const P2PDev &pp) {
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
   const int L = d.L;
   double v[2] = {0.0, 0.0};
@@ -170,7 +147,10 @@ __device__ __forceinline__ void dic_apply(const DicDev &d, const LduDev &a, doub
       double wc;
       const double rc = dic_forward_cell<KS>(d, a, c, r, q, w, upd, alpha, wc);
       v[0] += fabs(rc);
-      if (l == L - 1) v[1] = fma(wc, rc, v[1]);  // no upper neighbours: final
+      if (l == L - 1) {  // no upper neighbours: final
+        v[1] = fma(wc, rc, v[1]);
+        if (HALO && pp.P > 0) push_halo(m, pp.dstW, c, wc);
+      }
     }
     grid_barrier(bar);
   }
@@ -182,20 +162,22 @@ __device__ __forceinline__ void dic_apply(const DicDev &d, const LduDev &a, doub
       const double rc = dic_backward_cell<KS>(d, a, c, l == 0, r, q, w, upd, alpha, wc);
       if (l == 0) v[0] += fabs(rc);
       v[1] = fma(wc, rc, v[1]);
+      if (HALO && pp.P > 0) push_halo(m, pp.dstW, c, wc);
     }
     if (l > 0) grid_barrier(bar);
   }
-  grid_reduce_sync<2>(v, partials, bar, out, nop LF_DBG_ARG(0));
+  grid_reduce_sync<2>(v, partials, bar, out, pp LF_DBG_ARG(0));
 }
 
 // Phase-1 work of one cell in the DIC solve: deferred psi update, p = w +
 // beta p_old, q = A p over the full row (ascending neighbour label = the
-// order of lduMatrix::Amul's face loop), partial sums {p.q, psi}.
-template <int KS>
-__device__ __forceinline__ void dic_amul_cell(const MeshDev &m, const LduDev &a, const DicDev &d, int c,
-                                              bool first, bool cont, double alpha, double beta, double *psi,
-                                              const double *w, const double *pold, double *pnew, double *q,
-                                              double (&v1)[2]) {
+// order of lduMatrix::Amul's face loop) minus the processor-interface term
+// (HALO: halo p recomputed from the neighbour's w), partial sums {p.q, psi}.
+template <int KS, bool HALO>
+__device__ __forceinline__ void dic_amul_cell(const MeshDev &m, const LduDev &a, const DicDev &d,
+                                              const Workspace &ws, int k, int c, bool first, bool cont,
+                                              double alpha, double beta, double *psi, const double *w,
+                                              const double *pold, double *pnew, double *q, double (&v1)[2]) {
   double ps = psi[c];
   if (!first) {
     ps = fma(alpha, pold[c], ps);
@@ -217,6 +199,7 @@ __device__ __forceinline__ void dic_amul_cell(const MeshDev &m, const LduDev &a,
 #pragma unroll
     for (int kk = 0; kk < KS; ++kk)
       if (R.lab[kk] >= 0) qc = fma(R.u[kk], pn[kk], qc);
+    if (HALO) qc -= row_proc_p(m, a.bBnd, ws, first, beta, k, c);
     q[c] = qc;
     v1[0] = fma(pc, qc, v1[0]);
   }
@@ -228,14 +211,15 @@ __device__ __forceinline__ void dic_amul_cell(const MeshDev &m, const LduDev &a,
 //   set-up:    DIC factor (L-1 passes), w = M^-1 r (2L-2 barriers), sum w.r
 //   iteration: phase 1 (p, q = A p over full rows, sum p.q, deferred psi)
 //              | r -= alpha q fused into the sweeps, w = M^-1 r, sum|r|, sum w.r
-// Single rank, no processor patches (the DIC is processor-local in OpenFOAM;
-// the halo variant is future work).
-template <int KS>
+// HALO: processor patches through the peer-memory transport (halo w puts in
+// the sweeps, halo p recomputed in the Amul phase, rank-ordered mailbox
+// allreduce in the two reducing barriers), as k_pcg_persistent<.., true>.
+template <int KS, bool HALO>
 __global__ void __launch_bounds__(BS, LF_MINB_P)
     k_pcg_dic(MeshDev m, LduDev a, DicDev d, Workspace ws, unsigned *bar) {
   PcgCtl *ctl = ws.ctl;
   if (ctl->stop) return;
-  const P2PDev &nop = ws.p2p;  // P == 0: single rank (set by launch_pcg_dic)
+  const P2PDev &pp = ws.p2p;  // P == 0 unless HALO with the peer-memory transport
   struct St {
     double nf, initRes, finRes, wArA, alpha, beta;
     int k, cont, singular;
@@ -277,7 +261,7 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
       }
     }
     grid_barrier(bar);
-    dic_apply<KS>(d, a, r, q, w, false, 0.0, bar, ws.partials, ws.gsum->p2, nop);  // w = M^-1 r (set-up)
+    dic_apply<KS, HALO>(m, d, a, r, q, w, false, 0.0, bar, ws.partials, ws.gsum->p2, pp);  // set-up w
   }
   for (;;) {
     if (threadIdx.x == 0) {
@@ -306,14 +290,15 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
     if (pair) {
       const int n0 = __ldg(d.lvlStart + 1), n1 = m.n - n0, nt = max(n0, n1);
       for (int t = gtid; t < nt; t += stride) {
-        if (t < n0) dic_amul_cell<KS>(m, a, d, t, first, cont, alpha, beta, psi, w, pold, pnew, q, v1);
-        if (t < n1) dic_amul_cell<KS>(m, a, d, n0 + t, first, cont, alpha, beta, psi, w, pold, pnew, q, v1);
+        if (t < n0) dic_amul_cell<KS, HALO>(m, a, d, ws, k, t, first, cont, alpha, beta, psi, w, pold, pnew, q, v1);
+        if (t < n1)
+          dic_amul_cell<KS, HALO>(m, a, d, ws, k, n0 + t, first, cont, alpha, beta, psi, w, pold, pnew, q, v1);
       }
     } else {
       for (int c = gtid; c < m.n; c += stride)
-        dic_amul_cell<KS>(m, a, d, c, first, cont, alpha, beta, psi, w, pold, pnew, q, v1);
+        dic_amul_cell<KS, HALO>(m, a, d, ws, k, c, first, cont, alpha, beta, psi, w, pold, pnew, q, v1);
     }
-    grid_reduce_sync<2>(v1, ws.partials, bar, ws.gsum->p1, nop LF_DBG_ARG(0));
+    grid_reduce_sync<2>(v1, ws.partials, bar, ws.gsum->p1, pp LF_DBG_ARG(0));
     if (!cont) break;
     if (threadIdx.x == 0) {
       const double pq = __ldcg(&ws.gsum->p1[0]);
@@ -323,7 +308,7 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
     __syncthreads();
     if (st.singular) break;
     // ---- r -= alpha q, w = M^-1 r, sum|r|, sum w.r
-    dic_apply<KS>(d, a, r, q, w, true, st.alpha, bar, ws.partials, ws.gsum->p2, nop);
+    dic_apply<KS, HALO>(m, d, a, r, q, w, true, st.alpha, bar, ws.partials, ws.gsum->p2, pp);
     if (threadIdx.x == 0) ++st.k;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -339,21 +324,28 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
   }
 }
 
+template <bool HALO>
+static const void *dic_fn(int KS) {
+  return KS <= 6 ? (const void *)k_pcg_dic<6, HALO> : (const void *)k_pcg_dic<8, HALO>;
+}
+
 int dic_grid(int device, int KS) {
-  int sms = 0, nb = 0;
+  int sms = 0, best = 1 << 30;
   LF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-  const void *fn = KS <= 6 ? (const void *)k_pcg_dic<6> : (const void *)k_pcg_dic<8>;
-  LF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, BS, 0));
-  return sms * (nb < 1 ? 1 : nb);
+  for (const void *fn : {dic_fn<false>(KS), dic_fn<true>(KS)}) {  // co-resident for both variants
+    int nb = 0;
+    LF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, BS, 0));
+    best = std::min(best, nb);
+  }
+  return sms * (best < 1 ? 1 : best);
 }
 
 void launch_pcg_dic(cudaStream_t s, int grid, const MeshDev &m, const LduDev &a, const DicDev &d,
                     const Workspace &ws, unsigned *bar) {
-  Workspace w1 = ws;
-  w1.p2p.P = 0;  // single rank: the reductions exchange nothing
-  void *args[] = {(void *)&m, (void *)&a, (void *)&d, (void *)&w1, (void *)&bar};
-  const void *fn = d.KS <= 6 ? (const void *)k_pcg_dic<6> : (const void *)k_pcg_dic<8>;
-  LF_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(BS), args, 0, s));
+  void *args[] = {(void *)&m, (void *)&a, (void *)&d, (void *)&ws, (void *)&bar};
+  const bool halo = m.hasProc || ws.p2p.P > 0;
+  LF_CUDA(cudaLaunchCooperativeKernel(halo ? dic_fn<true>(d.KS) : dic_fn<false>(d.KS), dim3(grid), dim3(BS), args,
+                                      0, s));
 }
 
 // ------------------------------------------- full-row coefficients (fill)

@@ -836,6 +836,32 @@ __device__ void grid_reduce_sync(double (&v)[NV], double *partials, unsigned *ba
   }
 }
 
+// Plain grid barrier of the persistent kernels (no reduction): same
+// protocol as grid_reduce_sync (acq_rel arrival, release by the last block,
+// ld.acquire spin that also invalidates the SM's L1).
+__device__ __forceinline__ void grid_barrier(unsigned *bar) {
+  __shared__ int amLastB;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned gen = ld_acquire(bar + 1);
+    unsigned t;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(t) : "l"(bar) : "memory");
+    amLastB = (t == gridDim.x - 1);
+    if (amLastB) {
+      bar[0] = 0u;
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar + 1) : "memory");
+    } else {
+      const unsigned long long t0 = gtime_ns();
+      unsigned tries = 0;
+      while (ld_acquire(bar + 1) == gen) {
+        __nanosleep(32);
+        spin_check(t0, tries);
+      }
+    }
+  }
+  __syncthreads();
+}
+
 #ifndef LF_MINB_P
 #define LF_MINB_P 2  // persistent kernel blocks/SM (x512 threads): 64 registers, no spills
                      // (r1o: 100^3 3.39 ms/step at 64 regs vs 3.71 with 60 B of spills)
@@ -1073,8 +1099,8 @@ static const void *persistent_fn(const MeshDev &m) {
 
 void launch_pcg_persistent(cudaStream_t s, int grid, const MeshDev &m, const LduDev &a,
                            const Workspace &ws, unsigned *bar) {
-  void *args[] = {(void *)&m, (void *)&a, (void *)&ws, (void *)&bar};
   const bool halo = m.hasProc || ws.p2p.P > 0;
+  void *args[] = {(void *)&m, (void *)&a, (void *)&ws, (void *)&bar};
   const void *fn = halo ? persistent_fn<true>(m) : persistent_fn<false>(m);
   LF_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(BS), args, 0, s));
 }

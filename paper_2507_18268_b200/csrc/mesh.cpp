@@ -524,7 +524,7 @@ static void build_mesh(lf_context *ctx, const lf_mesh_desc *d, lf_mesh *M) {
                           : balanced(persistent_grid(ctx->device, md.K));
   int maxGrid = std::max({M->Lasm.grid, M->Lp1.grid, M->Lp2.grid, M->Lamul.grid, M->Lsetup.grid, M->Lsum.grid,
                           M->persistentGrid});
-  M->gridBar = A.alloc<unsigned>(2);
+  M->gridBar = A.alloc<unsigned>(2);  // {arrivals, generation}
   LF_CUDA(cudaMemsetAsync(M->gridBar, 0, 2 * sizeof(unsigned), s));
   Workspace &ws = M->ws;
   ws.maxGrid = maxGrid;

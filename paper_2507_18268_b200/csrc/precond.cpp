@@ -14,8 +14,10 @@
 namespace lf {
 
 void require_dic(const lf_mesh *M) {
-  LF_REQUIRE(M->nproc == 0 && !M->ctx->comm && !M->p2pConnected,
-             "the DIC preconditioner runs on a single rank without processor patches");
+  // the DIC solve is one persistent launch: processor patches need the
+  // peer-memory transport (halo and sums inside the kernel), not NCCL
+  LF_REQUIRE(!M->ctx->comm && (M->nproc == 0 || M->p2pConnected),
+             "the DIC preconditioner needs a single rank or the peer-memory transport (lf_p2p_*)");
   LF_REQUIRE(M->n < DIC_L0BIT, "the DIC preconditioner needs n_cells < 2^30");
 }
 

@@ -14,9 +14,10 @@ sys.path.insert(0, ROOT)
 
 # name -> (-D defines, bench --mode[, bench --precond])
 VARIANTS = {
-    "dic_p1": ([], "persistent", "DIC"),
-    "dic_p0": (["LF_DIC_PAIR=0"], "persistent", "DIC"),
-    "persist": ([], "persistent"),
+    "barall": ([], "persistent"),
+    "barlast": (["LF_BAR_ALL=0"], "persistent"),
+    "dic_barall": ([], "persistent", "DIC"),
+    "dic_barlast": (["LF_BAR_ALL=0"], "persistent", "DIC"),
 }
 
 

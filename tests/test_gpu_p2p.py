@@ -61,13 +61,48 @@ def test_p2p_loopback_single_process(P, persistent):
     ctx.close()
 
 
+@pytest.mark.parametrize("renumber", [0, 2])
+def test_p2p_loopback_dic(P, renumber):
+    """DIC through the peer-memory transport (processor-local factor and
+    sweeps, halo w puts, mailbox allreduce) vs the oracle on the same cut
+    mesh with its self halo, in the same numbering (A41, A42)."""
+    m = meshgen.block_mesh(10, 9, 12, bc={"ymin": ("fixedValue", 1.0)})
+    c = decompose.cut_mesh(m, decompose.z_plane_faces(m, 6))
+    s = meshgen.multimode_field(m)
+    order = meshgen.colour_order(c) if renumber == 2 else np.arange(c.n_cells)
+    co = meshgen.relabel_mesh(c, order) if renumber == 2 else c
+    To, _, po = oracle.laplacian_foam(co, s[order], 4, halo=oracle.self_halo(co), precond="DIC")
+    ctx = P.Context(0)
+    ctx.p2p_init(1, 0)
+    mesh = P.Mesh(ctx, c, renumber=renumber)
+    mesh.p2p_connect([mesh.p2p_export()], 0)
+    mesh.set_T(s)
+    pg = mesh.step(4, precond="DIC")
+    T = mesh.get_T()[order]
+    assert np.max(np.abs(T - To)) <= 1e-8 * np.max(np.abs(To))
+    assert all(abs(a["n_iterations"] - b["n_iterations"]) <= 1 for a, b in zip(pg, po)), (pg, po)
+    ctx.close()
+
+
+def test_dic_needs_peer_memory_with_processor_patches(P):
+    m = meshgen.block_mesh(6)
+    c = decompose.cut_mesh(m, decompose.z_plane_faces(m, 3))
+    ctx = P.Context(0)
+    mesh = P.Mesh(ctx, c)
+    mesh.set_T(np.ones(c.n_cells))
+    with pytest.raises(P.LfoamError) as e:
+        mesh.step(1, precond="DIC")
+    assert e.value.status == 1
+    ctx.close()
+
+
 def _free_port():
     with socket.socket() as sk:
         sk.bind(("127.0.0.1", 0))
         return sk.getsockname()[1]
 
 
-def _rank_main(rank, world, port, persistent, out):
+def _rank_main(rank, world, port, persistent, out, precond="diagonal"):
     import torch.distributed as dist
     import paper_2507_18268_b200 as P
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -84,9 +119,18 @@ def _rank_main(rank, world, port, persistent, out):
         hs = [None] * world
         dist.all_gather_object(hs, mesh.p2p_export())
         mesh.p2p_connect(hs, rank)
-        mesh.set_T(meshgen.multimode_field(g)[cells])
-        perfs = mesh.step(3)
-        out[rank] = ("ok", cells, mesh.get_T(), [p["n_iterations"] for p in perfs])
+        T0 = meshgen.multimode_field(g)[cells]
+        mesh.set_T(T0)
+        perfs = mesh.step(3, precond=precond)
+        ref = None
+        if precond != "diagonal":
+            # the decomposed oracle on the same subdomain (gloo gSum / halo):
+            # block-Jacobi DIC, processor-local like OpenFOAM's
+            from test_decompose import gloo_oracle_callbacks
+            gsum, halo = gloo_oracle_callbacks(m)
+            To, _, po = oracle.laplacian_foam(m, T0, 3, gsum=gsum, halo=halo, precond=precond)
+            ref = (To, [p["n_iterations"] for p in po])
+        out[rank] = ("ok", cells, mesh.get_T(), [p["n_iterations"] for p in perfs], ref)
         dist.barrier()
         ctx.close()
     except Exception as e:  # report instead of hanging the peer
@@ -120,8 +164,34 @@ def test_p2p_two_processes_one_gpu(P, persistent):
     To, _, po = oracle.laplacian_foam(g, s, 3)
     T = np.zeros(g.n_cells)
     for r in range(world):
-        _, cells, Tr, its = res[r]
+        _, cells, Tr, its, _ = res[r]
         T[cells] = Tr
         assert all(abs(a - b["n_iterations"]) <= 1 for a, b in zip(its, po)), (its, po)
     assert res[0][3] == res[1][3]          # identical stopping decisions on both ranks
     assert np.max(np.abs(T - To)) <= 1e-8 * np.max(np.abs(To))
+
+
+def test_p2p_two_processes_one_gpu_dic(P):
+    """Two ranks, DIC (block-Jacobi IC(0) across the slab interface): each
+    rank against the decomposed oracle run in the same process over gloo."""
+    import torch.multiprocessing as mp
+    world = 2
+    ctx = mp.get_context("spawn")
+    out = ctx.Manager().dict()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank_main, args=(r, world, port, True, out, "DIC")) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+    for p in procs:
+        if p.is_alive():
+            p.kill()
+    res = dict(out)
+    assert len(res) == world, res
+    for r in range(world):
+        assert res[r][0] == "ok", res[r]
+        _, cells, Tr, its, (To, its_o) = res[r]
+        assert np.max(np.abs(Tr - To)) <= 1e-8 * np.max(np.abs(To))
+        assert all(abs(a - b) <= 1 for a, b in zip(its, its_o)), (its, its_o)
+    assert res[0][3] == res[1][3]
