@@ -15,7 +15,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "gpurun_out")
-PROF = os.path.join(ROOT, "profiles")
+PROF = os.environ.get("NCU_SUMMARY_DIR", os.path.join(ROOT, "profiles"))
 
 DETAILS = ["Duration", "Elapsed Cycles", "SM Active Cycles", "DRAM Throughput", "Memory Throughput",
            "L2 Hit Rate", "L1/TEX Hit Rate", "Achieved Occupancy", "Registers Per Thread", "Grid Size",
