@@ -873,6 +873,10 @@ __device__ __forceinline__ void grid_barrier(unsigned *bar) {
 #define LF_CHUNKED 0  // persistent kernel: contiguous cell chunk per block (vs grid stride).
 #endif                // r1n: chunks raise the phase-1 arrival spread 6 -> 28 us at 100^3 -> off
 bool persistent_chunked() { return LF_CHUNKED != 0; }
+#ifndef LF_TAIL
+#define LF_TAIL 1  // persistent kernel: spread the last partial trip over all blocks
+#endif
+bool persistent_tail() { return LF_TAIL != 0; }
 #ifndef LF_P2P_UNROLL
 #define LF_P2P_UNROLL 2  // persistent phase 2 cells per trip
 #endif
@@ -911,6 +915,20 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
   const int cstart = cbeg + threadIdx.x, cstep = blockDim.x;
 #else
   const int cstart = blockIdx.x * blockDim.x + threadIdx.x, cend = m.n, cstep = gridDim.x * blockDim.x;
+#endif
+#if LF_TAIL
+  // full grid-stride trips while every thread has a cell, then ONE tail trip
+  // whose R leftover cells are spread evenly over all blocks (ceil(R/G)
+  // consecutive cells each): every block handles the same number of cells
+  // +-1 and all SMs still sweep the cell range together (L2 reuse of the
+  // neighbour gathers).  Same mapping in both phases.
+  const int nFull = m.n / cstep;
+  int tailC;
+  {
+    const int base = nFull * cstep, R = m.n - base, per = (R + (int)gridDim.x - 1) / (int)gridDim.x;
+    const int off = (int)blockIdx.x * per + (int)threadIdx.x;
+    tailC = ((int)threadIdx.x < per && off < R) ? base + off : -1;
+  }
 #endif
 #if LF_TIMING
   unsigned long long tprev = 0, tacc[4] = {0, 0, 0, 0};
@@ -959,7 +977,13 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
     // ---- phase 1: flush psi, p = w + beta p_old, q = A p, sums
     double v1[2] = {0.0, 0.0};
     LF_TSTAMP(0);
+#if LF_TAIL
+    for (int i = 0; i <= nFull; ++i) {
+      const int c = i < nFull ? cstart + i * cstep : tailC;
+      if (c < 0) break;
+#else
     for (int c = cstart; c < cend; c += cstep) {
+#endif
       double ps = psi[c];
       if (!first) {
         ps = fma(alpha, pold[c], ps);
@@ -992,20 +1016,21 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
     double v2[2] = {0.0, 0.0};
     {
       constexpr int U = LF_P2P_UNROLL;  // cells per trip, loads issued first
-      for (int c0 = cstart; c0 < cend; c0 += cstep * U) {
+      // U cells (c < 0: none): all loads first, then r, w and the sums
+      auto p2cells = [&](const int (&cs)[U]) {
         double q[U], r[U], d[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const int c = c0 + u * cstep;
-          const bool ok = c < cend;
+          const int c = cs[u];
+          const bool ok = c >= 0;
           q[u] = ok ? ws.q[c] : 0.0;
           r[u] = ok ? ws.r[c] : 0.0;
           d[u] = ok ? a.diag[c] : 1.0;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const int c = c0 + u * cstep;
-          if (c < cend) {
+          const int c = cs[u];
+          if (c >= 0) {
             const double rn = fma(-alpha2, q[u], r[u]);
             const double wc = (1.0 / d[u]) * rn;
             ws.r[c] = rn;
@@ -1015,7 +1040,25 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
             v2[1] = fma(wc, rn, v2[1]);
           }
         }
+      };
+#if LF_TAIL
+      for (int i = 0; i <= nFull; i += U) {
+        int cs[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int ii = i + u;
+          cs[u] = ii < nFull ? cstart + ii * cstep : (ii == nFull ? tailC : -1);
+        }
+        p2cells(cs);
       }
+#else
+      for (int c0 = cstart; c0 < cend; c0 += cstep * U) {
+        int cs[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) cs[u] = c0 + u * cstep < cend ? c0 + u * cstep : -1;
+        p2cells(cs);
+      }
+#endif
     }
     LF_TSTAMP(3);
     grid_reduce_sync<2>(v2, ws.partials, bar, ws.gsum->p2, ws.p2p LF_DBG_ARG(2 * k + 1));

@@ -194,6 +194,7 @@ void launch_phase2(cudaStream_t s, const Launch &L, const MeshDev &m, const LduD
 void launch_amul(cudaStream_t s, const Launch &L, const MeshDev &m, const LduDev &a,
                  const double *halo, const double *x, double *y);
 int persistent_grid(int device, int K);
+bool persistent_tail();  // LF_TAIL: SM-uniform grid, evenly spread tail trip
 bool persistent_chunked();
 void launch_pcg_persistent(cudaStream_t s, int grid, const MeshDev &m, const LduDev &a,
                            const Workspace &ws, unsigned *bar);

@@ -521,6 +521,8 @@ static void build_mesh(lf_context *ctx, const lf_mesh_desc *d, lf_mesh *M) {
   // holds the same number of blocks), or balanced grid-stride trips
   M->persistentGrid = persistent_chunked()
                           ? std::max(1, std::min(persistent_grid(ctx->device, md.K), (int)((n + 31) / 32)))
+                      : persistent_tail()
+                          ? std::max(1, std::min(persistent_grid(ctx->device, md.K), (int)((n + BSZ - 1) / BSZ)))
                           : balanced(persistent_grid(ctx->device, md.K));
   int maxGrid = std::max({M->Lasm.grid, M->Lp1.grid, M->Lp2.grid, M->Lamul.grid, M->Lsetup.grid, M->Lsum.grid,
                           M->persistentGrid});

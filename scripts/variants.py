@@ -14,10 +14,8 @@ sys.path.insert(0, ROOT)
 
 # name -> (-D defines, bench --mode[, bench --precond])
 VARIANTS = {
-    "barall": ([], "persistent"),
-    "barlast": (["LF_BAR_ALL=0"], "persistent"),
-    "dic_barall": ([], "persistent", "DIC"),
-    "dic_barlast": (["LF_BAR_ALL=0"], "persistent", "DIC"),
+    "tail": ([], "persistent"),
+    "notail": (["LF_TAIL=0"], "persistent"),
 }
 
 
