@@ -24,9 +24,30 @@
 // Row layout: full-row ELL (DicDev / LduDev.symU), every access coalesced;
 // coefficients written by the assembly kernel.
 
+#ifndef LF_DIC_TAIL
+#define LF_DIC_TAIL 0    // 1: level passes and the Amul phase spread the tail trip (r2e:
+#endif                   // neutral at 200^3, -2% at 100^3 -> off)
 #ifndef LF_DIC_PAIR
 #define LF_DIC_PAIR 0    // 1: phase 1 interleaves the two colours (thread t: cell t of each).
 #endif                   // r1x: 100^3 3.37 vs 3.13 ms/step, 200^3 39.2 vs 39.9 -> off
+
+// Grid-stride loop over [t0, t1) with the evenly spread tail trip of the
+// persistent kernels (LF_TAIL): full trips while every thread has an index,
+// then the leftover indices split into equal consecutive runs per block.
+template <class F>
+__device__ __forceinline__ void grid_range(int t0, int t1, F body) {
+  const int S = gridDim.x * blockDim.x, len = t1 - t0;
+  const int first = t0 + (int)(blockIdx.x * blockDim.x + threadIdx.x);
+#if LF_TAIL && LF_DIC_TAIL
+  const int nFull = len / S;
+  for (int i = 0; i < nFull; ++i) body(first + i * S);
+  const int R = len - nFull * S, per = (R + (int)gridDim.x - 1) / (int)gridDim.x;
+  const int off = (int)blockIdx.x * per + (int)threadIdx.x;
+  if ((int)threadIdx.x < per && off < R) body(t0 + nFull * S + off);
+#else
+  for (int t = first; t < t1; t += S) body(t);
+#endif
+}
 
 template <int KS>
 struct SymRow {
@@ -137,12 +158,10 @@ template <int KS, bool HALO>
 __device__ __forceinline__ void dic_apply(const MeshDev &m, const DicDev &d, const LduDev &a, double *r,
                                           const double *q, double *w, bool upd, double alpha, unsigned *bar,
                                           double *partials, double *out, const P2PDev &pp) {
-  const int gtid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
   const int L = d.L;
   double v[2] = {0.0, 0.0};
   for (int l = 1; l < L; ++l) {
-    const int t1 = __ldg(d.lvlStart + l + 1);
-    for (int t = __ldg(d.lvlStart + l) + gtid; t < t1; t += stride) {
+    grid_range(__ldg(d.lvlStart + l), __ldg(d.lvlStart + l + 1), [&](int t) {
       const int c = level_cell(d, t);
       double wc;
       const double rc = dic_forward_cell<KS>(d, a, c, r, q, w, upd, alpha, wc);
@@ -151,19 +170,18 @@ __device__ __forceinline__ void dic_apply(const MeshDev &m, const DicDev &d, con
         v[1] = fma(wc, rc, v[1]);
         if (HALO && pp.P > 0) push_halo(m, pp.dstW, c, wc);
       }
-    }
+    });
     grid_barrier(bar);
   }
   for (int l = L >= 2 ? L - 2 : 0; l >= 0; --l) {
-    const int t1 = __ldg(d.lvlStart + l + 1);
-    for (int t = __ldg(d.lvlStart + l) + gtid; t < t1; t += stride) {
+    grid_range(__ldg(d.lvlStart + l), __ldg(d.lvlStart + l + 1), [&](int t) {
       const int c = level_cell(d, t);
       double wc;
       const double rc = dic_backward_cell<KS>(d, a, c, l == 0, r, q, w, upd, alpha, wc);
       if (l == 0) v[0] += fabs(rc);
       v[1] = fma(wc, rc, v[1]);
       if (HALO && pp.P > 0) push_halo(m, pp.dstW, c, wc);
-    }
+    });
     if (l > 0) grid_barrier(bar);
   }
   grid_reduce_sync<2>(v, partials, bar, out, pp LF_DBG_ARG(0));
@@ -251,14 +269,13 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
     // diag of level-0 cells), then one pass per level
     for (int l = 0; l < L; ++l) {
       if (l >= 2) grid_barrier(bar);
-      const int t1 = __ldg(d.lvlStart + l + 1);
-      for (int t = __ldg(d.lvlStart + l) + gtid; t < t1; t += stride) {
+      grid_range(__ldg(d.lvlStart + l), __ldg(d.lvlStart + l + 1), [&](int t) {
         const int c = level_cell(d, t);
         if (l == 0)
           d.rD[c] = __ddiv_rn(1.0, a.diag[c]);
         else
           dic_factor_cell<KS>(d, a, c);
-      }
+      });
     }
     grid_barrier(bar);
     dic_apply<KS, HALO>(m, d, a, r, q, w, false, 0.0, bar, ws.partials, ws.gsum->p2, pp);  // set-up w
@@ -295,8 +312,9 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
           dic_amul_cell<KS, HALO>(m, a, d, ws, k, n0 + t, first, cont, alpha, beta, psi, w, pold, pnew, q, v1);
       }
     } else {
-      for (int c = gtid; c < m.n; c += stride)
+      grid_range(0, m.n, [&](int c) {
         dic_amul_cell<KS, HALO>(m, a, d, ws, k, c, first, cont, alpha, beta, psi, w, pold, pnew, q, v1);
+      });
     }
     grid_reduce_sync<2>(v1, ws.partials, bar, ws.gsum->p1, pp LF_DBG_ARG(0));
     if (!cont) break;

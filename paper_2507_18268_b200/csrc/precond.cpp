@@ -85,7 +85,9 @@ void ensure_dic(lf_mesh *M) {
     d.rD = A.alloc<double>(n);
     d.rDu = A.alloc<double>(n);
     M->hLvlStart = lstart;
-    M->dicGrid = balanced_grid(n, dic_grid(M->ctx->device, KS));
+    M->dicGrid = persistent_tail()  // SM-uniform grid: the passes spread their tail trips
+                     ? std::max(1, std::min(dic_grid(M->ctx->device, KS), (n + kernel_block_size() - 1) / kernel_block_size()))
+                     : balanced_grid(n, dic_grid(M->ctx->device, KS));
     if (M->dicGrid > M->ws.maxGrid) {  // partials sized for the largest grid
       M->ws.partials = A.alloc<double>(4 * (size_t)M->dicGrid);
       M->ws.maxGrid = M->dicGrid;

@@ -14,8 +14,9 @@ sys.path.insert(0, ROOT)
 
 # name -> (-D defines, bench --mode[, bench --precond])
 VARIANTS = {
+    "dic_tail": ([], "persistent", "DIC"),
+    "dic_notail": (["LF_DIC_TAIL=0"], "persistent", "DIC"),
     "tail": ([], "persistent"),
-    "notail": (["LF_TAIL=0"], "persistent"),
 }
 
 
