@@ -154,10 +154,11 @@ __device__ __forceinline__ int level_cell(const DicDev &d, int t) { return d.con
 // processor faces is stored into the neighbour ranks' recvW (peer memory),
 // ordered before the reduction's cross-rank exchange; the factor and the
 // sweeps themselves are processor-local, as OpenFOAM's DIC (reading A42).
-template <int KS, bool HALO>
+template <int KS, bool HALO, class Idle = NoIdle>
 __device__ __forceinline__ void dic_apply(const MeshDev &m, const DicDev &d, const LduDev &a, double *r,
                                           const double *q, double *w, bool upd, double alpha, unsigned *bar,
-                                          double *partials, double *out, const P2PDev &pp) {
+                                          double *partials, double *out, const P2PDev &pp,
+                                          Idle idle = Idle()) {
   const int L = d.L;
   double v[2] = {0.0, 0.0};
   for (int l = 1; l < L; ++l) {
@@ -184,7 +185,7 @@ __device__ __forceinline__ void dic_apply(const MeshDev &m, const DicDev &d, con
     });
     if (l > 0) grid_barrier(bar);
   }
-  grid_reduce_sync<2>(v, partials, bar, out, pp LF_DBG_ARG(0));
+  grid_reduce_sync<2>(v, partials, bar, out, pp LF_DBG_ARG(0), idle);
 }
 
 // Phase-1 work of one cell in the DIC solve: deferred psi update, p = w +
@@ -195,13 +196,18 @@ template <int KS, bool HALO>
 __device__ __forceinline__ void dic_amul_cell(const MeshDev &m, const LduDev &a, const DicDev &d,
                                               const Workspace &ws, int k, int c, bool first, bool cont,
                                               double alpha, double beta, double *psi, const double *w,
-                                              const double *pold, double *pnew, double *q, double (&v1)[2]) {
-  double ps = psi[c];
-  if (!first) {
-    ps = fma(alpha, pold[c], ps);
-    psi[c] = ps;
+                                              const double *pold, double *pnew, double *q, double (&v1)[2],
+                                              bool idleF) {
+  if (idleF) {  // psi was updated in the previous beta-barrier wait
+    if (first) v1[1] += psi[c];
+  } else {
+    double ps = psi[c];
+    if (!first) {
+      ps = fma(alpha, pold[c], ps);
+      psi[c] = ps;
+    }
+    v1[1] += ps;
   }
-  v1[1] += ps;
   if (cont) {
     SymRow<KS> R;
     load_row<KS>(d, a, c, R);
@@ -232,7 +238,7 @@ __device__ __forceinline__ void dic_amul_cell(const MeshDev &m, const LduDev &a,
 // HALO: processor patches through the peer-memory transport (halo w puts in
 // the sweeps, halo p recomputed in the Amul phase, rank-ordered mailbox
 // allreduce in the two reducing barriers), as k_pcg_persistent<.., true>.
-template <int KS, bool HALO>
+template <int KS, bool HALO, bool IDLE = false>
 __global__ void __launch_bounds__(BS, LF_MINB_P)
     k_pcg_dic(MeshDev m, LduDev a, DicDev d, Workspace ws, unsigned *bar) {
   PcgCtl *ctl = ws.ctl;
@@ -246,6 +252,8 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
   const int L = d.L;
   const bool pair = LF_DIC_PAIR && d.contig && L == 2;  // two contiguous colours: interleave in phase 1
+  const bool idleF = IDLE && !pair;  // psi flush in the beta-barrier wait (Workspace.idleFlush)
+  double psiSum = 0.0;
   double *psi = ctl->psi;
   double *r = ws.r, *w = ws.w, *q = ws.q;
 
@@ -304,16 +312,19 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
     // cell t of each colour together (LF_DIC_PAIR), so a cell's gathers hit
     // the lines its partner-colour neighbours just read.
     double v1[2] = {0.0, 0.0};
+    if (idleF) v1[1] = psiSum;
     if (pair) {
       const int n0 = __ldg(d.lvlStart + 1), n1 = m.n - n0, nt = max(n0, n1);
       for (int t = gtid; t < nt; t += stride) {
-        if (t < n0) dic_amul_cell<KS, HALO>(m, a, d, ws, k, t, first, cont, alpha, beta, psi, w, pold, pnew, q, v1);
+        if (t < n0)
+          dic_amul_cell<KS, HALO>(m, a, d, ws, k, t, first, cont, alpha, beta, psi, w, pold, pnew, q, v1, false);
         if (t < n1)
-          dic_amul_cell<KS, HALO>(m, a, d, ws, k, n0 + t, first, cont, alpha, beta, psi, w, pold, pnew, q, v1);
+          dic_amul_cell<KS, HALO>(m, a, d, ws, k, n0 + t, first, cont, alpha, beta, psi, w, pold, pnew, q, v1,
+                                  false);
       }
     } else {
       grid_range(0, m.n, [&](int c) {
-        dic_amul_cell<KS, HALO>(m, a, d, ws, k, c, first, cont, alpha, beta, psi, w, pold, pnew, q, v1);
+        dic_amul_cell<KS, HALO>(m, a, d, ws, k, c, first, cont, alpha, beta, psi, w, pold, pnew, q, v1, idleF);
       });
     }
     grid_reduce_sync<2>(v1, ws.partials, bar, ws.gsum->p1, pp LF_DBG_ARG(0));
@@ -326,7 +337,19 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
     __syncthreads();
     if (st.singular) break;
     // ---- r -= alpha q, w = M^-1 r, sum|r|, sum w.r
-    dic_apply<KS, HALO>(m, d, a, r, q, w, true, st.alpha, bar, ws.partials, ws.gsum->p2, pp);
+    // idleF: psi += alpha_k p_k for this thread's phase-1 cells while the
+    // block waits for beta (as k_pcg_persistent)
+    psiSum = 0.0;
+    const double alphaK = st.alpha;
+    auto flush = [&]() {
+      if (!idleF) return;
+      grid_range(0, m.n, [&](int c) {
+        const double ps = fma(alphaK, pnew[c], psi[c]);
+        psi[c] = ps;
+        psiSum += ps;
+      });
+    };
+    dic_apply<KS, HALO>(m, d, a, r, q, w, true, alphaK, bar, ws.partials, ws.gsum->p2, pp, flush);
     if (threadIdx.x == 0) ++st.k;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -342,15 +365,15 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
   }
 }
 
-template <bool HALO>
+template <bool HALO, bool IDLE = false>
 static const void *dic_fn(int KS) {
-  return KS <= 6 ? (const void *)k_pcg_dic<6, HALO> : (const void *)k_pcg_dic<8, HALO>;
+  return KS <= 6 ? (const void *)k_pcg_dic<6, HALO, IDLE> : (const void *)k_pcg_dic<8, HALO, IDLE>;
 }
 
 int dic_grid(int device, int KS) {
   int sms = 0, best = 1 << 30;
   LF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-  for (const void *fn : {dic_fn<false>(KS), dic_fn<true>(KS)}) {  // co-resident for both variants
+  for (const void *fn : {dic_fn<false>(KS), dic_fn<true>(KS), dic_fn<false, true>(KS)}) {  // co-resident for all
     int nb = 0;
     LF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, BS, 0));
     best = std::min(best, nb);
@@ -362,8 +385,10 @@ void launch_pcg_dic(cudaStream_t s, int grid, const MeshDev &m, const LduDev &a,
                     const Workspace &ws, unsigned *bar) {
   void *args[] = {(void *)&m, (void *)&a, (void *)&d, (void *)&ws, (void *)&bar};
   const bool halo = m.hasProc || ws.p2p.P > 0;
-  LF_CUDA(cudaLaunchCooperativeKernel(halo ? dic_fn<true>(d.KS) : dic_fn<false>(d.KS), dim3(grid), dim3(BS), args,
-                                      0, s));
+  const void *fn = halo                              ? dic_fn<true>(d.KS)
+                   : (LF_IDLE_FLUSH && ws.idleFlush) ? dic_fn<false, true>(d.KS)
+                                                     : dic_fn<false>(d.KS);
+  LF_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(BS), args, 0, s));
 }
 
 // ------------------------------------------- full-row coefficients (fill)

@@ -745,20 +745,27 @@ __device__ int g_dbg_last[LF_DBG_N];
 __device__ int g_dbg_i_dummy;
 #define g_dbg_i dbg_i
 #endif
-template <int NV>
+// `idle` (all threads of a block) runs while the block waits for the
+// release — after its arrival, or after the release in the last arriving
+// block — so independent work fills the barrier's sync latency.
+struct NoIdle {
+  __device__ void operator()() const {}
+};
+template <int NV, class Idle = NoIdle>
 __device__ void grid_reduce_sync(double (&v)[NV], double *partials, unsigned *bar, double *out,
                                  const P2PDev &P
 #if LF_TIMING
                                  , int dbg_i
 #endif
-                                 ) {
+                                 , Idle idle = Idle()) {
   __shared__ double sm[NV][32];
   __shared__ int amLast;
   block_sum<NV>(v, sm);
+  unsigned gen = 0;  // thread 0: barrier generation before arriving
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int k = 0; k < NV; ++k) partials[k * gridDim.x + blockIdx.x] = v[k];
-    const unsigned gen = ld_acquire(bar + 1);  // read before arriving: cannot move until we arrive
+    gen = ld_acquire(bar + 1);  // read before arriving: cannot move until we arrive
 #if LF_TIMING
     if (g_dbg_i < LF_DBG_N && blockIdx.x < LF_DBG_G) g_dbg_arr[g_dbg_i][blockIdx.x] = gtime_ns();
 #endif
@@ -777,7 +784,11 @@ __device__ void grid_reduce_sync(double (&v)[NV], double *partials, unsigned *ba
 #endif
     }
     amLast = (t == gridDim.x - 1);
-    if (!amLast) {
+  }
+  __syncthreads();
+  if (!amLast) idle();
+  if (!amLast && threadIdx.x == 0) {
+    {
       // ld.acquire.gpu orders the later loads and invalidates this SM's L1
       // (SASS CCTL.IVALL), so cached loads of other blocks' data are coherent
       const unsigned long long t0 = gtime_ns();
@@ -833,6 +844,8 @@ __device__ void grid_reduce_sync(double (&v)[NV], double *partials, unsigned *ba
 #endif
     }
     __syncthreads();
+    idle();  // the last arriver's own idle work, after releasing the others
+    __syncthreads();
   }
 }
 
@@ -873,6 +886,9 @@ __device__ __forceinline__ void grid_barrier(unsigned *bar) {
 #define LF_CHUNKED 0  // persistent kernel: contiguous cell chunk per block (vs grid stride).
 #endif                // r1n: chunks raise the phase-1 arrival spread 6 -> 28 us at 100^3 -> off
 bool persistent_chunked() { return LF_CHUNKED != 0; }
+#ifndef LF_IDLE_FLUSH
+#define LF_IDLE_FLUSH 1  // persistent kernel may do psi += alpha p while waiting at the beta
+#endif                   // barrier (Workspace.idleFlush, set per mesh: L2-resident sizes)
 #ifndef LF_TAIL
 #define LF_TAIL 1  // persistent kernel: spread the last partial trip over all blocks
 #endif
@@ -883,7 +899,7 @@ bool persistent_tail() { return LF_TAIL != 0; }
 // HALO = false: single rank without processor patches — the interface
 // term, halo puts and peer allreduce are compiled out of the hot loop
 // (they cost 13% at 100^3 even when branched around, r1o).
-template <int KE, bool HALO>
+template <int KE, bool HALO, bool IDLE = false>
 __global__ void __launch_bounds__(BS, LF_MINB_P)
     k_pcg_persistent(MeshDev m, LduDev a, Workspace ws, unsigned *bar) {
   PcgCtl *ctl = ws.ctl;
@@ -907,6 +923,7 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
   }
   double *psi = ctl->psi;
   const double *__restrict__ w = ws.w;
+  double psiSum = 0.0;  // LF_IDLE_FLUSH: this thread's sum of psi after its last flush
 #if LF_CHUNKED
   // block b owns the contiguous cells [b*C, (b+1)*C): equal work per block on
   // an SM-uniform grid (numSMs x blocks/SM), the same cells in both phases
@@ -977,6 +994,8 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
     // ---- phase 1: flush psi, p = w + beta p_old, q = A p, sums
     double v1[2] = {0.0, 0.0};
     LF_TSTAMP(0);
+    constexpr bool idleF = IDLE;  // psi flush in the beta-barrier wait (Workspace.idleFlush)
+    if (idleF) v1[1] = psiSum;  // sum psi after the flush done in the previous barrier's wait
 #if LF_TAIL
     for (int i = 0; i <= nFull; ++i) {
       const int c = i < nFull ? cstart + i * cstep : tailC;
@@ -984,12 +1003,16 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
 #else
     for (int c = cstart; c < cend; c += cstep) {
 #endif
-      double ps = psi[c];
-      if (!first) {
-        ps = fma(alpha, pold[c], ps);
-        psi[c] = ps;
+      if (idleF) {
+        if (first) v1[1] += psi[c];
+      } else {
+        double ps = psi[c];
+        if (!first) {
+          ps = fma(alpha, pold[c], ps);
+          psi[c] = ps;
+        }
+        v1[1] += ps;
       }
-      v1[1] += ps;
       if (cont) {
         const double pc = first ? w[c] : fma(beta, pold[c], w[c]);
         pnew[c] = pc;
@@ -1061,7 +1084,27 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
 #endif
     }
     LF_TSTAMP(3);
-    grid_reduce_sync<2>(v2, ws.partials, bar, ws.gsum->p2, ws.p2p LF_DBG_ARG(2 * k + 1));
+    // idleF: psi += alpha_k p_k for this thread's cells (p_k written by this
+    // thread in phase 1) while the block waits for beta — fills the barrier
+    // latency and takes the psi stream out of phase 1, at the price of
+    // re-reading p (8n).  OpenFOAM's order is kept (the update follows the
+    // singularity check of the same iteration).
+    psiSum = 0.0;
+    auto flush = [&]() {
+      if (!idleF) return;
+#if LF_TAIL
+      for (int i = 0; i <= nFull; ++i) {
+        const int c = i < nFull ? cstart + i * cstep : tailC;
+        if (c < 0) break;
+#else
+      for (int c = cstart; c < cend; c += cstep) {
+#endif
+        const double ps = fma(alpha2, pnew[c], psi[c]);
+        psi[c] = ps;
+        psiSum += ps;
+      }
+    };
+    grid_reduce_sync<2>(v2, ws.partials, bar, ws.gsum->p2, ws.p2p LF_DBG_ARG(2 * k + 1), flush);
     LF_TSTAMP(4);
     if (threadIdx.x == 0) ++st.k;
   }
@@ -1121,10 +1164,13 @@ int persistent_grid(int device, int K) {
   int sms = 0, nb = 0;
   LF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
   // the grid must be co-resident for every variant that may be launched
-  const void *fns[2] = {K == 4 ? (const void *)k_pcg_persistent<4, false>
+  const void *fns[3] = {K == 4 ? (const void *)k_pcg_persistent<4, false>
                                : (K > 0 ? (const void *)k_pcg_persistent<3, false> : (const void *)k_pcg_persistent<0, false>),
                         K == 4 ? (const void *)k_pcg_persistent<4, true>
-                               : (K > 0 ? (const void *)k_pcg_persistent<3, true> : (const void *)k_pcg_persistent<0, true>)};
+                               : (K > 0 ? (const void *)k_pcg_persistent<3, true> : (const void *)k_pcg_persistent<0, true>),
+                        K == 4 ? (const void *)k_pcg_persistent<4, false, true>
+                               : (K > 0 ? (const void *)k_pcg_persistent<3, false, true>
+                                        : (const void *)k_pcg_persistent<0, false, true>)};
   int best = 1 << 30;
   for (const void *fn : fns) {
     LF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, BS, 0));
@@ -1133,18 +1179,20 @@ int persistent_grid(int device, int K) {
   return sms * (best < 1 ? 1 : best);
 }
 
-template <bool HALO>
+template <bool HALO, bool IDLE = false>
 static const void *persistent_fn(const MeshDev &m) {
-  return (!LF_NO_ELL && m.K == 4) ? (const void *)k_pcg_persistent<4, HALO>
-         : (!LF_NO_ELL && m.K > 0) ? (const void *)k_pcg_persistent<3, HALO>
-                                   : (const void *)k_pcg_persistent<0, HALO>;
+  return (!LF_NO_ELL && m.K == 4) ? (const void *)k_pcg_persistent<4, HALO, IDLE>
+         : (!LF_NO_ELL && m.K > 0) ? (const void *)k_pcg_persistent<3, HALO, IDLE>
+                                   : (const void *)k_pcg_persistent<0, HALO, IDLE>;
 }
 
 void launch_pcg_persistent(cudaStream_t s, int grid, const MeshDev &m, const LduDev &a,
                            const Workspace &ws, unsigned *bar) {
   const bool halo = m.hasProc || ws.p2p.P > 0;
   void *args[] = {(void *)&m, (void *)&a, (void *)&ws, (void *)&bar};
-  const void *fn = halo ? persistent_fn<true>(m) : persistent_fn<false>(m);
+  const void *fn = halo                                 ? persistent_fn<true>(m)
+                   : (LF_IDLE_FLUSH && ws.idleFlush)    ? persistent_fn<false, true>(m)
+                                                        : persistent_fn<false>(m);
   LF_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(BS), args, 0, s));
 }
 

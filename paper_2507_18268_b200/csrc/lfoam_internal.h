@@ -152,6 +152,7 @@ struct Workspace {
   double *pH[2];        // p at the halo slots, recomputed locally (double-buffered like p)
   int32_t *sendCell;    // [n_proc] local cell of each send slot
   int maxGrid;
+  int idleFlush;        // persistent solve: psi flush in the beta-barrier wait (see mesh.cpp)
   P2PDev p2p;
 };
 

@@ -530,6 +530,16 @@ static void build_mesh(lf_context *ctx, const lf_mesh_desc *d, lf_mesh *M) {
   LF_CUDA(cudaMemsetAsync(M->gridBar, 0, 2 * sizeof(unsigned), s));
   Workspace &ws = M->ws;
   ws.maxGrid = maxGrid;
+  // Moving psi += alpha p into the wait of the beta barrier hides it in the
+  // barrier latency but re-reads p: a win while an iteration's working set
+  // (~96n + 16F bytes) is within ~1.5x the L2 — latency-bound sizes (r2h:
+  // 100^3 -4.8% time) — and a loss once HBM-bound (200^3 +3.4%).
+  {
+    int l2 = 0;
+    LF_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, ctx->device));
+    const double bytesIter = 96.0 * n + 16.0 * F;
+    ws.idleFlush = bytesIter <= 1.5 * (double)l2 ? 1 : 0;
+  }
   ws.r = A.alloc<double>(n);
   ws.w = A.alloc<double>(n);
   ws.q = A.alloc<double>(n);

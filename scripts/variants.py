@@ -14,9 +14,10 @@ sys.path.insert(0, ROOT)
 
 # name -> (-D defines, bench --mode[, bench --precond])
 VARIANTS = {
-    "dic_tail": ([], "persistent", "DIC"),
-    "dic_notail": (["LF_DIC_TAIL=0"], "persistent", "DIC"),
-    "tail": ([], "persistent"),
+    "idle": ([], "persistent"),
+    "noidle": (["LF_IDLE_FLUSH=0"], "persistent"),
+    "dic_idle": ([], "persistent", "DIC"),
+    "dic_noidle": (["LF_IDLE_FLUSH=0"], "persistent", "DIC"),
 }
 
 
