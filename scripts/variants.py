@@ -14,10 +14,8 @@ sys.path.insert(0, ROOT)
 
 # name -> (-D defines, bench --mode[, bench --precond])
 VARIANTS = {
-    "idle": ([], "persistent"),
-    "noidle": (["LF_IDLE_FLUSH=0"], "persistent"),
-    "dic_idle": ([], "persistent", "DIC"),
-    "dic_noidle": (["LF_IDLE_FLUSH=0"], "persistent", "DIC"),
+    "base": ([], "persistent"),
+    "lou": (["LF_LOU=1"], "persistent"),
 }
 
 
