@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--precond", default="diagonal", choices=["diagonal", "DIC"],
                     help="PCG preconditioner: the paper's diagonal (P:608), or SURVEY §8(f) row 3's DIC "
                          "(level-scheduled sweeps; 2 levels under the multicolour numbering)")
+    ap.add_argument("--variant", type=int, default=0,
+                    help="persistent solve variant: 0 by mesh size, 1 L2-resident, 2 HBM-bound")
     ap.add_argument("--mode", default="persistent", choices=["persistent", "graphs", "direct"],
                     help="PCG loop execution (single rank): one cooperative launch per solve, "
                          "CUDA-graph replays of per-phase launches, or direct launches")
@@ -245,6 +247,7 @@ def run_ours(args):
     ctx = P.Context(device, stream=stream)
     ctx.set_option("persistent", args.mode == "persistent")
     ctx.set_option("graphs", args.mode != "direct")
+    ctx.set_option("variant", args.variant)
 
     cfg = args.config
     wname = workload_name(cfg, args.corrected, args.dt_field, args.precond)
@@ -409,6 +412,7 @@ def run_ours(args):
         "config": {"workload": wname, "n_cells": n_global, "steps_per_run": args.steps,
                    "global_batch": 1, "seq_len": 0, "parallelism": "1gpu" if ws == 1 else f"domain{ws}-{args.transport}",
                    "renumber": args.renumber, "mode": args.mode, "precond": args.precond,
+                   "variant": args.variant,
                    "l2": "flushed between timed steps (256 MiB write)", "tol": TOL,
                    "pcg_iterations_per_step": {"min": min(its), "max": max(its), "mean": sum(its) / len(its)}},
         "roofline": {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": peak,

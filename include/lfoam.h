@@ -316,14 +316,20 @@ typedef enum {
   LF_K_COUNT = 11
 } lf_kernel_kind;
 
-/* Execution options of a context (all default 1):
- *   LF_OPT_PERSISTENT  single-rank meshes without processor patches run the
- *                      whole PCG loop as ONE cooperative launch (grid
- *                      barriers between the phases); 0 = one launch per phase
- *   LF_OPT_GRAPHS      phase launches are replayed from CUDA graphs of 2^i
- *                      iterations; 0 = direct launches
- * Results are identical up to reduction grid size (both are deterministic). */
-typedef enum { LF_OPT_PERSISTENT = 0, LF_OPT_GRAPHS = 1 } lf_option;
+/* Execution options of a context:
+ *   LF_OPT_PERSISTENT  (default 1) single-rank meshes without processor
+ *                      patches run the whole PCG loop as ONE cooperative
+ *                      launch (grid barriers between the phases); 0 = one
+ *                      launch per phase
+ *   LF_OPT_GRAPHS      (default 1) phase launches are replayed from CUDA
+ *                      graphs of 2^i iterations; 0 = direct launches
+ *   LF_OPT_SOLVE_VARIANT (default 0 = by mesh size) persistent single-rank
+ *                      solve variant: 1 the L2-resident one (psi update in
+ *                      the beta-barrier wait), 2 the HBM-bound one (psi update
+ *                      deferred into the Amul phase); mesh_create picks 1 when
+ *                      an iteration's working set fits ~1.5x the L2, else 2
+ * Results are identical up to reduction grid size (all are deterministic). */
+typedef enum { LF_OPT_PERSISTENT = 0, LF_OPT_GRAPHS = 1, LF_OPT_SOLVE_VARIANT = 2 } lf_option;
 LF_API lf_status lf_set_option(lf_context *ctx, lf_option opt, int value);
 
 /* enable != 0: bracket every launch of the hot kernels with CUDA events on

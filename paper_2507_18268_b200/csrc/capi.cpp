@@ -519,6 +519,10 @@ lf_status lf_set_option(lf_context *ctx, lf_option opt, int value) {
       ctx->persistent = value != 0;
     else if (opt == LF_OPT_GRAPHS)
       ctx->useGraphs = value != 0;
+    else if (opt == LF_OPT_SOLVE_VARIANT) {
+      LF_REQUIRE(value >= 0 && value <= 2, "solve variant must be 0, 1 or 2");
+      ctx->solveVariant = value;
+    }
     else
       throw Error{LF_ERR_INVALID_ARG, "unknown option"};
   });

@@ -38,6 +38,7 @@ struct lf_context {
   bool capturing = false;  // stream capture in progress: no events, no counting
   bool useGraphs = true;   // replay iteration chunks as CUDA graphs
   bool persistent = true;  // single-rank, no processor patches: one cooperative launch per solve
+  int solveVariant = 0;    // LF_OPT_SOLVE_VARIANT: 0 by mesh size, 1 L2-resident, 2 HBM-bound
   struct Pending {
     int kind;
     cudaEvent_t a, b;
@@ -97,6 +98,7 @@ struct lf_mesh {
   cudaGraphExec_t chunkGraph[kMaxGraphLog] = {};
   int kernelsPerIteration = 0;
   int persistentGrid = 0;     // co-resident grid of k_pcg_persistent
+  bool l2Resident = false;    // an iteration's working set fits ~1.5x the L2 (mesh.cpp)
   unsigned *gridBar = nullptr;  // device {count, generation}
   // peer-memory transport: one IPC-exportable block [flags | vals | recvT | recvW]
   char *p2pBlock = nullptr;

@@ -538,7 +538,8 @@ static void build_mesh(lf_context *ctx, const lf_mesh_desc *d, lf_mesh *M) {
     int l2 = 0;
     LF_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, ctx->device));
     const double bytesIter = 96.0 * n + 16.0 * F;
-    ws.idleFlush = bytesIter <= 1.5 * (double)l2 ? 1 : 0;
+    M->l2Resident = bytesIter <= 1.5 * (double)l2;
+    ws.idleFlush = M->l2Resident ? 1 : 0;
   }
   ws.r = A.alloc<double>(n);
   ws.w = A.alloc<double>(n);

@@ -29,7 +29,7 @@ KERNELS = {"assemble": 0, "setup": 1, "phase1": 2, "phase2": 3, "amul": 4, "sump
 PRECONDITIONERS = {"diagonal": 0, "DIC": 1, "DILU": 2}
 # lf_mesh_desc.renumber
 RENUMBER = {False: 0, True: 1, 0: 0, 1: 1, 2: 2, "none": 0, "rcm": 1, "colour": 2}
-OPTIONS = {"persistent": 0, "graphs": 1}
+OPTIONS = {"persistent": 0, "graphs": 1, "variant": 2}
 
 
 class LfoamError(RuntimeError):
@@ -196,8 +196,9 @@ class Context:
         _check(lib().lf_comm_info(self.h, C.byref(n), C.byref(r)))
         return n.value, r.value
 
-    def set_option(self, name: str, value: bool):
-        _check(lib().lf_set_option(self.h, OPTIONS[name], 1 if value else 0))
+    def set_option(self, name: str, value):
+        """persistent / graphs: bool; variant: 0 auto, 1 L2-resident, 2 HBM-bound."""
+        _check(lib().lf_set_option(self.h, OPTIONS[name], int(value)))
 
     def set_instrumentation(self, on: bool):
         _check(lib().lf_set_instrumentation(self.h, 1 if on else 0))

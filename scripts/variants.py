@@ -14,8 +14,9 @@ sys.path.insert(0, ROOT)
 
 # name -> (-D defines, bench --mode[, bench --precond])
 VARIANTS = {
-    "base": ([], "persistent"),
-    "lou": (["LF_LOU=1"], "persistent"),
+    "auto": ([], "persistent"),
+    "v1_l2": ([], "persistent", "diagonal", 1),
+    "v2_hbm": ([], "persistent", "diagonal", 2),
 }
 
 
@@ -48,7 +49,8 @@ def run(cfgs, steps=10):
             env = dict(os.environ, LFOAM_LIB=lib_for(name))
             r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", str(steps), "--warmup", "3",
                                 "--config", str(cfg), "--no-cpu-baseline", "--mode", mode,
-                                "--precond", pc[0] if pc else "diagonal"],
+                                "--precond", pc[0] if pc else "diagonal",
+                                "--variant", str(pc[1] if len(pc) > 1 else 0)],
                                capture_output=True, text=True, env=env, timeout=1800)
             line = [l for l in r.stdout.splitlines() if l.startswith("{")]
             if not line:

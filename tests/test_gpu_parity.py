@@ -410,3 +410,32 @@ def test_invalid_arguments(ctx):
     with pytest.raises(P.LfoamError):
         mesh.set_T(np.zeros(5))
     mesh.close()
+
+
+@pytest.mark.parametrize("variant", [1, 2])
+@pytest.mark.parametrize("dims", [(10, 10, 10), (37, 23, 19), (7, 5, 4), (64, 32, 24)])
+def test_solve_variants(variant, dims):
+    """The persistent solve's L2-resident variant (psi update in the beta-
+    barrier wait) and HBM-bound variant (psi update deferred into the Amul
+    phase), forced on meshes of several sizes and ragged tails, against the
+    oracle."""
+    c = P.Context(0)
+    c.set_option("variant", variant)
+    m = randomise_fixed_values(meshgen.block_mesh(*dims, bc=mixed_bc()))
+    T0 = meshgen.sine_field(m)
+    To, _, po = oracle.laplacian_foam(m, T0, 4)
+    mesh = P.Mesh(c, m)
+    mesh.set_T(T0)
+    pg = mesh.step(4)
+    T = mesh.get_T()
+    assert np.max(np.abs(T - To)) <= 1e-8 * np.max(np.abs(To))
+    assert all(abs(a["n_iterations"] - b["n_iterations"]) <= 1 for a, b in zip(pg, po)), (pg, po)
+    # pcg_solve from a standalone assembly through the same variant
+    x_ref, p_ref = oracle.pcg(m, oracle.assemble(m, 1.0, 0.2, T), T)
+    ldu = mesh.assemble(1.0, 0.2)
+    psi = dev(T)
+    perf = ldu.pcg_solve(psi)
+    assert np.max(np.abs(psi.cpu().numpy() - x_ref)) <= 1e-8 * np.max(np.abs(x_ref))
+    assert abs(perf["n_iterations"] - p_ref["n_iterations"]) <= 1
+    mesh.close()
+    c.close()
