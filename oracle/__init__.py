@@ -96,6 +96,9 @@ def lib():
         _lib.orc_laplacian_foam_corrected.argtypes = [C.POINTER(_Mesh), C.c_double, C.c_double, vp, vp,
                                                       C.c_int32, C.c_int32, C.c_double, C.c_double,
                                                       C.c_int32, C.c_int32, C.POINTER(Perf)]
+        _lib.orc_laplacian_foam_corrected_p.argtypes = [C.POINTER(_Mesh), C.c_double, C.c_double, vp, vp,
+                                                        C.c_int32, C.c_int32, C.c_double, C.c_double,
+                                                        C.c_int32, C.c_int32, C.c_int32, C.POINTER(Perf)]
     return _lib
 
 
@@ -339,7 +342,7 @@ def lap_correction(mesh, DT, g):
 
 
 def laplacian_foam_corrected(mesh, T0, n_steps, n_corr=1, DT=1.0, dt=0.2, tol=1e-10, rel_tol=0.0,
-                             max_iter=1000, min_iter=0, b_value=None):
+                             max_iter=1000, min_iter=0, b_value=None, precond="diagonal"):
     """Listing 1 with Gauss linear corrected laplacian and n_corr non-orthogonal
     correctors per step.  Returns (T, b_value, [perf per corrector solve])."""
     om = _om(mesh)
@@ -347,8 +350,8 @@ def laplacian_foam_corrected(mesh, T0, n_steps, n_corr=1, DT=1.0, dt=0.2, tol=1e
     T = np.array(T0, dtype=np.float64, copy=True)
     bv = np.array(om.b_value if b_value is None else b_value, dtype=np.float64, copy=True)
     perfs = (Perf * max(n_steps * (n_corr + 1), 1))()
-    rc = lib().orc_laplacian_foam_corrected(C.byref(om.s), DT, dt, _p(T), _p(bv), n_steps, n_corr, tol,
-                                            rel_tol, max_iter, min_iter, perfs)
+    rc = lib().orc_laplacian_foam_corrected_p(C.byref(om.s), DT, dt, _p(T), _p(bv), n_steps, n_corr, tol,
+                                              rel_tol, max_iter, min_iter, PRECONDITIONERS[precond], perfs)
     if rc:
         raise MemoryError
     return T, bv, [perfs[i].as_dict() for i in range(n_steps * (n_corr + 1))]

@@ -573,9 +573,10 @@ void orc_lap_correction(const orc_mesh *m, double DT, const double *w, const dou
  * T0 (old time) for ddt, and runs n_corr + 1 passes, each assembling with
  * the explicit correction of the CURRENT T and solving from it.
  * perf: [n_steps * (n_corr + 1)]. */
-int orc_laplacian_foam_corrected(const orc_mesh *m, double DT, double dt, double *T,
-                                 double *b_value, int32_t n_steps, int32_t n_corr, double tol,
-                                 double rel_tol, int32_t max_iter, int32_t min_iter, orc_perf *perf)
+int orc_laplacian_foam_corrected_p(const orc_mesh *m, double DT, double dt, double *T,
+                                   double *b_value, int32_t n_steps, int32_t n_corr, double tol,
+                                   double rel_tol, int32_t max_iter, int32_t min_iter,
+                                   int32_t precond, orc_perf *perf)
 {
     size_t nn = (size_t)(m->n_cells > 0 ? m->n_cells : 1);
     size_t nf = (size_t)(m->n_faces > 0 ? m->n_faces : 1);
@@ -607,8 +608,8 @@ int orc_laplacian_foam_corrected(const orc_mesh *m, double DT, double dt, double
                     if (m->patch_type[p] == ORC_FIXED_VALUE)
                         for (i = m->patch_start[p]; i < m->patch_start[p + 1]; i++)
                             source[m->b_cells[i]] += b_bnd[i];
-                rc = orc_pcg(m, diag, upper, b_bnd, source, T, tol, rel_tol, max_iter, min_iter,
-                             NULL, NULL, NULL, &perf[s * (n_corr + 1) + k]);
+                rc = orc_pcg_p(m, diag, upper, b_bnd, source, T, tol, rel_tol, max_iter, min_iter,
+                               precond, NULL, NULL, NULL, &perf[s * (n_corr + 1) + k]);
             }
         }
         orc_patch_values(m, T, b_value);
@@ -616,6 +617,14 @@ int orc_laplacian_foam_corrected(const orc_mesh *m, double DT, double dt, double
     free(diag); free(source); free(upper); free(w); free(corr); free(grad); free(lapSrc); free(T0);
     free(b_int); free(b_bnd);
     return rc;
+}
+
+int orc_laplacian_foam_corrected(const orc_mesh *m, double DT, double dt, double *T,
+                                 double *b_value, int32_t n_steps, int32_t n_corr, double tol,
+                                 double rel_tol, int32_t max_iter, int32_t min_iter, orc_perf *perf)
+{
+    return orc_laplacian_foam_corrected_p(m, DT, dt, T, b_value, n_steps, n_corr, tol, rel_tol,
+                                          max_iter, min_iter, ORC_PRECOND_DIAGONAL, perf);
 }
 
 /* Spatially varying DT: the laplacian's face

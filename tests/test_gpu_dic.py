@@ -253,3 +253,41 @@ def test_dic_invalid(ctx):
         mp.step(1, precond="DIC")
     assert e.value.status == 1
     mp.close()
+
+
+@pytest.mark.parametrize("colour", [False, True])
+def test_dic_corrected_laplacian(ctx, colour):
+    """DIC with the non-orthogonal correction loop (§8(f) rows 1 + 3) on a
+    sheared graded mesh: 1 corrector, vs the oracle in the same numbering."""
+    m = meshgen.skewed_block_mesh(9, 8, 7, shear=(0.3, 0.1, 0.2), grading=(2.0, 1.0, 0.5),
+                                  bc={"xmin": ("fixedValue", 1.0), "zmax": "zeroGradient"})
+    order = meshgen.colour_order(m) if colour else np.arange(m.n_cells)
+    mo = meshgen.relabel_mesh(m, order) if colour else m
+    T0 = meshgen.sine_field(m)
+    To, _, po = oracle.laplacian_foam_corrected(mo, T0[order], 3, n_corr=1, precond="DIC")
+    mesh = P.Mesh(ctx, m, renumber="colour" if colour else False)
+    mesh.set_T(T0)
+    pg = mesh.step(3, corrected=True, n_non_orth_correctors=1, precond="DIC")
+    T = mesh.get_T()[order]
+    assert np.max(np.abs(T - To)) <= 1e-8 * np.max(np.abs(To))
+    assert len(pg) == len(po) == 6
+    assert all(abs(a["n_iterations"] - b["n_iterations"]) <= 1 for a, b in zip(pg, po)), (pg, po)
+    mesh.close()
+
+
+def test_dic_dt_field(ctx):
+    """DIC with a two-material DT field (§8(f) rows 2 + 3), colour numbering."""
+    import dataclasses
+    base = meshgen.with_geometry(meshgen.block_mesh(10, 9, 8))
+    m = dataclasses.replace(base, DT_field=meshgen.layered_dt_field(base))
+    order = meshgen.colour_order(m)
+    mo = meshgen.relabel_mesh(m, order)
+    T0 = meshgen.sine_field(m)
+    To, _, po = oracle.laplacian_foam(mo, T0[order], 4, precond="DIC")
+    mesh = P.Mesh(ctx, m, renumber="colour")
+    mesh.set_T(T0)
+    pg = mesh.step(4, precond="DIC")
+    T = mesh.get_T()[order]
+    assert np.max(np.abs(T - To)) <= 1e-8 * np.max(np.abs(To))
+    assert all(abs(a["n_iterations"] - b["n_iterations"]) <= 1 for a, b in zip(pg, po)), (pg, po)
+    mesh.close()
