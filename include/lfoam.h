@@ -325,9 +325,11 @@ typedef enum {
  *                      graphs of 2^i iterations; 0 = direct launches
  *   LF_OPT_SOLVE_VARIANT (default 0 = by mesh size) persistent single-rank
  *                      solve variant: 1 the L2-resident one (psi update in
- *                      the beta-barrier wait), 2 the HBM-bound one (psi update
- *                      deferred into the Amul phase); mesh_create picks 1 when
- *                      an iteration's working set fits ~1.5x the L2, else 2
+ *                      the beta-barrier wait, {q, diag} kept in shared memory
+ *                      between the phases; needs <= 8 grid-stride trips per
+ *                      thread, else variant 2 runs), 2 the HBM-bound one (psi
+ *                      update deferred into the Amul phase); mesh_create picks
+ *                      1 when an iteration's working set fits ~1.5x the L2
  * Results are identical up to reduction grid size (all are deterministic). */
 typedef enum { LF_OPT_PERSISTENT = 0, LF_OPT_GRAPHS = 1, LF_OPT_SOLVE_VARIANT = 2 } lf_option;
 LF_API lf_status lf_set_option(lf_context *ctx, lf_option opt, int value);

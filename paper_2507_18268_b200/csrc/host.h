@@ -99,6 +99,7 @@ struct lf_mesh {
   int kernelsPerIteration = 0;
   int persistentGrid = 0;     // co-resident grid of k_pcg_persistent
   bool l2Resident = false;    // an iteration's working set fits ~1.5x the L2 (mesh.cpp)
+  bool stashOK = false;       // few enough trips per thread for the L2-resident variant
   unsigned *gridBar = nullptr;  // device {count, generation}
   // peer-memory transport: one IPC-exportable block [flags | vals | recvT | recvW]
   char *p2pBlock = nullptr;

@@ -889,10 +889,15 @@ bool persistent_chunked() { return LF_CHUNKED != 0; }
 #ifndef LF_IDLE_FLUSH
 #define LF_IDLE_FLUSH 1  // persistent kernel may do psi += alpha p while waiting at the beta
 #endif                   // barrier (Workspace.idleFlush, set per mesh: L2-resident sizes)
+#ifndef LF_STASH_TRIPS
+#define LF_STASH_TRIPS 8  // L2-resident variant: at most this many grid-stride trips per thread
+#endif
 #ifndef LF_TAIL
 #define LF_TAIL 1  // persistent kernel: spread the last partial trip over all blocks
 #endif
 bool persistent_tail() { return LF_TAIL != 0; }
+int stash_trips() { return LF_TAIL ? LF_STASH_TRIPS : 0; }
+static size_t stash_bytes() { return (size_t)LF_STASH_TRIPS * BS * sizeof(double2); }
 #ifndef LF_P2P_UNROLL
 #define LF_P2P_UNROLL 2  // persistent phase 2 cells per trip
 #endif
@@ -924,6 +929,11 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
   double *psi = ctl->psi;
   const double *__restrict__ w = ws.w;
   double psiSum = 0.0;  // LF_IDLE_FLUSH: this thread's sum of psi after its last flush
+  // IDLE (L2-resident sizes, <= LF_STASH_TRIPS trips per thread): phase 1
+  // keeps each cell's {q, diag} in shared memory (slot = trip) for phase 2,
+  // so q is never written to / read from global memory and diag is not
+  // re-read: phase 2 streams r only (-24n bytes per iteration)
+  extern __shared__ double2 lf_stash[];
 #if LF_CHUNKED
   // block b owns the contiguous cells [b*C, (b+1)*C): equal work per block on
   // an SM-uniform grid (numSMs x blocks/SM), the same cells in both phases
@@ -1016,10 +1026,16 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
       if (cont) {
         const double pc = first ? w[c] : fma(beta, pold[c], w[c]);
         pnew[c] = pc;
-        double q = a.diag[c] * pc;
+        const double dc = a.diag[c];
+        double q = dc * pc;
         q = row_offdiag<KE>(m, a, c, q, pnb);
         if (HALO) q -= row_proc_p(m, a.bBnd, ws, first, beta, k, c);
-        ws.q[c] = q;
+#if LF_TAIL
+        if (IDLE)
+          lf_stash[i * BS + threadIdx.x] = make_double2(q, dc);
+        else
+#endif
+          ws.q[c] = q;
         v1[0] = fma(pc, q, v1[0]);
       }
     }
@@ -1065,14 +1081,38 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
         }
       };
 #if LF_TAIL
-      for (int i = 0; i <= nFull; i += U) {
-        int cs[U];
+      if (IDLE) {
+        // {q, diag} from the stash, r streamed: all trips' loads issued first
+        constexpr int T = LF_STASH_TRIPS;
+        double rv[T];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int ii = i + u;
-          cs[u] = ii < nFull ? cstart + ii * cstep : (ii == nFull ? tailC : -1);
+        for (int i = 0; i < T; ++i) {
+          const int c = i < nFull ? cstart + i * cstep : (i == nFull ? tailC : -1);
+          rv[i] = (i <= nFull && c >= 0) ? ws.r[c] : 0.0;
         }
-        p2cells(cs);
+#pragma unroll
+        for (int i = 0; i < T; ++i) {
+          const int c = i < nFull ? cstart + i * cstep : (i == nFull ? tailC : -1);
+          if (i <= nFull && c >= 0) {
+            const double2 qd = lf_stash[i * BS + threadIdx.x];
+            const double rn = fma(-alpha2, qd.x, rv[i]);
+            const double wc = (1.0 / qd.y) * rn;
+            ws.r[c] = rn;
+            ws.w[c] = wc;
+            v2[0] += fabs(rn);
+            v2[1] = fma(wc, rn, v2[1]);
+          }
+        }
+      } else {
+        for (int i = 0; i <= nFull; i += U) {
+          int cs[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int ii = i + u;
+            cs[u] = ii < nFull ? cstart + ii * cstep : (ii == nFull ? tailC : -1);
+          }
+          p2cells(cs);
+        }
       }
 #else
       for (int c0 = cstart; c0 < cend; c0 += cstep * U) {
@@ -1176,6 +1216,13 @@ int persistent_grid(int device, int K) {
     LF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, BS, 0));
     best = std::min(best, nb);
   }
+  // the L2-resident variant with its shared-memory stash
+  const void *fi = K == 4 ? (const void *)k_pcg_persistent<4, false, true>
+                          : (K > 0 ? (const void *)k_pcg_persistent<3, false, true>
+                                   : (const void *)k_pcg_persistent<0, false, true>);
+  LF_CUDA(cudaFuncSetAttribute(fi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stash_bytes()));
+  LF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fi, BS, stash_bytes()));
+  best = std::min(best, nb);
   return sms * (best < 1 ? 1 : best);
 }
 
@@ -1190,10 +1237,9 @@ void launch_pcg_persistent(cudaStream_t s, int grid, const MeshDev &m, const Ldu
                            const Workspace &ws, unsigned *bar) {
   const bool halo = m.hasProc || ws.p2p.P > 0;
   void *args[] = {(void *)&m, (void *)&a, (void *)&ws, (void *)&bar};
-  const void *fn = halo                                 ? persistent_fn<true>(m)
-                   : (LF_IDLE_FLUSH && ws.idleFlush)    ? persistent_fn<false, true>(m)
-                                                        : persistent_fn<false>(m);
-  LF_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(BS), args, 0, s));
+  const bool idle = !halo && LF_IDLE_FLUSH && ws.idleFlush;
+  const void *fn = halo ? persistent_fn<true>(m) : idle ? persistent_fn<false, true>(m) : persistent_fn<false>(m);
+  LF_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(BS), args, idle ? stash_bytes() : 0, s));
 }
 
 // ------------------------------------------------------------------ Amul

@@ -196,6 +196,7 @@ void launch_amul(cudaStream_t s, const Launch &L, const MeshDev &m, const LduDev
                  const double *halo, const double *x, double *y);
 int persistent_grid(int device, int K);
 bool persistent_tail();  // LF_TAIL: SM-uniform grid, evenly spread tail trip
+int stash_trips();       // max grid-stride trips of the L2-resident variant (0: none)
 bool persistent_chunked();
 void launch_pcg_persistent(cudaStream_t s, int grid, const MeshDev &m, const LduDev &a,
                            const Workspace &ws, unsigned *bar);

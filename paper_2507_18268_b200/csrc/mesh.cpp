@@ -539,7 +539,8 @@ static void build_mesh(lf_context *ctx, const lf_mesh_desc *d, lf_mesh *M) {
     LF_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, ctx->device));
     const double bytesIter = 96.0 * n + 16.0 * F;
     M->l2Resident = bytesIter <= 1.5 * (double)l2;
-    ws.idleFlush = M->l2Resident ? 1 : 0;
+    M->stashOK = persistent_tail() && (int64_t)n / ((int64_t)M->persistentGrid * BSZ) + 1 <= stash_trips();
+    ws.idleFlush = (M->l2Resident && M->stashOK) ? 1 : 0;
   }
   ws.r = A.alloc<double>(n);
   ws.w = A.alloc<double>(n);

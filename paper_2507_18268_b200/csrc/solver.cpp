@@ -157,7 +157,8 @@ static void run_iterations(lf_mesh *M, lf_solver_perf *out) {
   int64_t launched = 0;
   int chunk = M->lastIters >= 0 ? M->lastIters + 1 : 8;
   // persistent variant: L2-resident (idle psi flush) or HBM-bound (TMA)
-  M->ws.idleFlush = ctx->solveVariant == 0 ? (M->l2Resident ? 1 : 0) : (ctx->solveVariant == 1 ? 1 : 0);
+  // (the L2-resident variant needs few enough trips per thread for its stash)
+  M->ws.idleFlush = M->stashOK && (ctx->solveVariant == 0 ? M->l2Resident : ctx->solveVariant == 1) ? 1 : 0;
   if (M->hctl->precond != LF_PRECOND_DIAGONAL) {
     // DIC (DILU = DIC on this symmetric matrix): one persistent launch with
     // the level-scheduled sweeps (single rank, checked in upload_controls)

@@ -14,9 +14,9 @@ sys.path.insert(0, ROOT)
 
 # name -> (-D defines, bench --mode[, bench --precond])
 VARIANTS = {
-    "auto": ([], "persistent"),
-    "v1_l2": ([], "persistent", "diagonal", 1),
-    "v2_hbm": ([], "persistent", "diagonal", 2),
+    "stash": ([], "persistent"),
+    "nostash_v2": ([], "persistent", "diagonal", 2),
+    "dic": ([], "persistent", "DIC"),
 }
 
 
