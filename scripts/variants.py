@@ -14,9 +14,8 @@ sys.path.insert(0, ROOT)
 
 # name -> (-D defines, bench --mode[, bench --precond])
 VARIANTS = {
-    "stash": ([], "persistent"),
-    "nostash_v2": ([], "persistent", "diagonal", 2),
-    "dic": ([], "persistent", "DIC"),
+    "pipe": ([], "persistent"),
+    "nopipe": (["LF_PIPE=0"], "persistent"),
 }
 
 
