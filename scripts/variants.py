@@ -14,8 +14,8 @@ sys.path.insert(0, ROOT)
 
 # name -> (-D defines, bench --mode[, bench --precond])
 VARIANTS = {
-    "pipe": ([], "persistent"),
-    "nopipe": (["LF_PIPE=0"], "persistent"),
+    "stashp": ([], "persistent"),
+    "nostashp": (["LF_STASH_P=0"], "persistent"),
 }
 
 
