@@ -1099,6 +1099,7 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
             const double wc = (1.0 / qd.y) * rn;
             ws.r[c] = rn;
             ws.w[c] = wc;
+            if (HALO && ws.p2p.P > 0) push_halo(m, ws.p2p.dstW, c, wc);
             v2[0] += fabs(rn);
             v2[1] = fma(wc, rn, v2[1]);
           }
@@ -1217,12 +1218,17 @@ int persistent_grid(int device, int K) {
     best = std::min(best, nb);
   }
   // the L2-resident variant with its shared-memory stash
-  const void *fi = K == 4 ? (const void *)k_pcg_persistent<4, false, true>
-                          : (K > 0 ? (const void *)k_pcg_persistent<3, false, true>
-                                   : (const void *)k_pcg_persistent<0, false, true>);
-  LF_CUDA(cudaFuncSetAttribute(fi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stash_bytes()));
-  LF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fi, BS, stash_bytes()));
-  best = std::min(best, nb);
+  for (int h = 0; h < 2; ++h) {  // the L2-resident variants (single rank / halo) with the stash
+    const void *fi = h ? (K == 4 ? (const void *)k_pcg_persistent<4, true, true>
+                                 : (K > 0 ? (const void *)k_pcg_persistent<3, true, true>
+                                          : (const void *)k_pcg_persistent<0, true, true>))
+                       : (K == 4 ? (const void *)k_pcg_persistent<4, false, true>
+                                 : (K > 0 ? (const void *)k_pcg_persistent<3, false, true>
+                                          : (const void *)k_pcg_persistent<0, false, true>));
+    LF_CUDA(cudaFuncSetAttribute(fi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stash_bytes()));
+    LF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fi, BS, stash_bytes()));
+    best = std::min(best, nb);
+  }
   return sms * (best < 1 ? 1 : best);
 }
 
@@ -1237,8 +1243,10 @@ void launch_pcg_persistent(cudaStream_t s, int grid, const MeshDev &m, const Ldu
                            const Workspace &ws, unsigned *bar) {
   const bool halo = m.hasProc || ws.p2p.P > 0;
   void *args[] = {(void *)&m, (void *)&a, (void *)&ws, (void *)&bar};
-  const bool idle = !halo && LF_IDLE_FLUSH && ws.idleFlush;
-  const void *fn = halo ? persistent_fn<true>(m) : idle ? persistent_fn<false, true>(m) : persistent_fn<false>(m);
+  // L2-resident variant (stash + psi update in the barrier wait) on either path
+  const bool idle = LF_IDLE_FLUSH && ws.idleFlush;
+  const void *fn = halo ? (idle ? persistent_fn<true, true>(m) : persistent_fn<true>(m))
+                        : (idle ? persistent_fn<false, true>(m) : persistent_fn<false>(m));
   LF_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(BS), args, idle ? stash_bytes() : 0, s));
 }
 
