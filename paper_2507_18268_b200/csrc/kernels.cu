@@ -889,6 +889,9 @@ bool persistent_chunked() { return LF_CHUNKED != 0; }
 #ifndef LF_IDLE_FLUSH
 #define LF_IDLE_FLUSH 1  // persistent kernel may do psi += alpha p while waiting at the beta
 #endif                   // barrier (Workspace.idleFlush, set per mesh: L2-resident sizes)
+#ifndef LF_REVERSE
+#define LF_REVERSE 1  // persistent phase 2 sweeps the trips in reverse order (L2 reuse)
+#endif
 #ifndef LF_STASH_TRIPS
 #define LF_STASH_TRIPS 8  // L2-resident variant: at most this many grid-stride trips per thread
 #endif
@@ -1105,12 +1108,15 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
           }
         }
       } else {
-        for (int i = 0; i <= nFull; i += U) {
+        // LF_REVERSE: phase 2 sweeps the trips backwards, so it starts on the
+        // cells phase 1 wrote last (q still in L2) and ends on the ones the
+        // next phase 1 reads first (w, r still in L2)
+        for (int i0 = 0; i0 <= nFull; i0 += U) {
           int cs[U];
 #pragma unroll
           for (int u = 0; u < U; ++u) {
-            const int ii = i + u;
-            cs[u] = ii < nFull ? cstart + ii * cstep : (ii == nFull ? tailC : -1);
+            const int ii = LF_REVERSE ? nFull - (i0 + u) : i0 + u;
+            cs[u] = (ii >= 0 && ii < nFull) ? cstart + ii * cstep : (ii == nFull ? tailC : -1);
           }
           p2cells(cs);
         }

@@ -14,8 +14,8 @@ sys.path.insert(0, ROOT)
 
 # name -> (-D defines, bench --mode[, bench --precond])
 VARIANTS = {
-    "stashp": ([], "persistent"),
-    "nostashp": (["LF_STASH_P=0"], "persistent"),
+    "rev": ([], "persistent"),
+    "fwd": (["LF_REVERSE=0"], "persistent"),
 }
 
 
