@@ -170,7 +170,6 @@ def _oracle_steps(om, T0, steps, corrected, **kw):
     import oracle
     if corrected < 0:
         return oracle.laplacian_foam(om, T0, steps, DT=DT, dt=DELTA_T, tol=TOL, **kw)
-    kw.pop("precond", None)
     return oracle.laplacian_foam_corrected(om, T0, steps, n_corr=corrected, DT=DT, dt=DELTA_T, tol=TOL, **kw)
 
 
@@ -255,8 +254,8 @@ def run_ours(args):
         raise SystemExit("--corrected: single rank only (the corrected path has no processor patches)")
     gmesh = workload_mesh(cfg, args.corrected, args.dt_field)
     kw = step_kw(args.corrected, args.precond)
-    if args.precond != "diagonal" and ws > 1:
-        raise SystemExit("--precond DIC: single rank only (the DIC is processor-local; no halo variant yet)")
+    if args.precond != "diagonal" and ws > 1 and args.transport != "p2p":
+        raise SystemExit("--precond DIC across ranks needs --transport p2p (the persistent DIC solve)")
     n_global = gmesh.n_cells
     T0g = meshgen.canonical_field(gmesh)
     if ws > 1:
