@@ -728,6 +728,9 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
   return v;
 }
 
+#ifndef LF_SPIN_NS
+#define LF_SPIN_NS 32  // grid-barrier poll back-off (ns)
+#endif
 #ifndef LF_BAR_ACQREL
 #define LF_BAR_ACQREL 1  // grid barrier with acq_rel atomics instead of fence + atomic
 #endif
@@ -794,7 +797,7 @@ __device__ void grid_reduce_sync(double (&v)[NV], double *partials, unsigned *ba
       const unsigned long long t0 = gtime_ns();
       unsigned tries = 0;
       while (ld_acquire(bar + 1) == gen) {
-        __nanosleep(32);
+        if (LF_SPIN_NS > 0) __nanosleep(LF_SPIN_NS);
         spin_check(t0, tries);
       }
 #if LF_TIMING
@@ -867,7 +870,7 @@ __device__ __forceinline__ void grid_barrier(unsigned *bar) {
       const unsigned long long t0 = gtime_ns();
       unsigned tries = 0;
       while (ld_acquire(bar + 1) == gen) {
-        __nanosleep(32);
+        if (LF_SPIN_NS > 0) __nanosleep(LF_SPIN_NS);
         spin_check(t0, tries);
       }
     }

@@ -14,8 +14,12 @@ sys.path.insert(0, ROOT)
 
 # name -> (-D defines, bench --mode[, bench --precond])
 VARIANTS = {
-    "rev": ([], "persistent"),
-    "fwd": (["LF_REVERSE=0"], "persistent"),
+    "spin32": ([], "persistent"),
+    "spin0": (["LF_SPIN_NS=0"], "persistent"),
+    "spin8": (["LF_SPIN_NS=8"], "persistent"),
+    "spin128": (["LF_SPIN_NS=128"], "persistent"),
+    "dic_spin32": ([], "persistent", "DIC"),
+    "dic_spin0": (["LF_SPIN_NS=0"], "persistent", "DIC"),
 }
 
 
