@@ -414,7 +414,7 @@ def test_invalid_arguments(ctx):
 
 @pytest.mark.parametrize("variant", [1, 2])
 @pytest.mark.parametrize("dims", [(10, 10, 10), (37, 23, 19), (7, 5, 4), (64, 32, 24)])
-def test_solve_variants(variant, dims):
+def test_solve_variants(ctx, variant, dims):
     """The persistent solve's L2-resident variant (psi update in the beta-
     barrier wait) and HBM-bound variant (psi update deferred into the Amul
     phase), forced on meshes of several sizes and ragged tails, against the
@@ -437,5 +437,52 @@ def test_solve_variants(variant, dims):
     perf = ldu.pcg_solve(psi)
     assert np.max(np.abs(psi.cpu().numpy() - x_ref)) <= 1e-8 * np.max(np.abs(x_ref))
     assert abs(perf["n_iterations"] - p_ref["n_iterations"]) <= 1
+    mesh.close()
+    c.close()
+
+
+def k4_mesh(n=9):
+    """A block mesh plus one extra 'diagonal' internal face per cell
+    ((i,j,k)-(i+1,j+1,k)): up to 4 owned and 4 neighbour-side faces per cell,
+    so the 4-slot ELL kernels run (hex meshes use 3 slots; permuted meshes
+    the CSR gather).  Any LDU mesh with positive coefficients is a valid
+    input of the method (SPD, diagonally dominant)."""
+    import dataclasses
+    m = meshgen.block_mesh(n, bc=mixed_bc())
+    c = np.arange(m.n_cells)
+    i, j = c % n, (c // n) % n
+    sel = (i < n - 1) & (j < n - 1)
+    o = c[sel].astype(np.int32)
+    nb = (o + 1 + n).astype(np.int32)
+    owner = np.concatenate([m.owner, o])
+    neighbour = np.concatenate([m.neighbour, nb])
+    key = np.lexsort((neighbour, owner))
+    h = 1.0 / n
+    extra = np.full(o.shape[0], 0.5 * h * h)
+    return dataclasses.replace(m, owner=owner[key], neighbour=neighbour[key],
+                               mag_sf=np.concatenate([m.mag_sf, extra])[key],
+                               delta=np.concatenate([m.delta, np.full(o.shape[0], 1.0 / (h * np.sqrt(2.0)))])[key])
+
+
+@pytest.mark.parametrize("variant", [1, 2])
+def test_k4_ell_mesh(ctx, variant):
+    c = P.Context(0)
+    c.set_option("variant", variant)
+    m = k4_mesh()
+    T0 = meshgen.sine_field(m)
+    To, _, po = oracle.laplacian_foam(m, T0, 3)
+    mesh = P.Mesh(c, m)
+    mesh.set_T(T0)
+    pg = mesh.step(3)
+    assert np.max(np.abs(mesh.get_T() - To)) <= 1e-8 * np.max(np.abs(To))
+    assert all(abs(a["n_iterations"] - b["n_iterations"]) <= 1 for a, b in zip(pg, po)), (pg, po)
+    ref = oracle.assemble(m, 1.0, 0.2, mesh.get_T())
+    ldu = mesh.assemble(1.0, 0.2)
+    got = ldu.export()
+    assert np.array_equal(got["diag"], ref["diag"]) and np.array_equal(got["upper"], ref["upper"])
+    x = meshgen.random_field(m, seed=5)
+    y = ldu.amul(dev(x), dev(np.zeros(m.n_cells))).cpu().numpy()
+    y_ref = oracle.amul(m, ref["diag"], ref["upper"], x)
+    assert np.max(np.abs(y - y_ref) / row_scale(m, ref["diag"], ref["upper"], x)) <= 1e-12
     mesh.close()
     c.close()
