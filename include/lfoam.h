@@ -323,8 +323,9 @@ typedef enum {
  *                      launch per phase
  *   LF_OPT_GRAPHS      (default 1) phase launches are replayed from CUDA
  *                      graphs of 2^i iterations; 0 = direct launches
- *   LF_OPT_SOLVE_VARIANT (default 0 = by mesh size) persistent single-rank
- *                      solve variant: 1 the L2-resident one (psi update in
+ *   LF_OPT_SOLVE_VARIANT (default 0 = by mesh size) persistent solve variant
+ *                      (single rank or peer-memory transport; diagonal and
+ *                      DIC): 1 the L2-resident one (psi update in
  *                      the beta-barrier wait, {q, diag} kept in shared memory
  *                      between the phases; needs <= 8 grid-stride trips per
  *                      thread, else variant 2 runs), 2 the HBM-bound one (psi
