@@ -14,12 +14,8 @@ sys.path.insert(0, ROOT)
 
 # name -> (-D defines, bench --mode[, bench --precond])
 VARIANTS = {
-    "spin32": ([], "persistent"),
-    "spin0": (["LF_SPIN_NS=0"], "persistent"),
-    "spin8": (["LF_SPIN_NS=8"], "persistent"),
-    "spin128": (["LF_SPIN_NS=128"], "persistent"),
-    "dic_spin32": ([], "persistent", "DIC"),
-    "dic_spin0": (["LF_SPIN_NS=0"], "persistent", "DIC"),
+    "base": ([], "persistent"),
+    "l2persist": (["LF_L2PERSIST=1"], "persistent"),
 }
 
 
