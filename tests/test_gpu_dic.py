@@ -291,3 +291,32 @@ def test_dic_dt_field(ctx):
     assert np.max(np.abs(T - To)) <= 1e-8 * np.max(np.abs(To))
     assert all(abs(a["n_iterations"] - b["n_iterations"]) <= 1 for a, b in zip(pg, po)), (pg, po)
     mesh.close()
+
+
+def test_dic_multicolour_8_neighbours(ctx):
+    """Block + diagonal faces: up to 8 neighbours per cell (the 8-slot rows)
+    and a first-fit colouring with 4 colours, i.e. 4 contiguous levels under
+    renumber = 2 (several forward and backward level passes) — bitwise
+    preconditioner and step parity."""
+    from test_gpu_parity import k4_mesh
+    m = k4_mesh(8)
+    order = meshgen.colour_order(m)
+    mc = meshgen.relabel_mesh(m, order)
+    deg = np.bincount(mc.owner, minlength=mc.n_cells) + np.bincount(mc.neighbour, minlength=mc.n_cells)
+    assert deg.max() == 8
+    T0 = meshgen.sine_field(m)
+    To, _, po = oracle.laplacian_foam(mc, T0[order], 3, precond="DIC")
+    mesh = P.Mesh(ctx, m, renumber="colour")
+    mesh.set_T(T0)
+    pg = mesh.step(3, precond="DIC")
+    assert np.max(np.abs(mesh.get_T()[order] - To)) <= 1e-8 * np.max(np.abs(To))
+    assert all(abs(a["n_iterations"] - b["n_iterations"]) <= 1 for a, b in zip(pg, po)), (pg, po)
+    ref = oracle.assemble(mc, 1.0, 0.2, mesh.get_T()[order])
+    ldu = mesh.assemble(1.0, 0.2)
+    r = meshgen.random_field(mc, seed=3)
+    rD_o, w_o = oracle.dic(mc, ref["diag"], ref["upper"], r)
+    w, rD = dev(np.zeros(m.n_cells)), dev(np.zeros(m.n_cells))
+    ldu.precondition(dev(r), w, "DIC", rD)
+    np.testing.assert_array_equal(rD.cpu().numpy(), rD_o)
+    np.testing.assert_array_equal(w.cpu().numpy(), w_o)
+    mesh.close()
