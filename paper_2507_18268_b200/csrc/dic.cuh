@@ -28,8 +28,8 @@
 #define LF_DIC_TAIL 0    // 1: level passes and the Amul phase spread the tail trip (r2e:
 #endif                   // neutral at 200^3, -2% at 100^3 -> off)
 #ifndef LF_DIC_PAIR
-#define LF_DIC_PAIR 0    // 1: phase 1 interleaves the two colours (thread t: cell t of each).
-#endif                   // r1x: 100^3 3.37 vs 3.13 ms/step, 200^3 39.2 vs 39.9 -> off
+#define LF_DIC_PAIR 1    // phase 1 interleaves the two colours (thread t: cell t of each) in the
+#endif                   // HBM-bound variant (r1x: 200^3 39.2 vs 39.9 ms/step; 100^3 3.37 vs 3.13)
 
 // Grid-stride loop over [t0, t1) with the evenly spread tail trip of the
 // persistent kernels (LF_TAIL): full trips while every thread has an index,
@@ -251,8 +251,9 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
   __shared__ St st;
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
   const int L = d.L;
-  const bool pair = LF_DIC_PAIR && d.contig && L == 2;  // two contiguous colours: interleave in phase 1
-  const bool idleF = IDLE && !pair;  // psi flush in the beta-barrier wait (Workspace.idleFlush)
+  // two contiguous colours: interleave them in phase 1 (HBM-bound variant only)
+  const bool pair = LF_DIC_PAIR && !IDLE && d.contig && L == 2;
+  const bool idleF = IDLE;  // psi flush in the beta-barrier wait (Workspace.idleFlush)
   double psiSum = 0.0;
   double *psi = ctl->psi;
   double *r = ws.r, *w = ws.w, *q = ws.q;

@@ -14,8 +14,8 @@ sys.path.insert(0, ROOT)
 
 # name -> (-D defines, bench --mode[, bench --precond])
 VARIANTS = {
-    "base": ([], "persistent"),
-    "l2persist": (["LF_L2PERSIST=1"], "persistent"),
+    "dic_pair": ([], "persistent", "DIC"),
+    "dic_nopair": (["LF_DIC_PAIR=0"], "persistent", "DIC"),
 }
 
 
