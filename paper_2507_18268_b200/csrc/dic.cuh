@@ -27,6 +27,9 @@
 #ifndef LF_DIC_TAIL
 #define LF_DIC_TAIL 0    // 1: level passes and the Amul phase spread the tail trip (r2e:
 #endif                   // neutral at 200^3, -2% at 100^3 -> off)
+#ifndef LF_DIC_REVERSE
+#define LF_DIC_REVERSE 1  // 2-level forward sweep in reverse trip order (L2 reuse)
+#endif
 #ifndef LF_DIC_PAIR
 #define LF_DIC_PAIR 1    // phase 1 interleaves the two colours (thread t: cell t of each) in the
 #endif                   // HBM-bound variant (r1x: 200^3 39.2 vs 39.9 ms/step; 100^3 3.37 vs 3.13)
@@ -47,6 +50,16 @@ __device__ __forceinline__ void grid_range(int t0, int t1, F body) {
 #else
   for (int t = first; t < t1; t += S) body(t);
 #endif
+}
+
+// The same trips in reverse order (the last trip first): a pass that
+// starts where the previous one ended finds that pass's lines still in L2.
+template <class F>
+__device__ __forceinline__ void grid_range_rev(int t0, int t1, F body) {
+  const int S = gridDim.x * blockDim.x;
+  const int first = t0 + (int)(blockIdx.x * blockDim.x + threadIdx.x);
+  if (first >= t1) return;
+  for (int t = first + ((t1 - 1 - first) / S) * S; t >= t0; t -= S) body(t);
 }
 
 template <int KS>
@@ -162,7 +175,7 @@ __device__ __forceinline__ void dic_apply(const MeshDev &m, const DicDev &d, con
   const int L = d.L;
   double v[2] = {0.0, 0.0};
   for (int l = 1; l < L; ++l) {
-    grid_range(__ldg(d.lvlStart + l), __ldg(d.lvlStart + l + 1), [&](int t) {
+    auto fwd = [&](int t) {
       const int c = level_cell(d, t);
       double wc;
       const double rc = dic_forward_cell<KS>(d, a, c, r, q, w, upd, alpha, wc);
@@ -171,7 +184,13 @@ __device__ __forceinline__ void dic_apply(const MeshDev &m, const DicDev &d, con
         v[1] = fma(wc, rc, v[1]);
         if (HALO && pp.P > 0) push_halo(m, pp.dstW, c, wc);
       }
-    });
+    };
+    // two levels: the forward pass walks backwards from where the Amul phase
+    // ended (LF_DIC_REVERSE), the backward pass then forwards from there
+    if (LF_DIC_REVERSE && L == 2)
+      grid_range_rev(__ldg(d.lvlStart + l), __ldg(d.lvlStart + l + 1), fwd);
+    else
+      grid_range(__ldg(d.lvlStart + l), __ldg(d.lvlStart + l + 1), fwd);
     grid_barrier(bar);
   }
   for (int l = L >= 2 ? L - 2 : 0; l >= 0; --l) {

@@ -14,8 +14,8 @@ sys.path.insert(0, ROOT)
 
 # name -> (-D defines, bench --mode[, bench --precond])
 VARIANTS = {
-    "dic_pair": ([], "persistent", "DIC"),
-    "dic_nopair": (["LF_DIC_PAIR=0"], "persistent", "DIC"),
+    "dic_rev": ([], "persistent", "DIC"),
+    "dic_norev": (["LF_DIC_REVERSE=0"], "persistent", "DIC"),
 }
 
 
