@@ -27,9 +27,12 @@
 #ifndef LF_DIC_TAIL
 #define LF_DIC_TAIL 0    // 1: level passes and the Amul phase spread the tail trip (r2e:
 #endif                   // neutral at 200^3, -2% at 100^3 -> off)
-#ifndef LF_DIC_REVERSE
-#define LF_DIC_REVERSE 1  // 2-level forward sweep in reverse trip order (L2 reuse)
+#ifndef LF_REV_ALIGN
+#define LF_REV_ALIGN 0
 #endif
+#ifndef LF_DIC_REVERSE
+#define LF_DIC_REVERSE 1  // 1: the 2-level forward sweep in reverse trip order (L2 reuse);
+#endif                    // 2: every pass reversed on alternate iterations
 #ifndef LF_DIC_PAIR
 #define LF_DIC_PAIR 1    // phase 1 interleaves the two colours (thread t: cell t of each) in the
 #endif                   // HBM-bound variant (r1x: 200^3 39.2 vs 39.9 ms/step; 100^3 3.37 vs 3.13)
@@ -58,8 +61,18 @@ template <class F>
 __device__ __forceinline__ void grid_range_rev(int t0, int t1, F body) {
   const int S = gridDim.x * blockDim.x;
   const int first = t0 + (int)(blockIdx.x * blockDim.x + threadIdx.x);
+#if LF_REV_ALIGN
+  // the same trip index in every thread
+  for (int i = (t1 - t0 + S - 1) / S - 1; i >= 0; --i) {
+    const int t = first + i * S;
+    if (t < t1) body(t);
+  }
+#else
+  // each thread starts at its own last index (threads past the end of the
+  // partial last trip start one trip lower)
   if (first >= t1) return;
   for (int t = first + ((t1 - 1 - first) / S) * S; t >= t0; t -= S) body(t);
+#endif
 }
 
 template <int KS>
@@ -171,7 +184,7 @@ template <int KS, bool HALO, class Idle = NoIdle>
 __device__ __forceinline__ void dic_apply(const MeshDev &m, const DicDev &d, const LduDev &a, double *r,
                                           const double *q, double *w, bool upd, double alpha, unsigned *bar,
                                           double *partials, double *out, const P2PDev &pp,
-                                          Idle idle = Idle()) {
+                                          Idle idle = Idle(), bool odd = false) {
   const int L = d.L;
   double v[2] = {0.0, 0.0};
   for (int l = 1; l < L; ++l) {
@@ -185,23 +198,28 @@ __device__ __forceinline__ void dic_apply(const MeshDev &m, const DicDev &d, con
         if (HALO && pp.P > 0) push_halo(m, pp.dstW, c, wc);
       }
     };
-    // two levels: the forward pass walks backwards from where the Amul phase
-    // ended (LF_DIC_REVERSE), the backward pass then forwards from there
-    if (LF_DIC_REVERSE && L == 2)
+    // two levels (LF_DIC_REVERSE): every pass starts where the previous one
+    // ended — even iterations: Amul forwards, this pass backwards, the
+    // backward pass forwards; odd iterations the mirror image
+    if (LF_DIC_REVERSE && L == 2 && !odd)
       grid_range_rev(__ldg(d.lvlStart + l), __ldg(d.lvlStart + l + 1), fwd);
     else
       grid_range(__ldg(d.lvlStart + l), __ldg(d.lvlStart + l + 1), fwd);
     grid_barrier(bar);
   }
   for (int l = L >= 2 ? L - 2 : 0; l >= 0; --l) {
-    grid_range(__ldg(d.lvlStart + l), __ldg(d.lvlStart + l + 1), [&](int t) {
+    auto bwd = [&](int t) {
       const int c = level_cell(d, t);
       double wc;
       const double rc = dic_backward_cell<KS>(d, a, c, l == 0, r, q, w, upd, alpha, wc);
       if (l == 0) v[0] += fabs(rc);
       v[1] = fma(wc, rc, v[1]);
       if (HALO && pp.P > 0) push_halo(m, pp.dstW, c, wc);
-    });
+    };
+    if (LF_DIC_REVERSE == 2 && L == 2 && odd)
+      grid_range_rev(__ldg(d.lvlStart + l), __ldg(d.lvlStart + l + 1), bwd);
+    else
+      grid_range(__ldg(d.lvlStart + l), __ldg(d.lvlStart + l + 1), bwd);
     if (l > 0) grid_barrier(bar);
   }
   grid_reduce_sync<2>(v, partials, bar, out, pp LF_DBG_ARG(0), idle);
@@ -333,19 +351,28 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
     // the lines its partner-colour neighbours just read.
     double v1[2] = {0.0, 0.0};
     if (idleF) v1[1] = psiSum;
+    const bool odd = LF_DIC_REVERSE == 2 && L == 2 && (k & 1);  // walk backwards on odd iterations
     if (pair) {
       const int n0 = __ldg(d.lvlStart + 1), n1 = m.n - n0, nt = max(n0, n1);
-      for (int t = gtid; t < nt; t += stride) {
+      auto two = [&](int t) {
         if (t < n0)
           dic_amul_cell<KS, HALO>(m, a, d, ws, k, t, first, cont, alpha, beta, psi, w, pold, pnew, q, v1, false);
         if (t < n1)
           dic_amul_cell<KS, HALO>(m, a, d, ws, k, n0 + t, first, cont, alpha, beta, psi, w, pold, pnew, q, v1,
                                   false);
-      }
+      };
+      if (odd)
+        grid_range_rev(0, nt, two);
+      else
+        for (int t = gtid; t < nt; t += stride) two(t);
     } else {
-      grid_range(0, m.n, [&](int c) {
+      auto one = [&](int c) {
         dic_amul_cell<KS, HALO>(m, a, d, ws, k, c, first, cont, alpha, beta, psi, w, pold, pnew, q, v1, idleF);
-      });
+      };
+      if (odd)
+        grid_range_rev(0, m.n, one);
+      else
+        grid_range(0, m.n, one);
     }
     grid_reduce_sync<2>(v1, ws.partials, bar, ws.gsum->p1, pp LF_DBG_ARG(0));
     if (!cont) break;
@@ -369,7 +396,8 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
         psiSum += ps;
       });
     };
-    dic_apply<KS, HALO>(m, d, a, r, q, w, true, alphaK, bar, ws.partials, ws.gsum->p2, pp, flush);
+    dic_apply<KS, HALO>(m, d, a, r, q, w, true, alphaK, bar, ws.partials, ws.gsum->p2, pp, flush,
+                        LF_DIC_REVERSE == 2 && L == 2 && (st.k & 1));
     if (threadIdx.x == 0) ++st.k;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
