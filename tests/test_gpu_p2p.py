@@ -139,10 +139,10 @@ def _rank_main(rank, world, port, persistent, out, precond="diagonal"):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("persistent", [False, True])
-def test_p2p_two_processes_one_gpu(P, persistent):
+@pytest.mark.parametrize("persistent,world", [(False, 2), (True, 2), (True, 3)])
+def test_p2p_two_processes_one_gpu(P, persistent, world):
+    """world = 3: the middle rank has two processor patches (an interior slab)."""
     import torch.multiprocessing as mp
-    world = 2
     ctx = mp.get_context("spawn")
     mgr = ctx.Manager()
     out = mgr.dict()
@@ -167,7 +167,7 @@ def test_p2p_two_processes_one_gpu(P, persistent):
         _, cells, Tr, its, _ = res[r]
         T[cells] = Tr
         assert all(abs(a - b["n_iterations"]) <= 1 for a, b in zip(its, po)), (its, po)
-    assert res[0][3] == res[1][3]          # identical stopping decisions on both ranks
+    assert all(res[r][3] == res[0][3] for r in range(world))  # identical stopping decisions on all ranks
     assert np.max(np.abs(T - To)) <= 1e-8 * np.max(np.abs(To))
 
 
