@@ -222,7 +222,7 @@ __device__ __forceinline__ void dic_apply(const MeshDev &m, const DicDev &d, con
       grid_range(__ldg(d.lvlStart + l), __ldg(d.lvlStart + l + 1), bwd);
     if (l > 0) grid_barrier(bar);
   }
-  grid_reduce_sync<2>(v, partials, bar, out, pp LF_DBG_ARG(0), idle);
+  grid_reduce_sync<2, HALO>(v, partials, bar, out, pp LF_DBG_ARG(0), idle);
 }
 
 // Phase-1 work of one cell in the DIC solve: deferred psi update, p = w +
@@ -374,7 +374,7 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
       else
         grid_range(0, m.n, one);
     }
-    grid_reduce_sync<2>(v1, ws.partials, bar, ws.gsum->p1, pp LF_DBG_ARG(0));
+    grid_reduce_sync<2, HALO>(v1, ws.partials, bar, ws.gsum->p1, pp LF_DBG_ARG(0));
     if (!cont) break;
     if (threadIdx.x == 0) {
       const double pq = __ldcg(&ws.gsum->p1[0]);

@@ -145,6 +145,7 @@ void allreduce(lf_mesh *M, const double *local, double *global, size_t count);
 void upload_controls(lf_mesh *M, const lf_solver_controls *c, double *psi);
 // precond.cpp
 void ensure_dic(lf_mesh *M);  // build the DIC levels / rows (once), fill symU if assembled
+void build_rows(lf_mesh *M);  // the same without the DIC transport check (mesh_create, K > 4)
 void require_dic(const lf_mesh *M);  // INVALID_ARG where the DIC kernels cannot run
 void precondition(lf_mesh *M, int precond, const double *r, double *w, double *rD);
 // mesh.cpp: resident grid with equal grid-stride trips per block

@@ -221,10 +221,33 @@ __device__ bool reduce_grid(double (&v)[NV], double *partials, unsigned *ticket,
 // upper-triangular face order exactly the face-loop order of
 // lduMatrix::Amul.  Returns acc + sum upper_f x_other(f);
 // sU (optional) receives sum upper_f (row sum for sumA).
+// KE > 0: half ELL slices with KE slots per side; KE < 0: full-row ELL with
+// -KE slots (the DIC rows; meshes with more than 4 faces on a side), each
+// row in ascending neighbour label = the same summation order; KE == 0: CSR.
 template <int KE, class XF>
 __device__ __forceinline__ double row_offdiag(const MeshDev &m, const LduDev &a, int c, double acc,
                                               XF xval, double *sU = nullptr) {
-  if constexpr (KE > 0) {
+  if constexpr (KE < 0) {
+    constexpr int KS = -KE;
+    int lab[KS];
+    double u[KS], x[KS];
+#pragma unroll
+    for (int k = 0; k < KS; ++k) {
+      lab[k] = __ldg(m.symN + k * m.ldS + c);
+      u[k] = __ldg(a.symU + k * m.ldS + c);
+    }
+#pragma unroll
+    for (int k = 0; k < KS; ++k) x[k] = lab[k] >= 0 ? xval(lab[k] & (DIC_L0BIT - 1)) : 0.0;
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < KS; ++k)
+      if (lab[k] >= 0) {
+        acc = fma(u[k], x[k], acc);
+        s += u[k];
+      }
+    if (sU) *sU = s;
+    return acc;
+  } else if constexpr (KE > 0) {
     const int n = m.ldE;  // slab stride
     int lo[KE], nb[KE];
     double uo[KE];
@@ -354,6 +377,8 @@ __device__ __forceinline__ bool conv(double res, double init, const PcgCtl *ctl)
   do {                                                                     \
     if (!LF_NO_ELL && (m).K > 0 && (m).K <= 3) KERNEL<3> __VA_ARGS__;       \
     else if (!LF_NO_ELL && (m).K == 4) KERNEL<4> __VA_ARGS__;               \
+    else if ((m).KS == 6) KERNEL<-6> __VA_ARGS__;                          \
+    else if ((m).KS == 8) KERNEL<-8> __VA_ARGS__;                          \
     else KERNEL<0> __VA_ARGS__;                                            \
   } while (0)
 
@@ -754,7 +779,8 @@ __device__ int g_dbg_i_dummy;
 struct NoIdle {
   __device__ void operator()() const {}
 };
-template <int NV, class Idle = NoIdle>
+// PEER = false compiles the cross-rank exchange out (single-rank variants).
+template <int NV, bool PEER = true, class Idle = NoIdle>
 __device__ void grid_reduce_sync(double (&v)[NV], double *partials, unsigned *bar, double *out,
                                  const P2PDev &P
 #if LF_TIMING
@@ -773,7 +799,7 @@ __device__ void grid_reduce_sync(double (&v)[NV], double *partials, unsigned *ba
     if (g_dbg_i < LF_DBG_N && blockIdx.x < LF_DBG_G) g_dbg_arr[g_dbg_i][blockIdx.x] = gtime_ns();
 #endif
     unsigned t;
-    if (P.P > 0) {
+    if (PEER && P.P > 0) {
       __threadfence_system();  // peer-memory halo stores of this block precede the arrival
       t = atomicAdd(bar, 1u);
     } else {
@@ -828,7 +854,7 @@ __device__ void grid_reduce_sync(double (&v)[NV], double *partials, unsigned *ba
         for (int k = 0; k < NV; ++k) s[k] += t[u][k];
     }
     block_sum<NV>(s, sm);
-    if (P.P > 0) p2p_allreduce<NV>(P, s);  // ranks exchange totals before the local release
+    if (PEER && P.P > 0) p2p_allreduce<NV>(P, s);  // ranks exchange totals before the local release
     if (threadIdx.x == 0) {
 #pragma unroll
       for (int k = 0; k < NV; ++k) out[k] = s[k];
@@ -1046,7 +1072,7 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
       }
     }
     LF_TSTAMP(1);
-    grid_reduce_sync<2>(v1, ws.partials, bar, ws.gsum->p1, ws.p2p LF_DBG_ARG(2 * k));
+    grid_reduce_sync<2, HALO>(v1, ws.partials, bar, ws.gsum->p1, ws.p2p LF_DBG_ARG(2 * k));
     LF_TSTAMP(2);
     if (!cont) break;
     // ---- phase 2: singularity, alpha, r -= alpha q, w = r/diag, sums
@@ -1154,7 +1180,7 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
         psiSum += ps;
       }
     };
-    grid_reduce_sync<2>(v2, ws.partials, bar, ws.gsum->p2, ws.p2p LF_DBG_ARG(2 * k + 1), flush);
+    grid_reduce_sync<2, HALO>(v2, ws.partials, bar, ws.gsum->p2, ws.p2p LF_DBG_ARG(2 * k + 1), flush);
     LF_TSTAMP(4);
     if (threadIdx.x == 0) ++st.k;
   }
@@ -1210,33 +1236,35 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
   }
 }
 
-int persistent_grid(int device, int K) {
-  int sms = 0, nb = 0;
-  LF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-  // the grid must be co-resident for every variant that may be launched
-  const void *fns[3] = {K == 4 ? (const void *)k_pcg_persistent<4, false>
-                               : (K > 0 ? (const void *)k_pcg_persistent<3, false> : (const void *)k_pcg_persistent<0, false>),
-                        K == 4 ? (const void *)k_pcg_persistent<4, true>
-                               : (K > 0 ? (const void *)k_pcg_persistent<3, true> : (const void *)k_pcg_persistent<0, true>),
-                        K == 4 ? (const void *)k_pcg_persistent<4, false, true>
-                               : (K > 0 ? (const void *)k_pcg_persistent<3, false, true>
-                                        : (const void *)k_pcg_persistent<0, false, true>)};
-  int best = 1 << 30;
-  for (const void *fn : fns) {
+// co-resident grid for every persistent variant that may be launched on a
+// mesh (any row layout: the full-row rows are chosen after this call)
+template <int KE>
+static void persistent_occupancy(int &best) {
+  int nb = 0;
+  for (const void *fn : {(const void *)k_pcg_persistent<KE, false>, (const void *)k_pcg_persistent<KE, true>}) {
     LF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, BS, 0));
     best = std::min(best, nb);
   }
-  // the L2-resident variant with its shared-memory stash
-  for (int h = 0; h < 2; ++h) {  // the L2-resident variants (single rank / halo) with the stash
-    const void *fi = h ? (K == 4 ? (const void *)k_pcg_persistent<4, true, true>
-                                 : (K > 0 ? (const void *)k_pcg_persistent<3, true, true>
-                                          : (const void *)k_pcg_persistent<0, true, true>))
-                       : (K == 4 ? (const void *)k_pcg_persistent<4, false, true>
-                                 : (K > 0 ? (const void *)k_pcg_persistent<3, false, true>
-                                          : (const void *)k_pcg_persistent<0, false, true>));
+  // the L2-resident variants with the shared-memory stash
+  for (const void *fi : {(const void *)k_pcg_persistent<KE, false, true>, (const void *)k_pcg_persistent<KE, true, true>}) {
     LF_CUDA(cudaFuncSetAttribute(fi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stash_bytes()));
     LF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fi, BS, stash_bytes()));
     best = std::min(best, nb);
+  }
+}
+
+int persistent_grid(int device, int K) {
+  int sms = 0;
+  LF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  int best = 1 << 30;
+  if (K == 4)
+    persistent_occupancy<4>(best);
+  else if (K > 0)
+    persistent_occupancy<3>(best);
+  else {
+    persistent_occupancy<0>(best);
+    persistent_occupancy<-6>(best);
+    persistent_occupancy<-8>(best);
   }
   return sms * (best < 1 ? 1 : best);
 }
@@ -1245,6 +1273,8 @@ template <bool HALO, bool IDLE = false>
 static const void *persistent_fn(const MeshDev &m) {
   return (!LF_NO_ELL && m.K == 4) ? (const void *)k_pcg_persistent<4, HALO, IDLE>
          : (!LF_NO_ELL && m.K > 0) ? (const void *)k_pcg_persistent<3, HALO, IDLE>
+         : m.KS == 6               ? (const void *)k_pcg_persistent<-6, HALO, IDLE>
+         : m.KS == 8               ? (const void *)k_pcg_persistent<-8, HALO, IDLE>
                                    : (const void *)k_pcg_persistent<0, HALO, IDLE>;
 }
 

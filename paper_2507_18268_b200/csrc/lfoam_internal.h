@@ -91,6 +91,10 @@ struct MeshDev {
   // slot k of cell c at k*n + c.  See kernels.cu header.
   int32_t K, ldE;  // ldE: slab stride (n rounded up to 4: 16-byte aligned slabs)
   const int32_t *nbrE, *loE;
+  // full-row ELL (the DIC rows, DicDev): used by the Amul gathers of meshes
+  // with more than 4 faces on a side (K == 0) and at most 8 neighbours
+  int32_t KS, ldS;
+  const int32_t *symN;
   // spatially varying DT (§8(f) row 2): face / boundary diffusivities, or
   // null (the scalar DT argument of the kernels)
   const double *gammaF, *gammaB;

@@ -6,6 +6,10 @@
 
 #include "host.h"
 
+#ifndef LF_NO_SYM_ROWS
+#define LF_NO_SYM_ROWS 0  // 1: meshes with K > 4 keep the CSR gather (ablation)
+#endif
+
 namespace lf {
 
 // Reverse Cuthill-McKee on the cell graph (host, once per mesh).  Returns
@@ -472,6 +476,9 @@ static void build_mesh(lf_context *ctx, const lf_mesh_desc *d, lf_mesh *M) {
   md.K = 0;
   md.nbrE = md.loE = nullptr;
   L.upperE = nullptr;
+  md.KS = md.ldS = 0;  // full-row ELL: built at the end for K > 4 meshes
+  md.symN = nullptr;
+  L.symU = nullptr;
   if (F > 0 && n < (1 << 29)) {
     std::vector<int32_t> hs(n + 1), hl(n + 1);
     LF_CUDA(cudaMemcpyAsync(hs.data(), ownerStart, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost, s));
@@ -594,6 +601,21 @@ static void build_mesh(lf_context *ctx, const lf_mesh_desc *d, lf_mesh *M) {
   } else {
     M->nTotal = nloc;
   }
+  // ---------------------------------------------- full-row ELL (K > 4)
+  // Meshes with more than 4 faces on a side (e.g. randomly numbered ones)
+  // take the full-row rows of the DIC for the Amul gathers when every cell
+  // has at most 8 neighbours: labels and coefficients coalesced, no
+  // start offsets, no face -> coefficient indirection; else the CSR gather.
+  if (md.K == 0 && F > 0 && n < (1 << 29) && !LF_NO_SYM_ROWS) {
+    std::vector<int32_t> hs(n + 1), hl(n + 1);
+    LF_CUDA(cudaMemcpyAsync(hs.data(), ownerStart, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost, s));
+    LF_CUDA(cudaMemcpyAsync(hl.data(), losortStart, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost, s));
+    LF_CUDA(cudaStreamSynchronize(s));
+    int32_t deg = 0;
+    for (int32_t c = 0; c < n; ++c) deg = std::max(deg, (hs[c + 1] - hs[c]) + (hl[c + 1] - hl[c]));
+    if (deg <= 8) build_rows(M);
+  }
+
   LF_CUDA(cudaStreamSynchronize(s));
   LF_CUDA(cudaGetLastError());
   M->ldu.mesh = M;

@@ -23,8 +23,13 @@ void require_dic(const lf_mesh *M) {
 
 void ensure_dic(lf_mesh *M) {
   require_dic(M);
+  build_rows(M);
+}
+
+void build_rows(lf_mesh *M) {
   cudaStream_t s = M->ctx->stream;
   if (!M->dicBuilt) {
+    LF_REQUIRE(M->n < DIC_L0BIT, "full-row ELL needs n_cells < 2^30");
     const int32_t n = M->n, F = M->F;
     std::vector<int32_t> os(n + 1), nb(F), ls(n + 1), lo(F);
     LF_CUDA(cudaMemcpyAsync(os.data(), M->md.ownerStart, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost, s));
@@ -95,6 +100,11 @@ void ensure_dic(lf_mesh *M) {
     LF_CUDA(cudaStreamSynchronize(s));  // host vectors are released on return
     M->ld.symU = symU;
     M->ld.ldS = ld;
+    for (lf::MeshDev *md : {&M->md, &M->mdVar}) {
+      md->KS = KS;
+      md->ldS = ld;
+      md->symN = dSymN;
+    }
     M->dicBuilt = true;
     if (M->ldu.assembled)
       M->ctx->launch(LF_K_PRECOND, [&] { launch_sym_fill(s, M->Lamul, M->md, M->ld); });
