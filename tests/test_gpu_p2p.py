@@ -30,14 +30,15 @@ def P():
     return _P
 
 
-@pytest.mark.parametrize("persistent", [True, False])
-def test_p2p_loopback_single_process(P, persistent):
+@pytest.mark.parametrize("persistent,variant", [(True, 0), (False, 0), (True, 2)])
+def test_p2p_loopback_single_process(P, persistent, variant):
     m = meshgen.block_mesh(14, 12, 16, bc={"ymin": ("fixedValue", 1.0)})
     c = decompose.cut_mesh(m, decompose.z_plane_faces(m, 7))
     s = meshgen.multimode_field(m)
     To, _, po = oracle.laplacian_foam(m, s, 4)
     ctx = P.Context(0)
     ctx.set_option("persistent", persistent)
+    ctx.set_option("variant", variant)
     ctx.p2p_init(1, 0)
     mesh = P.Mesh(ctx, c)
     mesh.p2p_connect([mesh.p2p_export()], 0)
@@ -102,7 +103,7 @@ def _free_port():
         return sk.getsockname()[1]
 
 
-def _rank_main(rank, world, port, persistent, out, precond="diagonal"):
+def _rank_main(rank, world, port, persistent, out, precond="diagonal", variant=0):
     import torch.distributed as dist
     import paper_2507_18268_b200 as P
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -114,6 +115,7 @@ def _rank_main(rank, world, port, persistent, out, precond="diagonal"):
         m, cells = decompose.local_mesh(g, part, rank)
         ctx = P.Context(0)
         ctx.set_option("persistent", persistent)
+        ctx.set_option("variant", variant)
         ctx.p2p_init(world, rank)
         mesh = P.Mesh(ctx, m)
         hs = [None] * world
@@ -139,15 +141,18 @@ def _rank_main(rank, world, port, persistent, out, precond="diagonal"):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("persistent,world", [(False, 2), (True, 2), (True, 3)])
-def test_p2p_two_processes_one_gpu(P, persistent, world):
-    """world = 3: the middle rank has two processor patches (an interior slab)."""
+@pytest.mark.parametrize("persistent,world,variant", [(False, 2, 0), (True, 2, 0), (True, 3, 0), (True, 2, 2)])
+def test_p2p_two_processes_one_gpu(P, persistent, world, variant):
+    """world = 3: the middle rank has two processor patches (an interior slab);
+    variant = 2 forces the HBM-bound persistent variant on the halo path (the
+    small test meshes otherwise take the L2-resident one)."""
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     mgr = ctx.Manager()
     out = mgr.dict()
     port = _free_port()
-    procs = [ctx.Process(target=_rank_main, args=(r, world, port, persistent, out)) for r in range(world)]
+    procs = [ctx.Process(target=_rank_main, args=(r, world, port, persistent, out, "diagonal", variant))
+             for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
