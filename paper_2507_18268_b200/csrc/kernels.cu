@@ -1306,6 +1306,11 @@ void launch_amul(cudaStream_t s, const Launch &L, const MeshDev &m, const LduDev
   LF_DISPATCH_KE(m, k_amul, <<<L.grid, BS, 0, s>>>(m, a, halo, x, y));
 }
 
+// ------------------------------------------------------ solver controls
+__global__ void k_set_ctl(PcgCtl *ctl, PcgCtl v) { *ctl = v; }
+
+void launch_set_ctl(cudaStream_t s, PcgCtl *ctl, const PcgCtl &value) { k_set_ctl<<<1, 1, 0, s>>>(ctl, value); }
+
 // ------------------------------------------------------------ halo packs
 __global__ void k_pack_x(int32_t ns, const int32_t *__restrict__ cells, const double *__restrict__ x,
                          double *__restrict__ buf) {

@@ -219,6 +219,7 @@ void launch_diag_precondition(cudaStream_t s, const Launch &L, int32_t n, const 
                               const double *r, double *w);
 void launch_pack_x(cudaStream_t s, int32_t nsend, const int32_t *cells, const double *x,
                    double *buf);
+void launch_set_ctl(cudaStream_t s, PcgCtl *ctl, const PcgCtl &value);  // *ctl = value, stream-ordered
 void launch_permute(cudaStream_t s, int32_t n, const int32_t *idx, const double *in, double *out,
                     bool scatter);
 void launch_gather_f64(cudaStream_t s, int64_t n, const int32_t *idx, const double *in,

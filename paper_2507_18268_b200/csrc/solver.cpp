@@ -61,9 +61,10 @@ void upload_controls(lf_mesh *M, const lf_solver_controls *c, double *psi) {
   h->psi = psi;
   h->precond = c->preconditioner;
   h->stop = 1;  // nothing runs until a setup kernel resets it
-  LF_CUDA(cudaMemcpyAsync(M->ws.ctl, h, sizeof(PcgCtl), cudaMemcpyHostToDevice, M->ctx->stream));
-  // the pinned mirror is read by the copy engine asynchronously: wait before reuse
-  LF_CUDA(cudaStreamSynchronize(M->ctx->stream));
+  // passed by value to a one-thread kernel: stream-ordered, no host sync
+  // (a host->device copy from the pinned mirror would have to be waited for
+  // before the mirror is reused — a host round trip inside every step)
+  M->ctx->launch(LF_K_SETUP, [&] { launch_set_ctl(M->ctx->stream, M->ws.ctl, *h); });
 }
 
 // Host-side halo of a cell field (NCCL / local copies): x at the send cells
