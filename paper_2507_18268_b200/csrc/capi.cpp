@@ -17,6 +17,7 @@ template <class F>
 static lf_status guard(F &&fn, lf_mesh *M = nullptr) {
   try {
     if (M && M->broken) throw Error{LF_ERR_STATE, "mesh unusable after an earlier CUDA/NCCL error"};
+    if (M && M->ctx) LF_CUDA(cudaSetDevice(M->ctx->device));  // the mesh's device, whatever the caller's current one
     fn();
     return LF_OK;
   } catch (const Error &e) {
