@@ -33,6 +33,9 @@
 #ifndef LF_DIC_REVERSE
 #define LF_DIC_REVERSE 1  // 1: the 2-level forward sweep in reverse trip order (L2 reuse);
 #endif                    // 2: every pass reversed on alternate iterations
+#ifndef LF_DIC_STASH
+#define LF_DIC_STASH 1   // L2-resident DIC solve keeps {q, rD} on chip (see k_pcg_dic)
+#endif
 #ifndef LF_DIC_PAIR
 #define LF_DIC_PAIR 1    // phase 1 interleaves the two colours (thread t: cell t of each) in the
 #endif                   // HBM-bound variant (r1x: 200^3 39.2 vs 39.9 ms/step; 100^3 3.37 vs 3.13)
@@ -94,7 +97,7 @@ __device__ __forceinline__ int sym_cell(int lab) { return lab & (DIC_L0BIT - 1);
 
 // calcReciprocalD for a cell on level >= 1 (its lower neighbours are final)
 template <int KS>
-__device__ __forceinline__ void dic_factor_cell(const DicDev &d, const LduDev &a, int c) {
+__device__ __forceinline__ double dic_factor_cell(const DicDev &d, const LduDev &a, int c) {
   SymRow<KS> R;
   load_row<KS>(d, a, c, R);
   double rdu = a.diag[c];
@@ -108,7 +111,9 @@ __device__ __forceinline__ void dic_factor_cell(const DicDev &d, const LduDev &a
     }
   }
   d.rDu[c] = rdu;
-  d.rD[c] = __ddiv_rn(1.0, rdu);
+  const double rd = __ddiv_rn(1.0, rdu);
+  d.rD[c] = rd;
+  return rd;
 }
 
 // r of a cell after this iteration's update (upd) — identical operation
@@ -122,12 +127,13 @@ __device__ __forceinline__ double r_new(const double *r, const double *q, bool u
 template <int KS>
 __device__ __forceinline__ double dic_forward_cell(const DicDev &d, const LduDev &a, int c, double *r,
                                                    const double *q, double *w, bool upd, double alpha,
-                                                   double &wOut) {
+                                                   double &wOut, const double2 *own = nullptr) {
+  // own: {q_c, rD_c} from the shared-memory stash instead of global memory
   SymRow<KS> R;
   load_row<KS>(d, a, c, R);
-  const double rc = r_new(r, q, upd, alpha, c);
+  const double rc = own ? (upd ? fma(-alpha, own->x, r[c]) : r[c]) : r_new(r, q, upd, alpha, c);
   if (upd) r[c] = rc;
-  const double rd = d.rD[c];
+  const double rd = own ? own->y : d.rD[c];
   double wv = __dmul_rn(rd, rc);
 #pragma unroll
   for (int k = 0; k < KS; ++k) {
@@ -148,13 +154,13 @@ __device__ __forceinline__ double dic_forward_cell(const DicDev &d, const LduDev
 template <int KS>
 __device__ __forceinline__ double dic_backward_cell(const DicDev &d, const LduDev &a, int c, bool level0,
                                                     double *r, const double *q, double *w, bool upd,
-                                                    double alpha, double &wOut) {
+                                                    double alpha, double &wOut, const double2 *own = nullptr) {
   SymRow<KS> R;
   load_row<KS>(d, a, c, R);
-  const double rd = d.rD[c];
+  const double rd = own ? own->y : d.rD[c];
   double rc, wv;
   if (level0) {
-    rc = r_new(r, q, upd, alpha, c);
+    rc = own ? (upd ? fma(-alpha, own->x, r[c]) : r[c]) : r_new(r, q, upd, alpha, c);
     if (upd) r[c] = rc;
     wv = __dmul_rn(rd, rc);
   } else {
@@ -184,9 +190,39 @@ template <int KS, bool HALO, class Idle = NoIdle>
 __device__ __forceinline__ void dic_apply(const MeshDev &m, const DicDev &d, const LduDev &a, double *r,
                                           const double *q, double *w, bool upd, double alpha, unsigned *bar,
                                           double *partials, double *out, const P2PDev &pp,
-                                          Idle idle = Idle(), bool odd = false) {
+                                          Idle idle = Idle(), bool odd = false, const double2 *stash = nullptr,
+                                          int n = 0) {
   const int L = d.L;
   double v[2] = {0.0, 0.0};
+  if (stash) {
+    // two contiguous levels, each thread's cells at the Amul-phase mapping
+    // c = gtid + i*S with {q, rD} of trip i in stash[i*BS + tid]
+    const int S = gridDim.x * blockDim.x, gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int T = (n + S - 1) / S, n0 = __ldg(d.lvlStart + 1);
+    for (int i = T - 1; i >= 0; --i) {  // forward sweep of level 1, backwards (L2 reuse)
+      const int c = gtid + i * S;
+      if (c >= n0 && c < n) {
+        double wc;
+        const double rc = dic_forward_cell<KS>(d, a, c, r, q, w, upd, alpha, wc, &stash[i * BS + threadIdx.x]);
+        v[0] += fabs(rc);
+        v[1] = fma(wc, rc, v[1]);
+        if (HALO && pp.P > 0) push_halo(m, pp.dstW, c, wc);
+      }
+    }
+    grid_barrier(bar);
+    for (int i = 0; i < T; ++i) {  // backward sweep of level 0
+      const int c = gtid + i * S;
+      if (c < n0) {
+        double wc;
+        const double rc = dic_backward_cell<KS>(d, a, c, true, r, q, w, upd, alpha, wc, &stash[i * BS + threadIdx.x]);
+        v[0] += fabs(rc);
+        v[1] = fma(wc, rc, v[1]);
+        if (HALO && pp.P > 0) push_halo(m, pp.dstW, c, wc);
+      }
+    }
+    grid_reduce_sync<2, HALO>(v, partials, bar, out, pp LF_DBG_ARG(0), idle);
+    return;
+  }
   for (int l = 1; l < L; ++l) {
     auto fwd = [&](int t) {
       const int c = level_cell(d, t);
@@ -234,7 +270,7 @@ __device__ __forceinline__ void dic_amul_cell(const MeshDev &m, const LduDev &a,
                                               const Workspace &ws, int k, int c, bool first, bool cont,
                                               double alpha, double beta, double *psi, const double *w,
                                               const double *pold, double *pnew, double *q, double (&v1)[2],
-                                              bool idleF) {
+                                              bool idleF, double *qOut = nullptr, bool writeQ = true) {
   if (idleF) {  // psi was updated in the previous beta-barrier wait
     if (first) v1[1] += psi[c];
   } else {
@@ -261,7 +297,8 @@ __device__ __forceinline__ void dic_amul_cell(const MeshDev &m, const LduDev &a,
     for (int kk = 0; kk < KS; ++kk)
       if (R.lab[kk] >= 0) qc = fma(R.u[kk], pn[kk], qc);
     if (HALO) qc -= row_proc_p(m, a.bBnd, ws, first, beta, k, c);
-    q[c] = qc;
+    if (writeQ) q[c] = qc;
+    if (qOut) *qOut = qc;
     v1[0] = fma(pc, qc, v1[0]);
   }
 }
@@ -294,6 +331,15 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
   double psiSum = 0.0;
   double *psi = ctl->psi;
   double *r = ws.r, *w = ws.w, *q = ws.q;
+  // L2-resident variant, two contiguous levels, <= LF_STASH_TRIPS trips per
+  // thread (LF_DIC_STASH): {q, rD} of the thread's cells stay in shared
+  // memory (slot = trip of the Amul-phase mapping c = gtid + i*S) — q of
+  // level-1 cells is never written to global memory and the sweeps read
+  // their own q and rD on chip
+  extern __shared__ double2 lf_dstash[];
+  const int nTrips = (m.n + stride - 1) / stride;
+  const bool stash = LF_DIC_STASH && IDLE && d.contig && L == 2 && nTrips <= LF_STASH_TRIPS;
+  const int n0s = stash ? __ldg(d.lvlStart + 1) : 0;
 
   if (threadIdx.x == 0) {
     st.k = ctl->it;
@@ -310,7 +356,26 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
     st.cont = ctl->minIter > 0 || !conv(st.finRes, st.initRes, ctl);
   }
   __syncthreads();
-  if (st.cont) {
+  if (st.cont && stash) {
+    // calcReciprocalD of both levels in one pass at the Amul-phase mapping
+    // (level 1 reads only diag of its level-0 neighbours), rD stashed
+    for (int i = 0; i < nTrips; ++i) {
+      const int c = gtid + i * stride;
+      if (c < m.n) {
+        double rd;
+        if (c < n0s) {
+          rd = __ddiv_rn(1.0, a.diag[c]);
+          d.rD[c] = rd;
+        } else {
+          rd = dic_factor_cell<KS>(d, a, c);
+        }
+        lf_dstash[i * BS + threadIdx.x].y = rd;
+      }
+    }
+    grid_barrier(bar);
+    dic_apply<KS, HALO>(m, d, a, r, q, w, false, 0.0, bar, ws.partials, ws.gsum->p2, pp, NoIdle(), false,
+                        lf_dstash, m.n);  // set-up w (q unused)
+  } else if (st.cont) {
     // ---- calcReciprocalD: levels 0 and 1 in one pass (level 1 reads only
     // diag of level-0 cells), then one pass per level
     for (int l = 0; l < L; ++l) {
@@ -365,6 +430,16 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
         grid_range_rev(0, nt, two);
       else
         for (int t = gtid; t < nt; t += stride) two(t);
+    } else if (stash) {
+      for (int i = 0; i < nTrips; ++i) {
+        const int c = gtid + i * stride;
+        if (c < m.n) {
+          double qc;
+          dic_amul_cell<KS, HALO>(m, a, d, ws, k, c, first, cont, alpha, beta, psi, w, pold, pnew, q, v1, idleF,
+                                  &qc, c < n0s);  // level-0 q is read by neighbours: global
+          if (cont) lf_dstash[i * BS + threadIdx.x].x = qc;
+        }
+      }
     } else {
       auto one = [&](int c) {
         dic_amul_cell<KS, HALO>(m, a, d, ws, k, c, first, cont, alpha, beta, psi, w, pold, pnew, q, v1, idleF);
@@ -397,7 +472,7 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
       });
     };
     dic_apply<KS, HALO>(m, d, a, r, q, w, true, alphaK, bar, ws.partials, ws.gsum->p2, pp, flush,
-                        LF_DIC_REVERSE == 2 && L == 2 && (st.k & 1));
+                        LF_DIC_REVERSE == 2 && L == 2 && (st.k & 1), stash ? lf_dstash : nullptr, m.n);
     if (threadIdx.x == 0) ++st.k;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -423,7 +498,9 @@ int dic_grid(int device, int KS) {
   LF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
   for (const void *fn : {dic_fn<false>(KS), dic_fn<true>(KS), dic_fn<false, true>(KS)}) {  // co-resident for all
     int nb = 0;
-    LF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, BS, 0));
+    const size_t sm = fn == dic_fn<false, true>(KS) ? stash_bytes() : 0;  // the L2 variant's stash
+    if (sm) LF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    LF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, BS, sm));
     best = std::min(best, nb);
   }
   return sms * (best < 1 ? 1 : best);
@@ -433,10 +510,9 @@ void launch_pcg_dic(cudaStream_t s, int grid, const MeshDev &m, const LduDev &a,
                     const Workspace &ws, unsigned *bar) {
   void *args[] = {(void *)&m, (void *)&a, (void *)&d, (void *)&ws, (void *)&bar};
   const bool halo = m.hasProc || ws.p2p.P > 0;
-  const void *fn = halo                              ? dic_fn<true>(d.KS)
-                   : (LF_IDLE_FLUSH && ws.idleFlush) ? dic_fn<false, true>(d.KS)
-                                                     : dic_fn<false>(d.KS);
-  LF_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(BS), args, 0, s));
+  const bool idle = !halo && LF_IDLE_FLUSH && ws.idleFlush;
+  const void *fn = halo ? dic_fn<true>(d.KS) : idle ? dic_fn<false, true>(d.KS) : dic_fn<false>(d.KS);
+  LF_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(BS), args, idle ? stash_bytes() : 0, s));
 }
 
 // ------------------------------------------- full-row coefficients (fill)

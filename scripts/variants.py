@@ -14,10 +14,8 @@ sys.path.insert(0, ROOT)
 
 # name -> (-D defines, bench --mode[, bench --precond])
 VARIANTS = {
-    "dic_rev1_unal": ([], "persistent", "DIC"),
-    "dic_rev1_al": (["LF_REV_ALIGN=1"], "persistent", "DIC"),
-    "dic_rev2_unal": (["LF_DIC_REVERSE=2"], "persistent", "DIC"),
-    "dic_rev0": (["LF_DIC_REVERSE=0"], "persistent", "DIC"),
+    "dic_stash": ([], "persistent", "DIC"),
+    "dic_nostash": (["LF_DIC_STASH=0"], "persistent", "DIC"),
 }
 
 
