@@ -496,9 +496,9 @@ static const void *dic_fn(int KS) {
 int dic_grid(int device, int KS) {
   int sms = 0, best = 1 << 30;
   LF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-  for (const void *fn : {dic_fn<false>(KS), dic_fn<true>(KS), dic_fn<false, true>(KS)}) {  // co-resident for all
-    int nb = 0;
-    const size_t sm = fn == dic_fn<false, true>(KS) ? stash_bytes() : 0;  // the L2 variant's stash
+  for (const void *fn : {dic_fn<false>(KS), dic_fn<true>(KS), dic_fn<false, true>(KS), dic_fn<true, true>(KS)}) {
+    int nb = 0;  // co-resident for all variants; the L2 ones carry the stash
+    const size_t sm = (fn == dic_fn<false, true>(KS) || fn == dic_fn<true, true>(KS)) ? stash_bytes() : 0;
     if (sm) LF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     LF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, BS, sm));
     best = std::min(best, nb);
@@ -510,8 +510,9 @@ void launch_pcg_dic(cudaStream_t s, int grid, const MeshDev &m, const LduDev &a,
                     const Workspace &ws, unsigned *bar) {
   void *args[] = {(void *)&m, (void *)&a, (void *)&d, (void *)&ws, (void *)&bar};
   const bool halo = m.hasProc || ws.p2p.P > 0;
-  const bool idle = !halo && LF_IDLE_FLUSH && ws.idleFlush;
-  const void *fn = halo ? dic_fn<true>(d.KS) : idle ? dic_fn<false, true>(d.KS) : dic_fn<false>(d.KS);
+  const bool idle = LF_IDLE_FLUSH && ws.idleFlush;  // L2-resident variant, single rank or halo
+  const void *fn = halo ? (idle ? dic_fn<true, true>(d.KS) : dic_fn<true>(d.KS))
+                        : (idle ? dic_fn<false, true>(d.KS) : dic_fn<false>(d.KS));
   LF_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(BS), args, idle ? stash_bytes() : 0, s));
 }
 
