@@ -921,6 +921,9 @@ bool persistent_chunked() { return LF_CHUNKED != 0; }
 #ifndef LF_REVERSE
 #define LF_REVERSE 1  // persistent phase 2 sweeps the trips in reverse order (L2 reuse)
 #endif
+#ifndef LF_STASH_DIAG
+#define LF_STASH_DIAG 1  // L2-resident variant: diag re-read from the stash after iteration 0
+#endif
 #ifndef LF_STASH_TRIPS
 #define LF_STASH_TRIPS 8  // L2-resident variant: at most this many grid-stride trips per thread
 #endif
@@ -1058,7 +1061,13 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
       if (cont) {
         const double pc = first ? w[c] : fma(beta, pold[c], w[c]);
         pnew[c] = pc;
+#if LF_TAIL
+        // the L2-resident variant reads diag from HBM once per solve: later
+        // iterations take it from the stash slot it stays in
+        const double dc = (IDLE && LF_STASH_DIAG && !first) ? lf_stash[i * BS + threadIdx.x].y : a.diag[c];
+#else
         const double dc = a.diag[c];
+#endif
         double q = dc * pc;
         q = row_offdiag<KE>(m, a, c, q, pnb);
         if (HALO) q -= row_proc_p(m, a.bBnd, ws, first, beta, k, c);

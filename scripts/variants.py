@@ -14,8 +14,8 @@ sys.path.insert(0, ROOT)
 
 # name -> (-D defines, bench --mode[, bench --precond])
 VARIANTS = {
-    "dic_stash": ([], "persistent", "DIC"),
-    "dic_nostash": (["LF_DIC_STASH=0"], "persistent", "DIC"),
+    "stashdiag": ([], "persistent"),
+    "nostashdiag": (["LF_STASH_DIAG=0"], "persistent"),
 }
 
 
