@@ -36,6 +36,9 @@
 #ifndef LF_DIC_STASH
 #define LF_DIC_STASH 1   // L2-resident DIC solve keeps {q, rD} on chip (see k_pcg_dic)
 #endif
+#ifndef LF_DIC_STASH_DIAG
+#define LF_DIC_STASH_DIAG 0  // ... and diag (phase 1 reads it from the stash after iteration 0)
+#endif
 #ifndef LF_DIC_PAIR
 #define LF_DIC_PAIR 1    // phase 1 interleaves the two colours (thread t: cell t of each) in the
 #endif                   // HBM-bound variant (r1x: 200^3 39.2 vs 39.9 ms/step; 100^3 3.37 vs 3.13)
@@ -270,7 +273,8 @@ __device__ __forceinline__ void dic_amul_cell(const MeshDev &m, const LduDev &a,
                                               const Workspace &ws, int k, int c, bool first, bool cont,
                                               double alpha, double beta, double *psi, const double *w,
                                               const double *pold, double *pnew, double *q, double (&v1)[2],
-                                              bool idleF, double *qOut = nullptr, bool writeQ = true) {
+                                              bool idleF, double *qOut = nullptr, bool writeQ = true,
+                                              double *dSlot = nullptr) {
   if (idleF) {  // psi was updated in the previous beta-barrier wait
     if (first) v1[1] += psi[c];
   } else {
@@ -292,7 +296,14 @@ __device__ __forceinline__ void dic_amul_cell(const MeshDev &m, const LduDev &a,
       const int j = sym_cell(R.lab[kk]);
       pn[kk] = R.lab[kk] >= 0 ? (first ? w[j] : fma(beta, pold[j], w[j])) : 0.0;
     }
-    double qc = a.diag[c] * pc;
+    double dc;
+    if (dSlot) {  // stashed diag: global on the first iteration only
+      if (first) *dSlot = a.diag[c];
+      dc = *dSlot;
+    } else {
+      dc = a.diag[c];
+    }
+    double qc = dc * pc;
 #pragma unroll
     for (int kk = 0; kk < KS; ++kk)
       if (R.lab[kk] >= 0) qc = fma(R.u[kk], pn[kk], qc);
@@ -337,6 +348,7 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
   // level-1 cells is never written to global memory and the sweeps read
   // their own q and rD on chip
   extern __shared__ double2 lf_dstash[];
+  double *lf_ddiag = reinterpret_cast<double *>(lf_dstash + LF_STASH_TRIPS * BS);  // LF_DIC_STASH_DIAG
   const int nTrips = (m.n + stride - 1) / stride;
   const bool stash = LF_DIC_STASH && IDLE && d.contig && L == 2 && nTrips <= LF_STASH_TRIPS;
   const int n0s = stash ? __ldg(d.lvlStart + 1) : 0;
@@ -436,7 +448,8 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
         if (c < m.n) {
           double qc;
           dic_amul_cell<KS, HALO>(m, a, d, ws, k, c, first, cont, alpha, beta, psi, w, pold, pnew, q, v1, idleF,
-                                  &qc, c < n0s);  // level-0 q is read by neighbours: global
+                                  &qc, c < n0s,  // level-0 q is read by neighbours: global
+                                  LF_DIC_STASH_DIAG ? lf_ddiag + i * BS + threadIdx.x : nullptr);
           if (cont) lf_dstash[i * BS + threadIdx.x].x = qc;
         }
       }
@@ -493,12 +506,16 @@ static const void *dic_fn(int KS) {
   return KS <= 6 ? (const void *)k_pcg_dic<6, HALO, IDLE> : (const void *)k_pcg_dic<8, HALO, IDLE>;
 }
 
+static size_t dic_stash_bytes() {
+  return stash_bytes() + (LF_DIC_STASH_DIAG ? (size_t)LF_STASH_TRIPS * BS * sizeof(double) : 0);
+}
+
 int dic_grid(int device, int KS) {
   int sms = 0, best = 1 << 30;
   LF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
   for (const void *fn : {dic_fn<false>(KS), dic_fn<true>(KS), dic_fn<false, true>(KS), dic_fn<true, true>(KS)}) {
     int nb = 0;  // co-resident for all variants; the L2 ones carry the stash
-    const size_t sm = (fn == dic_fn<false, true>(KS) || fn == dic_fn<true, true>(KS)) ? stash_bytes() : 0;
+    const size_t sm = (fn == dic_fn<false, true>(KS) || fn == dic_fn<true, true>(KS)) ? dic_stash_bytes() : 0;
     if (sm) LF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     LF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, BS, sm));
     best = std::min(best, nb);
@@ -513,7 +530,7 @@ void launch_pcg_dic(cudaStream_t s, int grid, const MeshDev &m, const LduDev &a,
   const bool idle = LF_IDLE_FLUSH && ws.idleFlush;  // L2-resident variant, single rank or halo
   const void *fn = halo ? (idle ? dic_fn<true, true>(d.KS) : dic_fn<true>(d.KS))
                         : (idle ? dic_fn<false, true>(d.KS) : dic_fn<false>(d.KS));
-  LF_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(BS), args, idle ? stash_bytes() : 0, s));
+  LF_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(BS), args, idle ? dic_stash_bytes() : 0, s));
 }
 
 // ------------------------------------------- full-row coefficients (fill)

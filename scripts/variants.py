@@ -14,8 +14,8 @@ sys.path.insert(0, ROOT)
 
 # name -> (-D defines, bench --mode[, bench --precond])
 VARIANTS = {
-    "stashdiag": ([], "persistent"),
-    "nostashdiag": (["LF_STASH_DIAG=0"], "persistent"),
+    "dicdiag0": ([], "persistent", "DIC"),
+    "dicdiag1": (["LF_DIC_STASH_DIAG=1"], "persistent", "DIC"),
 }
 
 
