@@ -530,7 +530,9 @@ void launch_pcg_dic(cudaStream_t s, int grid, const MeshDev &m, const LduDev &a,
   const bool idle = LF_IDLE_FLUSH && ws.idleFlush;  // L2-resident variant, single rank or halo
   const void *fn = halo ? (idle ? dic_fn<true, true>(d.KS) : dic_fn<true>(d.KS))
                         : (idle ? dic_fn<false, true>(d.KS) : dic_fn<false>(d.KS));
-  LF_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(BS), args, idle ? dic_stash_bytes() : 0, s));
+  // the diag slots follow LF_STASH_TRIPS full {q, rD} rows: fit only without them
+  const size_t smem = LF_DIC_STASH_DIAG ? dic_stash_bytes() : stash_fit(m.n, grid, sizeof(double2));
+  LF_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(BS), args, idle ? smem : 0, s));
 }
 
 // ------------------------------------------- full-row coefficients (fill)

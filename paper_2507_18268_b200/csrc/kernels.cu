@@ -933,6 +933,16 @@ bool persistent_chunked() { return LF_CHUNKED != 0; }
 bool persistent_tail() { return LF_TAIL != 0; }
 int stash_trips() { return LF_TAIL ? LF_STASH_TRIPS : 0; }
 static size_t stash_bytes() { return (size_t)LF_STASH_TRIPS * BS * sizeof(double2); }
+#ifndef LF_STASH_FIT
+#define LF_STASH_FIT 1  // launch with only the stash slots the mesh's trips use (more L1 left)
+#endif
+// dynamic shared memory of an L2-resident launch: slot i * BS + thread for
+// the trips i < ceil(n / (grid * BS)) (<= LF_STASH_TRIPS), times `per` bytes
+static size_t stash_fit(int n, int grid, size_t per) {
+  const long long cstep = (long long)grid * BS, trips = (n + cstep - 1) / cstep;
+  const long long t = LF_STASH_FIT ? std::max(1LL, std::min<long long>(trips, LF_STASH_TRIPS)) : LF_STASH_TRIPS;
+  return (size_t)t * BS * per;
+}
 #ifndef LF_P2P_UNROLL
 #define LF_P2P_UNROLL 2  // persistent phase 2 cells per trip
 #endif
@@ -1295,7 +1305,8 @@ void launch_pcg_persistent(cudaStream_t s, int grid, const MeshDev &m, const Ldu
   const bool idle = LF_IDLE_FLUSH && ws.idleFlush;
   const void *fn = halo ? (idle ? persistent_fn<true, true>(m) : persistent_fn<true>(m))
                         : (idle ? persistent_fn<false, true>(m) : persistent_fn<false>(m));
-  LF_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(BS), args, idle ? stash_bytes() : 0, s));
+  LF_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(BS), args,
+                                      idle ? stash_fit(m.n, grid, sizeof(double2)) : 0, s));
 }
 
 // ------------------------------------------------------------------ Amul

@@ -14,8 +14,10 @@ sys.path.insert(0, ROOT)
 
 # name -> (-D defines, bench --mode[, bench --precond])
 VARIANTS = {
-    "dicdiag0": ([], "persistent", "DIC"),
-    "dicdiag1": (["LF_DIC_STASH_DIAG=1"], "persistent", "DIC"),
+    "fit1": ([], "persistent"),
+    "fit0": (["LF_STASH_FIT=0"], "persistent"),
+    "fit1-dic": ([], "persistent", "DIC"),
+    "fit0-dic": (["LF_STASH_FIT=0"], "persistent", "DIC"),
 }
 
 
