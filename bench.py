@@ -386,7 +386,7 @@ def run_ours(args):
         full = oracle_numbering(workload_mesh(cfg, args.corrected, args.dt_field), args.renumber)
         its_gpu = sum(p["n_iterations"] for p in perfs) / len(perfs)
         if n_global <= 2_000_000:
-            steps = args.cpu_steps or 2
+            steps = args.cpu_steps or max(2, min(200, round(12e6 / n_global)))  # ~10 s of oracle work
             rate, secs, po = oracle_rate(full, meshgen.canonical_field(full), steps, args.corrected, args.precond)
             sample = (f"first {steps} laplacianFoam steps of {wname} "
                       f"({secs:.1f} s, PCG iterations {[p['n_iterations'] for p in po]})")
@@ -394,7 +394,7 @@ def run_ours(args):
             # bounded sample: step 0 truncated to `cap` PCG iterations, scaled to
             # the GPU run's mean iterations per step (the oracle does the same
             # work per iteration; assembly is counted once)
-            cap = max(2, int(20 * 8e6 / n_global))
+            cap = max(2, int(80 * 8e6 / n_global))  # ~10-20 s of oracle work
             _, secs, po = oracle_rate_capped(full, meshgen.canonical_field(full), cap, args.corrected, args.precond)
             its_cpu = sum(p["n_iterations"] for p in po) / len(po)
             rate = n_global / (secs * its_gpu / its_cpu)
