@@ -3,9 +3,15 @@
 
 One bench step = one laplacianFoam time step (fvm::ddt + fvm::laplacian
 assembly fused with the PCG setup, then the diagonal-PCG solve to tol 1e-10)
-on the BASELINE config (default: config 2, 100^3 cube, 1M cells).  Metric:
-cell-updates/s = n_cells * steps / device time.  Inputs are resident in HBM;
-L2 is flushed (256 MiB write) between timed steps, outside the events.
+on the BASELINE config (default: config 3, the 200^3 cube with 8M cells —
+the largest single-GPU config and the one SURVEY §8(d) grades the roofline
+on; config 2 is L2-resident).  Metric: cell-updates/s = n_cells * steps /
+device time.  Inputs are resident in HBM (and larger than L2); L2 is also
+flushed (256 MiB write) between timed steps, outside the events.
+
+Roofline bytes: SURVEY §8(d)'s algorithmic count, 88n + 16F per PCG
+iteration + 24n per solve launch (final psi flush); the implementation's own
+byte model is reported beside it as `impl_bytes_per_launch`.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
 N>1: launch under torchrun; the mesh is decomposed into N contiguous cell
@@ -39,10 +45,13 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=0, help="oracle steps for cpu_baseline (0 = auto)")
+    ap.add_argument("--repeats", type=int, default=5,
+                    help="timed passes of K steps (the paper's five executions, P:608): the first is the "
+                         "contract's `value`, all of them give `repeats` mean +- std")
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
                     help="N>1 data path: peer memory (CUDA IPC over NVLink, fused into the kernels) or NCCL")
     ap.add_argument("--renumber", type=int, default=-1,
@@ -50,6 +59,8 @@ def parse():
     ap.add_argument("--precond", default="diagonal", choices=["diagonal", "DIC"],
                     help="PCG preconditioner: the paper's diagonal (P:608), or SURVEY §8(f) row 3's DIC "
                          "(level-scheduled sweeps; 2 levels under the multicolour numbering)")
+    ap.add_argument("--labels", default="compressed", choices=["compressed", "int32"],
+                    help="gather labels of ELL meshes: 16-bit codes (default) or the int32 labels")
     ap.add_argument("--variant", type=int, default=0,
                     help="persistent solve variant: 0 by mesh size, 1 L2-resident, 2 HBM-bound")
     ap.add_argument("--mode", default="persistent", choices=["persistent", "graphs", "direct"],
@@ -154,15 +165,52 @@ def measured_peak():
         return 6650.0, "fallback"
 
 
+DEVICE_SOURCES = ("kernels.cu", "dic.cuh", "nonorth.cu", "gamg.cuh", "lfoam_internal.h")
+
+
+def build_id():
+    """Hash of the device-code sources: ties a committed ncu figure to the
+    build it was measured on (a stale figure is reported as null)."""
+    import hashlib
+    h = hashlib.sha256()
+    d = os.path.join(ROOT, "paper_2507_18268_b200", "csrc")
+    for f in DEVICE_SOURCES:
+        fp = os.path.join(d, f)
+        if os.path.exists(fp):
+            h.update(f.encode())
+            h.update(open(fp, "rb").read())
+    return h.hexdigest()[:12]
+
+
 def ncu_traffic(cfg, kernel):
-    """Per-launch DRAM bytes of `kernel` from the committed ncu summary, or None."""
+    """Per-launch DRAM bytes (read + write) of `kernel` from the committed ncu
+    capture of THIS build (profiles/ncu_traffic.json), else None."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get(f"config{cfg}", {}).get(kernel)
+        e = d.get(f"config{cfg}", {}).get(kernel)
+        if isinstance(e, dict) and e.get("build") == build_id():
+            return e["bytes"], e.get("tag")
     except Exception:
-        return None
+        pass
+    return None, None
+
+
+def host_cpu():
+    """CPU model, sockets and logical cores of this host (lscpu / nproc)."""
+    info = {"model": None, "sockets": None, "nproc": os.cpu_count()}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            k, _, v = line.partition(":")
+            if k.strip() == "Model name" and info["model"] is None:
+                info["model"] = v.strip()
+            elif k.strip() == "Socket(s)":
+                info["sockets"] = int(v.strip()) if v.strip().isdigit() else v.strip()
+    except Exception:
+        pass
+    return info
 
 
 # --------------------------------------------------------------- oracle arm
@@ -198,22 +246,27 @@ def run_reference(args):
     cfg = args.config
     mesh = oracle_numbering(workload_mesh(cfg, args.corrected, args.dt_field), args.renumber)
     T0 = meshgen.canonical_field(mesh)
-    K = min(args.steps, 20)
-    W = min(args.warmup, 1)
+    # bounded sample: the first K' full steps of the same workload (K' <= 20;
+    # ~30 s of oracle work at 200^3, one step at 400^3), no warm-up step above
+    # 2M cells (it would double the run)
+    big = mesh.n_cells > 2_000_000
+    K = min(args.steps, 20) if not big else max(1, min(args.steps, round(16e6 / mesh.n_cells)))
+    W = min(args.warmup, 1) if not big else 0
     if W:
         oracle_rate(mesh, T0, W, args.corrected, args.precond)
     rate, secs, perfs = oracle_rate(mesh, T0, K, args.corrected, args.precond)
     its = [p["n_iterations"] for p in perfs]
     wname = workload_name(cfg, args.corrected, args.dt_field, args.precond)
-    sample = (f"first {K} laplacianFoam steps of {wname} (of --steps {args.steps}); "
-              f"single-threaded C oracle, PCG iterations/step {min(its)}-{max(its)}")
+    sample = (f"first {K} full laplacianFoam steps of {wname} (of --steps {args.steps}); "
+              f"single-threaded C oracle, PCG iterations/step {min(its)}-{max(its)}, {secs:.1f} s")
     line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus,
             "steps": K, "warmup": W, "ms_per_step": secs / K * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": wname, "n_cells": mesh.n_cells, "global_batch": 1,
                        "seq_len": 0, "parallelism": "cpu-1core", "precond": args.precond,
                        "renumber": args.renumber},
-            "cpu_baseline": {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
+                             "host": host_cpu()},
             "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -226,6 +279,23 @@ def oracle_numbering(mesh, renumber):
 
 
 # ----------------------------------------------------------------- GPU arm
+def l2_resident(n, F, device):
+    """The library's variant rule (mesh.cpp): an iteration's working set
+    within 1.5x the L2 -> the L2-resident persistent variant (barrier- and
+    L2-latency-bound, not HBM-bound)."""
+    import torch
+    l2 = torch.cuda.get_device_properties(device).L2_cache_size
+    return (96 * n + 16 * F) <= 1.5 * l2
+
+
+def impl_iter_bytes(n, F, l2res):
+    """What the shipped persistent solve moves per iteration by its own
+    design (DESIGN.md §5): L2-resident variant {q, diag} on chip, 72n + 16F;
+    HBM-bound variant 96n + 16F (w stored)."""
+    return (72 * n + 16 * F) if l2res else (96 * n + 16 * F)
+
+
+
 def run_ours(args):
     import torch
     import paper_2507_18268_b200 as P
@@ -247,6 +317,7 @@ def run_ours(args):
     ctx.set_option("persistent", args.mode == "persistent")
     ctx.set_option("graphs", args.mode != "direct")
     ctx.set_option("variant", args.variant)
+    ctx.set_option("compressed_labels", args.labels == "compressed")
 
     cfg = args.config
     wname = workload_name(cfg, args.corrected, args.dt_field, args.precond)
@@ -308,14 +379,23 @@ def run_ours(args):
         ms = sum(a.elapsed_time(b) for a, b in ev)
         return ms, perfs
 
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
     with ClockSampler(device) as clk:
         total_ms, perfs = timed_pass(False)
-    launches = ctx.launch_count()
-    if dist is not None:
-        t = torch.tensor([total_ms], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+        launches = ctx.launch_count()
+        rep_ms = [total_ms]
+        for _ in range(max(args.repeats, 1) - 1):   # the paper's five executions
+            rep_ms.append(timed_pass(False)[0])
+    total_ms = max_over_ranks(total_ms)
+    rep_ms = [max_over_ranks(x) for x in rep_ms]
     value = n_global * args.steps / (total_ms / 1e3)
+    rep_vals = [n_global * args.steps / (x / 1e3) for x in rep_ms]
 
     # instrumented replay of the same K steps: per-kernel CUDA-event durations
     inst_ms, perfs_i = timed_pass(True)
@@ -329,33 +409,43 @@ def run_ours(args):
     # grad gather (40n + 40F + 37B) + correction gather (40n + 48F), per pass
     bytes_no_pass = 80 * n_local + 88 * F_local + 37 * B_local
     iters = sum(p["n_iterations"] for p in perfs_i)
-    bytes_p1 = 56 * n_local + 16 * F_local          # per full phase-1 launch
-    bytes_p2 = 40 * n_local
+    # SURVEY §8(d) algorithmic bytes: a PCG iteration (2 global syncs, psi
+    # update deferred) = 88n + 16F; phase 1 = 56n + 16F, phase 2 = 32n
+    survey_iter = 88 * n_local + 16 * F_local
+    bytes_p1 = 56 * n_local + 16 * F_local
+    bytes_p2 = 32 * n_local
     peak, peak_kind = measured_peak()
+    l2res = l2_resident(n_local, F_local, device)
     if n_dic > 0:
-        # persistent DIC solve: per iteration the Amul phase
-        # (56n + 16F) + r update and both sweeps (r, q, rD read, r and w
-        # written: 40n; coefficient + label per face per sweep: 24F); per
-        # launch the factor (diag read, rD written, 16n + 12F), the set-up
-        # sweeps (24n + 24F) and the final psi flush (24n)
+        # persistent DIC solve (SURVEY §8(d) has no DIC row, so the
+        # implementation's count is the algorithmic one): per iteration the Amul
+        # phase (56n + 16F) + r update and both sweeps (r, q, rD read, r and w
+        # written: 40n; coefficient + label per face per sweep: 24F); per launch
+        # the factor (16n + 12F), the set-up sweeps (24n + 24F), the psi flush (24n)
         kernel = "k_pcg_dic"
         total_bytes = (iters * (96 * n_local + 40 * F_local)
                        + n_dic * (64 * n_local + 36 * F_local))
+        impl_bytes = total_bytes
         k_launches, k_ms = n_dic, ms_dic
     elif n_pcg > 0:
-        # persistent whole-solve kernel: per launch = its iterations x (96n + 16F)
+        # persistent whole-solve kernel: per launch = its iterations x (88n + 16F)
         # + the final flush pass (psi, p_old read, psi written: 24n)
         kernel = "k_pcg_persistent"
-        total_bytes = iters * (bytes_p1 + bytes_p2) + n_pcg * 24 * n_local
+        total_bytes = iters * survey_iter + n_pcg * 24 * n_local
+        impl_bytes = iters * impl_iter_bytes(n_local, F_local, l2res) + n_pcg * 24 * n_local
         k_launches, k_ms = n_pcg, ms_pcg
     else:
         kernel = "k_phase1"
         total_bytes = bytes_p1 * iters
+        impl_bytes = total_bytes
         k_launches, k_ms = n_p1, ms_p1
     achieved = total_bytes / (k_ms / 1e3) / 1e9 if k_ms > 0 else None
+    avg_launch_ms = k_ms / max(k_launches, 1)
     tkey = (f"{cfg}{'' if args.corrected < 0 else f'-corr{args.corrected}'}{'-dt' if args.dt_field else ''}"
-            f"{'' if args.precond == 'diagonal' else '-' + args.precond.lower()}")
-    traffic = ncu_traffic(tkey, kernel) if ws == 1 else None
+            f"{'' if args.precond == 'diagonal' else '-' + args.precond.lower()}"
+            f"{'-rcm' if args.renumber == 1 else ''}")
+    traffic, traffic_tag = ncu_traffic(tkey, kernel) if ws == 1 else (None, None)
+    dram_frac = (traffic / (avg_launch_ms / 1e3) / 1e9 / peak) if traffic and avg_launch_ms > 0 else None
 
     # e2e through the public API with host buffers (pinned), copies inside the region
     T0h = torch.from_numpy(np.ascontiguousarray(T0)).pin_memory()
@@ -388,38 +478,49 @@ def run_ours(args):
         if n_global <= 2_000_000:
             steps = args.cpu_steps or max(2, min(200, round(12e6 / n_global)))  # ~10 s of oracle work
             rate, secs, po = oracle_rate(full, meshgen.canonical_field(full), steps, args.corrected, args.precond)
-            sample = (f"first {steps} laplacianFoam steps of {wname} "
+            sample = (f"first {steps} full laplacianFoam steps of {wname} "
+                      f"({secs:.1f} s, PCG iterations {[p['n_iterations'] for p in po]})")
+        elif n_global <= 16_000_000:
+            # step 0 in full (the canonical mode is self-similar: every step
+            # needs the same iterations, ~15 s of oracle work at 200^3)
+            steps = args.cpu_steps or 1
+            rate, secs, po = oracle_rate(full, meshgen.canonical_field(full), steps, args.corrected, args.precond)
+            sample = (f"first {steps} full laplacianFoam step(s) of {wname} "
                       f"({secs:.1f} s, PCG iterations {[p['n_iterations'] for p in po]})")
         else:
-            # bounded sample: step 0 truncated to `cap` PCG iterations, scaled to
-            # the GPU run's mean iterations per step (the oracle does the same
-            # work per iteration; assembly is counted once)
+            # 64M cells: step 0 truncated to `cap` PCG iterations, scaled to the
+            # GPU run's mean iterations per step (same work per iteration;
+            # assembly counted once) — labelled projected
             cap = max(2, int(80 * 8e6 / n_global))  # ~10-20 s of oracle work
             _, secs, po = oracle_rate_capped(full, meshgen.canonical_field(full), cap, args.corrected, args.precond)
             its_cpu = sum(p["n_iterations"] for p in po) / len(po)
             rate = n_global / (secs * its_gpu / its_cpu)
             sample = (f"step 0 of {wname} capped at {po[0]['n_iterations']} PCG iterations "
                       f"({secs:.1f} s), scaled to {its_gpu:.1f} iterations/step (projected)")
-        cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample}
+        cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample, "host": host_cpu()}
 
     its = [p["n_iterations"] for p in perfs]
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "impl": "ours", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "weak" if ws == 1 else "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": wname, "n_cells": n_global, "steps_per_run": args.steps,
                    "global_batch": 1, "seq_len": 0, "parallelism": "1gpu" if ws == 1 else f"domain{ws}-{args.transport}",
                    "renumber": args.renumber, "mode": args.mode, "precond": args.precond,
-                   "variant": args.variant,
+                   "variant": args.variant, "labels": args.labels,
                    "l2": "flushed between timed steps (256 MiB write)", "tol": TOL,
                    "pcg_iterations_per_step": {"min": min(its), "max": max(its), "mean": sum(its) / len(its)}},
-        "roofline": {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": peak,
-                     "peak_kind": peak_kind, "unit": "GB/s",
+        "roofline": {"bound": "l2/barrier" if l2res else "hbm", "kernel": kernel, "achieved": achieved,
+                     "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None,
-                     "traffic": traffic, "bytes_per_launch": total_bytes / max(k_launches, 1),
+                     "bytes_model": "SURVEY §8(d): 88n+16F per PCG iteration + 24n per launch"
+                                    if kernel != "k_pcg_dic" else "DESIGN.md §5 DIC: 96n+40F per iteration + 64n+36F per launch",
+                     "traffic": traffic, "traffic_ncu_tag": traffic_tag, "dram_frac": dram_frac,
+                     "bytes_per_launch": total_bytes / max(k_launches, 1),
+                     "impl_bytes_per_launch": impl_bytes / max(k_launches, 1),
                      "launches": k_launches,
-                     "avg_launch_ms": k_ms / max(k_launches, 1),
+                     "avg_launch_ms": avg_launch_ms,
                      "share_of_step": k_ms / inst_ms if inst_ms > 0 else None,
                      "mode": args.mode,
                      "phase1": {"achieved": bytes_p1 * iters / (ms_p1 / 1e3) / 1e9 if ms_p1 > 0 else None,
@@ -432,6 +533,9 @@ def run_ours(args):
                                   "avg_launch_ms": ms_no / n_no, "share_of_step": ms_no / inst_ms}
                                  if n_no > 0 and ms_no > 0 else None),
                      "instrumented_ms_per_step": inst_ms / args.steps},
+        "repeats": {"n": len(rep_vals), "mean": statistics.mean(rep_vals),
+                    "std": statistics.stdev(rep_vals) if len(rep_vals) > 1 else 0.0,
+                    "values": rep_vals, "unit": UNIT},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * n_local,
                 "d2h_bytes_per_step": 8 * n_local},

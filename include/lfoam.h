@@ -156,6 +156,14 @@ LF_API lf_status lf_p2p_connect(lf_mesh *mesh, int nranks, int rank, const void 
 LF_API lf_status lf_mesh_info(const lf_mesh *mesh, int32_t *n_cells, int32_t *n_faces,
                        int32_t *n_boundary_faces, int64_t *device_bytes);
 
+/* Gather layout chosen by mesh_create (for tests and reports; any pointer may
+ * be NULL): ell_width = slots per side of the ELL slices (3 or 4; 0 = CSR or
+ * full rows), row_width = slots of the full-row ELL (6 or 8; 0 = none),
+ * label_escapes = compressed-label entries that escape to int32 labels
+ * (-1 = compressed labels not built, LF_OPT_COMPRESSED_LABELS). */
+LF_API lf_status lf_mesh_layout(const lf_mesh *mesh, int32_t *ell_width, int32_t *row_width,
+                                int32_t *label_escapes);
+
 /* Host copies of the addressing built by mesh_create, for tests (internal
  * numbering and face order).  Any pointer may be NULL.
  *   owner_start[n+1], losort[F], losort_start[n+1], face_order[F] (internal
@@ -331,8 +339,16 @@ typedef enum {
  *                      thread, else variant 2 runs), 2 the HBM-bound one (psi
  *                      update deferred into the Amul phase); mesh_create picks
  *                      1 when an iteration's working set fits ~1.5x the L2
+ *   LF_OPT_COMPRESSED_LABELS (default 1; read by mesh_create) ELL meshes also
+ *                      store their gather labels as 16-bit codes relative to a
+ *                      per-32-cell offset (4 B instead of 8 B per face slot,
+ *                      escapes to the int32 labels where a code does not fit);
+ *                      the persistent diagonal solve gathers through them.
+ *                      0 = int32 labels only.  Decoded labels are identical,
+ *                      so results are bitwise the same either way.
  * Results are identical up to reduction grid size (all are deterministic). */
-typedef enum { LF_OPT_PERSISTENT = 0, LF_OPT_GRAPHS = 1, LF_OPT_SOLVE_VARIANT = 2 } lf_option;
+typedef enum { LF_OPT_PERSISTENT = 0, LF_OPT_GRAPHS = 1, LF_OPT_SOLVE_VARIANT = 2,
+               LF_OPT_COMPRESSED_LABELS = 3 } lf_option;
 LF_API lf_status lf_set_option(lf_context *ctx, lf_option opt, int value);
 
 /* enable != 0: bracket every launch of the hot kernels with CUDA events on

@@ -27,8 +27,8 @@ _SRC = os.path.join(_HERE, "lfoam_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 _TYPES = {"fixedValue": 0, "zeroGradient": 1, "processor": 2}
 # preconditioners (OpenFOAM fvSolution names): diagonal (the paper's),
-# DIC
-PRECONDITIONERS = {"diagonal": 0, "DIC": 1}
+# DIC and GAMG
+PRECONDITIONERS = {"diagonal": 0, "DIC": 1, "GAMG": 3}
 
 
 def build(force: bool = False) -> str:
@@ -86,6 +86,8 @@ def lib():
                                               C.c_int32, C.c_double, C.c_double, C.c_int32,
                                               C.c_int32, C.c_int32, GSUM, HALO, vp, C.POINTER(Perf)]
         _lib.orc_dic.argtypes = [C.POINTER(_Mesh), vp, vp, vp, vp, vp]
+        _lib.orc_gamg.argtypes = [C.POINTER(_Mesh), vp, vp, vp, vp, vp, vp, vp]
+        _lib.orc_gamg_level.argtypes = [C.POINTER(_Mesh), vp, vp, C.c_int32, vp, vp, vp, vp]
         _lib.orc_patch_values.argtypes = [C.POINTER(_Mesh), vp, vp]
         _lib.orc_weights.argtypes = [C.POINTER(_Mesh), vp]
         _lib.orc_corr_vectors.argtypes = [C.POINTER(_Mesh), vp]
@@ -276,6 +278,51 @@ def dic(mesh, diag, upper, r=None):
     if rc:
         raise MemoryError
     return rD, w
+
+
+GAMG_MAXL = 30
+
+
+def gamg(mesh, diag=None, upper=None, r=None):
+    """GAMG hierarchy of a mesh (reading A43): dict(n=[cells per level],
+    nf=[faces per level], agg=[level l -> l+1 maps]) and, with (diag, upper,
+    r), w = M^-1 r (one V-cycle)."""
+    om = _om(mesh)
+    n = np.zeros(GAMG_MAXL + 1, np.int32)
+    nf = np.zeros(GAMG_MAXL + 1, np.int32)
+    aggs = np.zeros(max(2 * om.n_cells, 1), np.int32)
+    w = np.zeros(om.n_cells) if r is not None else None
+    d = None if diag is None else np.ascontiguousarray(diag, np.float64)
+    u = None if upper is None else np.ascontiguousarray(upper, np.float64)
+    rr = None if r is None else np.ascontiguousarray(r, np.float64)
+    L = lib().orc_gamg(C.byref(om.s), _p(d), _p(u), n.ctypes.data, nf.ctypes.data, aggs.ctypes.data,
+                       _p(rr), _p(w))
+    if L < 0:
+        raise ValueError(f"GAMG oracle failed ({L})")
+    sizes = [int(x) for x in n[:L + 1]]
+    out, off = [], 0
+    for l in range(L):
+        out.append(aggs[off:off + sizes[l]].copy())
+        off += sizes[l]
+    res = dict(n=sizes, nf=[int(x) for x in nf[:L + 1]], agg=out)
+    if w is not None:
+        res["w"] = w
+    return res
+
+
+def gamg_level(mesh, diag, upper, level):
+    """Coarse matrix of `level`: dict(D, U, l, u) (faces upper-triangular)."""
+    om = _om(mesh)
+    info = gamg(mesh)
+    n, nf = info["n"][level], info["nf"][level]
+    D, U = np.zeros(n), np.zeros(max(nf, 1))
+    fl, fu = np.zeros(max(nf, 1), np.int32), np.zeros(max(nf, 1), np.int32)
+    rc = lib().orc_gamg_level(C.byref(om.s), _p(np.ascontiguousarray(diag, np.float64)),
+                              _p(np.ascontiguousarray(upper, np.float64)), level, D.ctypes.data,
+                              U.ctypes.data, fl.ctypes.data, fu.ctypes.data)
+    if rc:
+        raise ValueError(f"GAMG oracle failed ({rc})")
+    return dict(D=D, U=U[:nf], l=fl[:nf], u=fu[:nf])
 
 
 def self_halo(mesh):

@@ -23,6 +23,9 @@
  *     residual / normFactor, strict '<' (reading A9), singularity 1e-300.
  *   - OpenFOAM DIC preconditioner, face-loop form over
  *     the upper-triangular face order (reading A39).
+ *   - GAMG preconditioner: pairwise face
+ *     agglomeration, Galerkin coarse LDU matrices, symmetric Jacobi V-cycle
+ *     with an exact coarsest solve (reading A43).
  *   - CSR cell->face grouping (§5.2): the plain definition — a
  *     stable counting sort (items grouped by key, ties in input order,
  *     starts = exclusive scan of counts with the total appended, A13/A14).
@@ -282,13 +285,368 @@ int orc_dic(const orc_mesh *m, const double *diag, const double *upper,
     return 0;
 }
 
+/* ----------------------------------------------------------------- GAMG */
+/* GAMG preconditioner ("GAMG/AmgX (the paper's
+ * suggested alternative)"; §7 names an AMG preconditioner "a better
+ * alternative").  The paper gives no algorithm; the reading (A43)
+ * follows OpenFOAM's GAMG with pairwise face agglomeration:
+ *   agglomeration (once per mesh, geometric weights w_f = magSf_f*delta_f):
+ *     one PAIRING PASS over a graph (cells, faces (l,u,w) upper-triangular):
+ *       for c in order (ascending; DESCENDING on odd passes), unassigned:
+ *         j = the unassigned neighbour with the largest w (first in ascending
+ *             neighbour label on ties); if any: c and j form a new aggregate;
+ *         else j = the neighbour with the largest w: c joins j's aggregate;
+ *         else (no neighbour) c is a singleton aggregate.
+ *       aggregates are numbered in creation order; the coarse graph has one
+ *       face per pair of adjacent aggregates (I < J, sorted), weight = sum of
+ *       the fine weights in ascending fine-face order.
+ *     a LEVEL = two pairing passes (OpenFOAM mergeLevels 2); levels are added
+ *     while the current one has more than GAMG_NMIN cells and the new one has
+ *     at most 90% of its cells (at most GAMG_MAXL levels).
+ *   coarse matrices (per solve, Galerkin A_{l+1} = P^T A_l P with P the
+ *     piecewise-constant aggregation): D_{l+1}[I] = sum over members c of I
+ *     (ascending) of D_l[c], then over the faces internal to I (ascending)
+ *     of (U_f + U_f); U_{l+1}[F] = sum of U_f over the faces of F (ascending).
+ *   V-cycle (one per application, zero initial guess, symmetric: one Jacobi
+ *     sweep x += omega*rD*(b - A x) before and after the coarse correction,
+ *     omega = GAMG_OMEGA; the coarsest level solved exactly with the inverse
+ *     from a Cholesky factorisation):
+ *       b_0 = r
+ *       l = 0..L-1:  x_l = omega*(rD_l*b_l);  b_{l+1} = P^T (b_l - A_l x_l)
+ *       x_L = A_L^-1 b_L
+ *       l = L-1..0:  z = x_l + P x_{l+1};  x_l = z + omega*(rD_l*(b_l - A_l z))
+ *       M^-1 r = x_0
+ *   A_l x uses the face loop of lduMatrix::Amul over the level's
+ *   upper-triangular faces (a cell's terms in ascending neighbour label).
+ * Single rank (no processor interfaces on the coarse levels). */
+#define GAMG_NMIN 64
+#define GAMG_MAXL 30
+#define GAMG_OMEGA 0.9
+#define GAMG_MAXCOARSEST 2048
+
+typedef struct {
+    int32_t n, nf;
+    int32_t *l, *u;       /* [nf] faces, upper-triangular, sorted by (l, u) */
+    double *w;            /* [nf] agglomeration weights */
+    int32_t *agg;         /* [n] cell -> cell of the next level (not on the coarsest) */
+    int32_t *cface;       /* [nf] face -> face of the next level, -1 inside an aggregate */
+    double *D, *U, *rD;   /* per solve */
+    double *x, *b, *y;    /* work */
+} orc_glevel;
+
+typedef struct {
+    int32_t L;            /* index of the coarsest level (levels 0..L) */
+    orc_glevel lv[GAMG_MAXL + 1];
+    int32_t *fmap;        /* level-0 face k = mesh face fmap[k] */
+    double *inv;          /* [nL*nL] inverse of the coarsest matrix (row major) */
+} orc_gamg_t;
+
+/* neighbours of every cell in ascending label: CSR over the faces */
+static int graph_rows(int32_t n, int32_t nf, const int32_t *l, const int32_t *u, const double *w,
+                      int32_t **start, int32_t **nb, double **wt)
+{
+    int32_t c, f, *cnt = (int32_t *)calloc((size_t)n + 1, sizeof(int32_t));
+    if (!cnt) return 2;
+    for (f = 0; f < nf; f++) { cnt[l[f] + 1]++; cnt[u[f] + 1]++; }
+    for (c = 0; c < n; c++) cnt[c + 1] += cnt[c];
+    *start = cnt;
+    *nb = (int32_t *)malloc(sizeof(int32_t) * (size_t)(2 * nf + 1));
+    *wt = (double *)malloc(sizeof(double) * (size_t)(2 * nf + 1));
+    int32_t *pos = (int32_t *)malloc(sizeof(int32_t) * ((size_t)n + 1));
+    if (!*nb || !*wt || !pos) return 2;
+    memcpy(pos, cnt, sizeof(int32_t) * (size_t)n);
+    /* faces sorted by (l, u): for cell c the faces (l', c) come in ascending
+     * l' < c, then the faces (c, u') in ascending u' -> ascending labels
+     * when both sides are appended in face order, lower side first */
+    for (f = 0; f < nf; f++) { (*nb)[pos[u[f]]] = l[f]; (*wt)[pos[u[f]]++] = w[f]; }
+    for (f = 0; f < nf; f++) { (*nb)[pos[l[f]]] = u[f]; (*wt)[pos[l[f]]++] = w[f]; }
+    free(pos);
+    return 0;
+}
+
+typedef struct { int32_t l, u, f; } orc_cf;
+static int cf_cmp(const void *a, const void *b)
+{
+    const orc_cf *x = (const orc_cf *)a, *y = (const orc_cf *)b;
+    if (x->l != y->l) return x->l < y->l ? -1 : 1;
+    if (x->u != y->u) return x->u < y->u ? -1 : 1;
+    return x->f < y->f ? -1 : (x->f > y->f);
+}
+
+/* one pairing pass on (n, nf, l, u, w): agg[n], *nc, and the coarse graph
+ * (*cl, *cu, *cw, *ncf) with cface[nf] (-1 inside an aggregate) */
+static int pair_pass(int32_t n, int32_t nf, const int32_t *l, const int32_t *u, const double *w,
+                     int reverse, int32_t *agg, int32_t *nc, int32_t *cface,
+                     int32_t **cl, int32_t **cu, double **cw, int32_t *ncf)
+{
+    int32_t *st, *nb, i, k, f, m = 0;
+    double *wt;
+    if (graph_rows(n, nf, l, u, w, &st, &nb, &wt)) return 2;
+    for (i = 0; i < n; i++) agg[i] = -1;
+    *nc = 0;
+    for (i = 0; i < n; i++) {
+        int32_t c = reverse ? n - 1 - i : i, best = -1;
+        double bw = -1.0;
+        if (agg[c] >= 0) continue;
+        for (k = st[c]; k < st[c + 1]; k++)
+            if (agg[nb[k]] < 0 && wt[k] > bw) { bw = wt[k]; best = nb[k]; }
+        if (best >= 0) {
+            agg[c] = agg[best] = (*nc)++;
+        } else {
+            bw = -1.0;
+            for (k = st[c]; k < st[c + 1]; k++)
+                if (wt[k] > bw) { bw = wt[k]; best = nb[k]; }
+            agg[c] = best >= 0 ? agg[best] : (*nc)++;
+        }
+    }
+    free(st); free(nb); free(wt);
+    /* coarse faces: distinct (I, J), I < J, sorted; weights summed in fine order */
+    orc_cf *t = (orc_cf *)malloc(sizeof(orc_cf) * (size_t)(nf > 0 ? nf : 1));
+    if (!t) return 2;
+    for (f = 0; f < nf; f++) {
+        int32_t a = agg[l[f]], b = agg[u[f]];
+        cface[f] = -1;
+        if (a == b) continue;
+        t[m].l = a < b ? a : b; t[m].u = a < b ? b : a; t[m].f = f; m++;
+    }
+    qsort(t, (size_t)m, sizeof(orc_cf), cf_cmp);
+    *cl = (int32_t *)malloc(sizeof(int32_t) * (size_t)(m > 0 ? m : 1));
+    *cu = (int32_t *)malloc(sizeof(int32_t) * (size_t)(m > 0 ? m : 1));
+    *cw = (double *)calloc((size_t)(m > 0 ? m : 1), sizeof(double));
+    if (!*cl || !*cu || !*cw) return 2;
+    *ncf = 0;
+    for (k = 0; k < m; k++) {
+        if (k == 0 || t[k].l != t[k - 1].l || t[k].u != t[k - 1].u) {
+            (*cl)[*ncf] = t[k].l; (*cu)[*ncf] = t[k].u; (*ncf)++;
+        }
+        cface[t[k].f] = *ncf - 1;
+    }
+    /* weights in ascending fine-face order (t is sorted by face within a pair) */
+    for (f = 0; f < nf; f++)
+        if (cface[f] >= 0) (*cw)[cface[f]] += w[f];
+    free(t);
+    return 0;
+}
+
+static void gamg_free(orc_gamg_t *g)
+{
+    int32_t i;
+    for (i = 0; i <= g->L; i++) {
+        orc_glevel *v = &g->lv[i];
+        free(v->l); free(v->u); free(v->w); free(v->agg); free(v->cface);
+        free(v->D); free(v->U); free(v->rD); free(v->x); free(v->b); free(v->y);
+    }
+    free(g->fmap); free(g->inv);
+    memset(g, 0, sizeof(*g));
+}
+
+/* the level hierarchy of a mesh (agglomeration only) */
+static int gamg_build(const orc_mesh *m, orc_gamg_t *g)
+{
+    int32_t f, k;
+    memset(g, 0, sizeof(*g));
+    orc_face3 *t = upper_triangular_faces(m);
+    if (!t) return 2;
+    orc_glevel *v = &g->lv[0];
+    v->n = m->n_cells; v->nf = m->n_faces;
+    size_t F1 = (size_t)(m->n_faces > 0 ? m->n_faces : 1);
+    v->l = (int32_t *)malloc(sizeof(int32_t) * F1); v->u = (int32_t *)malloc(sizeof(int32_t) * F1);
+    v->w = (double *)malloc(sizeof(double) * F1); g->fmap = (int32_t *)malloc(sizeof(int32_t) * F1);
+    if (!v->l || !v->u || !v->w || !g->fmap) return 2;
+    for (k = 0; k < m->n_faces; k++) {
+        f = t[k].f;
+        v->l[k] = t[k].l; v->u[k] = t[k].u; g->fmap[k] = f;
+        v->w[k] = m->mag_sf[f] * m->delta[f];
+    }
+    free(t);
+    int32_t pass = 0;
+    while (g->L < GAMG_MAXL && g->lv[g->L].n > GAMG_NMIN) {
+        orc_glevel *a = &g->lv[g->L];
+        /* two pairing passes: a -> mid -> coarse */
+        int32_t n1, nf1, n2, nf2, *l1, *u1, *l2, *u2;
+        double *w1, *w2;
+        int32_t *agg1 = (int32_t *)malloc(sizeof(int32_t) * (size_t)(a->n > 0 ? a->n : 1));
+        int32_t *cf1 = (int32_t *)malloc(sizeof(int32_t) * (size_t)(a->nf > 0 ? a->nf : 1));
+        if (!agg1 || !cf1) return 2;
+        if (pair_pass(a->n, a->nf, a->l, a->u, a->w, pass & 1, agg1, &n1, cf1, &l1, &u1, &w1, &nf1)) return 2;
+        int32_t *agg2 = (int32_t *)malloc(sizeof(int32_t) * (size_t)(n1 > 0 ? n1 : 1));
+        int32_t *cf2 = (int32_t *)malloc(sizeof(int32_t) * (size_t)(nf1 > 0 ? nf1 : 1));
+        if (!agg2 || !cf2) return 2;
+        if (pair_pass(n1, nf1, l1, u1, w1, (pass + 1) & 1, agg2, &n2, cf2, &l2, &u2, &w2, &nf2)) return 2;
+        pass += 2;
+        free(l1); free(u1); free(w1);
+        if ((double)n2 > 0.9 * (double)a->n) {  /* coarsening stalled: a is the coarsest */
+            free(agg1); free(cf1); free(agg2); free(cf2); free(l2); free(u2); free(w2);
+            break;
+        }
+        a->agg = agg1; a->cface = cf1;
+        for (k = 0; k < a->n; k++) a->agg[k] = agg2[agg1[k]];
+        for (f = 0; f < a->nf; f++) a->cface[f] = cf1[f] < 0 ? -1 : cf2[cf1[f]];
+        free(agg2); free(cf2);
+        orc_glevel *c = &g->lv[++g->L];
+        c->n = n2; c->nf = nf2; c->l = l2; c->u = u2; c->w = w2;
+    }
+    if (g->lv[g->L].n > GAMG_MAXCOARSEST) return 3;
+    for (k = 0; k <= g->L; k++) {
+        orc_glevel *a = &g->lv[k];
+        size_t nn = (size_t)(a->n > 0 ? a->n : 1), ff = (size_t)(a->nf > 0 ? a->nf : 1);
+        a->D = (double *)calloc(nn, sizeof(double)); a->rD = (double *)calloc(nn, sizeof(double));
+        a->U = (double *)calloc(ff, sizeof(double));
+        a->x = (double *)calloc(nn, sizeof(double)); a->b = (double *)calloc(nn, sizeof(double));
+        a->y = (double *)calloc(nn, sizeof(double));
+        if (!a->D || !a->rD || !a->U || !a->x || !a->b || !a->y) return 2;
+    }
+    int32_t nL = g->lv[g->L].n;
+    g->inv = (double *)calloc((size_t)nL * (size_t)nL + 1, sizeof(double));
+    return g->inv ? 0 : 2;
+}
+
+/* y = A_l x, face loop (lduMatrix::Amul) */
+static void glevel_amul(const orc_glevel *a, const double *x, double *y)
+{
+    int32_t c, f;
+    for (c = 0; c < a->n; c++) y[c] = a->D[c] * x[c];
+    for (f = 0; f < a->nf; f++) {
+        y[a->u[f]] += a->U[f] * x[a->l[f]];
+        y[a->l[f]] += a->U[f] * x[a->u[f]];
+    }
+}
+
+/* coarse matrices of the current fine matrix and the coarsest inverse */
+static int gamg_setup(orc_gamg_t *g, const double *diag, const double *upper)
+{
+    int32_t l, c, f, i, j, k;
+    orc_glevel *a0 = &g->lv[0];
+    for (c = 0; c < a0->n; c++) a0->D[c] = diag[c];
+    for (f = 0; f < a0->nf; f++) a0->U[f] = upper[g->fmap[f]];
+    for (l = 0; l < g->L; l++) {
+        orc_glevel *a = &g->lv[l], *b = &g->lv[l + 1];
+        for (c = 0; c < b->n; c++) b->D[c] = 0.0;
+        for (f = 0; f < b->nf; f++) b->U[f] = 0.0;
+        for (c = 0; c < a->n; c++) b->D[a->agg[c]] += a->D[c];
+        for (f = 0; f < a->nf; f++)
+            if (a->cface[f] < 0) b->D[a->agg[a->l[f]]] += a->U[f] + a->U[f];
+        for (f = 0; f < a->nf; f++)
+            if (a->cface[f] >= 0) b->U[a->cface[f]] += a->U[f];
+    }
+    for (l = 0; l <= g->L; l++)
+        for (c = 0; c < g->lv[l].n; c++) g->lv[l].rD[c] = 1.0 / g->lv[l].D[c];
+    /* coarsest: dense A, Cholesky (row by row), inverse column by column */
+    orc_glevel *z = &g->lv[g->L];
+    int32_t n = z->n;
+    double *A = (double *)calloc((size_t)n * (size_t)n + 1, sizeof(double));
+    double *Lm = (double *)calloc((size_t)n * (size_t)n + 1, sizeof(double));
+    double *yv = (double *)calloc((size_t)n + 1, sizeof(double));
+    if (!A || !Lm || !yv) return 2;
+    for (c = 0; c < n; c++) A[c * n + c] = z->D[c];
+    for (f = 0; f < z->nf; f++) { A[z->l[f] * n + z->u[f]] = z->U[f]; A[z->u[f] * n + z->l[f]] = z->U[f]; }
+    for (i = 0; i < n; i++)
+        for (j = 0; j <= i; j++) {
+            double s = A[i * n + j];
+            for (k = 0; k < j; k++) s -= Lm[i * n + k] * Lm[j * n + k];
+            if (i == j) {
+                if (!(s > 0.0)) { free(A); free(Lm); free(yv); return 4; }  /* not SPD */
+                Lm[i * n + i] = sqrt(s);
+            } else {
+                Lm[i * n + j] = s / Lm[j * n + j];
+            }
+        }
+    for (k = 0; k < n; k++) {  /* column k of the inverse: L L^T x = e_k */
+        for (i = 0; i < n; i++) {
+            double s = i == k ? 1.0 : 0.0;
+            for (j = 0; j < i; j++) s -= Lm[i * n + j] * yv[j];
+            yv[i] = s / Lm[i * n + i];
+        }
+        for (i = n - 1; i >= 0; i--) {
+            double s = yv[i];
+            for (j = i + 1; j < n; j++) s -= Lm[j * n + i] * g->inv[j * n + k];
+            g->inv[i * n + k] = s / Lm[i * n + i];
+        }
+    }
+    free(A); free(Lm); free(yv);
+    return 0;
+}
+
+/* wA = M^-1 rA: one V-cycle */
+static void gamg_precondition(orc_gamg_t *g, const double *rA, double *wA)
+{
+    int32_t l, c, k;
+    orc_glevel *a0 = &g->lv[0];
+    for (c = 0; c < a0->n; c++) a0->b[c] = rA[c];
+    for (l = 0; l < g->L; l++) {
+        orc_glevel *a = &g->lv[l], *b = &g->lv[l + 1];
+        for (c = 0; c < a->n; c++) a->x[c] = GAMG_OMEGA * (a->rD[c] * a->b[c]);
+        glevel_amul(a, a->x, a->y);
+        for (c = 0; c < b->n; c++) b->b[c] = 0.0;
+        for (c = 0; c < a->n; c++) b->b[a->agg[c]] += a->b[c] - a->y[c];
+    }
+    orc_glevel *z = &g->lv[g->L];
+    for (c = 0; c < z->n; c++) {
+        double s = 0.0;
+        for (k = 0; k < z->n; k++) s += g->inv[c * z->n + k] * z->b[k];
+        z->x[c] = s;
+    }
+    for (l = g->L - 1; l >= 0; l--) {
+        orc_glevel *a = &g->lv[l], *b = &g->lv[l + 1];
+        for (c = 0; c < a->n; c++) a->x[c] = a->x[c] + b->x[a->agg[c]];   /* z = x + P x_c */
+        glevel_amul(a, a->x, a->y);
+        for (c = 0; c < a->n; c++) a->x[c] = a->x[c] + GAMG_OMEGA * (a->rD[c] * (a->b[c] - a->y[c]));
+    }
+    for (c = 0; c < a0->n; c++) wA[c] = a0->x[c];
+}
+
+/* Test access: level sizes, agglomeration maps and coarse matrices of the
+ * hierarchy for (diag, upper); and w = M^-1 r.  out_n[GAMG_MAXL+1] cell
+ * counts, out_nf[...] face counts, returns L (>= 0) or -error.  If
+ * agg_out != NULL it receives the level-0 -> level-1 ... maps concatenated
+ * (sum of n_l for l < L); if r != NULL, w = M^-1 r. */
+int orc_gamg(const orc_mesh *m, const double *diag, const double *upper, int32_t *out_n,
+             int32_t *out_nf, int32_t *agg_out, const double *r, double *w)
+{
+    orc_gamg_t g;
+    int32_t l, off = 0, rc = gamg_build(m, &g);
+    if (rc) { gamg_free(&g); return -rc; }
+    if (diag && (rc = gamg_setup(&g, diag, upper))) { gamg_free(&g); return -rc; }
+    for (l = 0; l <= g.L; l++) {
+        if (out_n) out_n[l] = g.lv[l].n;
+        if (out_nf) out_nf[l] = g.lv[l].nf;
+        if (agg_out && l < g.L) {
+            memcpy(agg_out + off, g.lv[l].agg, sizeof(int32_t) * (size_t)g.lv[l].n);
+            off += g.lv[l].n;
+        }
+    }
+    if (r && w) gamg_precondition(&g, r, w);
+    l = g.L;
+    gamg_free(&g);
+    return l;
+}
+
+/* coarse matrix of level lev (1..L): D[n_lev], U[nf_lev], faces l/u */
+int orc_gamg_level(const orc_mesh *m, const double *diag, const double *upper, int32_t lev,
+                   double *D, double *U, int32_t *fl, int32_t *fu)
+{
+    orc_gamg_t g;
+    int32_t rc = gamg_build(m, &g);
+    if (rc || lev < 0 || lev > g.L) { gamg_free(&g); return rc ? -rc : -1; }
+    if ((rc = gamg_setup(&g, diag, upper))) { gamg_free(&g); return -rc; }
+    orc_glevel *a = &g.lv[lev];
+    memcpy(D, a->D, sizeof(double) * (size_t)a->n);
+    memcpy(U, a->U, sizeof(double) * (size_t)a->nf);
+    memcpy(fl, a->l, sizeof(int32_t) * (size_t)a->nf);
+    memcpy(fu, a->u, sizeof(int32_t) * (size_t)a->nf);
+    gamg_free(&g);
+    return 0;
+}
+
 #define ORC_PRECOND_DIAGONAL 0
 #define ORC_PRECOND_DIC 1
+#define ORC_PRECOND_GAMG 3
 
 /* ------------------------------------------------------------------ PCG */
 /* OpenFOAM PCG::scalarSolve, SURVEY §8(c.1) "PCG" block, step by step in
  * its order; precond = ORC_PRECOND_DIAGONAL (diagonalPreconditioner, the
- * paper's choice P:608) or ORC_PRECOND_DIC (DICPreconditioner, above; built
+ * paper's choice P:608), ORC_PRECOND_GAMG (one V-cycle, above) or
+ * ORC_PRECOND_DIC (DICPreconditioner, above; built
  * where OpenFOAM constructs the preconditioner, once per solve). */
 int orc_pcg_p(const orc_mesh *m, const double *diag, const double *upper,
               const double *b_bnd, const double *source, double *psi,
@@ -307,6 +665,8 @@ int orc_pcg_p(const orc_mesh *m, const double *diag, const double *upper,
     double *xr = (double *)calloc(nb, sizeof(double));
     double s[2], normFactor, psibar, wArA, wArAold, wApA, alpha, beta;
     int32_t it = 0;
+    orc_gamg_t gamg;
+    int have_gamg = 0;
     if (!wA || !rA || !pA || !rD || !tmp || !xr) return 2;
 
     memset(perf, 0, sizeof(*perf));
@@ -339,6 +699,11 @@ int orc_pcg_p(const orc_mesh *m, const double *diag, const double *upper,
             t = upper_triangular_faces(m);
             if (!t) return 2;
             dic_rD(m, t, diag, upper, rD);
+        } else if (precond == ORC_PRECOND_GAMG) {
+            int rc = gamg_build(m, &gamg);
+            if (!rc) rc = gamg_setup(&gamg, diag, upper);
+            if (rc) { gamg_free(&gamg); return rc; }
+            have_gamg = 1;
         } else {
             for (c = 0; c < n; c++) rD[c] = 1.0 / diag[c];
         }
@@ -347,6 +712,8 @@ int orc_pcg_p(const orc_mesh *m, const double *diag, const double *upper,
             wArAold = wArA;
             if (precond == ORC_PRECOND_DIC)                           /* precondition */
                 dic_precondition(m, t, rD, upper, rA, wA);
+            else if (precond == ORC_PRECOND_GAMG)
+                gamg_precondition(&gamg, rA, wA);
             else
                 for (c = 0; c < n; c++) wA[c] = rD[c] * rA[c];
             s[0] = 0.0;
@@ -384,6 +751,7 @@ int orc_pcg_p(const orc_mesh *m, const double *diag, const double *upper,
     perf->n_iterations = it;
     perf->converged = converged(perf->final_residual, perf->initial_residual, tol, rel_tol);
     free(wA); free(rA); free(pA); free(rD); free(tmp); free(xr); free(t);
+    if (have_gamg) gamg_free(&gamg);
     return 0;
 }
 

@@ -204,6 +204,15 @@ lf_status lf_mesh_info(const lf_mesh *M, int32_t *n, int32_t *F, int32_t *B, int
   });
 }
 
+lf_status lf_mesh_layout(const lf_mesh *M, int32_t *ell_width, int32_t *row_width, int32_t *label_escapes) {
+  return guard([&] {
+    LF_REQUIRE(M != nullptr, "mesh is NULL");
+    if (ell_width) *ell_width = M->md.K;
+    if (row_width) *row_width = M->md.KS;
+    if (label_escapes) *label_escapes = M->md.codeE ? M->ell16Escapes : -1;
+  });
+}
+
 lf_status lf_mesh_export_addressing(const lf_mesh *M, int32_t *owner_start, int32_t *losort,
                                     int32_t *losort_start, int32_t *face_order, int32_t *cell_order) {
   return guard([&] {
@@ -262,9 +271,20 @@ lf_status field_set(lf_mesh *M, lf_field f, int32_t patch, const double *v, int6
       LF_REQUIRE(n == M->n, "n must equal n_cells");
       LF_REQUIRE(M->hasGeom, "a DT field needs the full geometry (interpolation weights)");
       LF_REQUIRE(M->nproc == 0, "a DT field is not supported with processor patches");
-      if (!on_device)
+      {
+        // validated on the host either way (a device field is copied back once:
+        // DT is set once per case, not per step)
+        std::vector<double> hv;
+        const double *chk = v;
+        if (on_device) {
+          hv.resize(n);
+          LF_CUDA(cudaMemcpyAsync(hv.data(), v, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+          LF_CUDA(cudaStreamSynchronize(s));
+          chk = hv.data();
+        }
         for (int64_t i = 0; i < n; ++i)
-          LF_REQUIRE(v[i] > 0.0 && std::isfinite(v[i]), "DT must be > 0 and finite");
+          LF_REQUIRE(chk[i] > 0.0 && std::isfinite(chk[i]), "DT must be > 0 and finite");
+      }
       if (!M->DTc) {
         M->DTc = M->arena.alloc<double>(M->n);
         M->gammaF = M->arena.alloc<double>(M->F);
@@ -362,7 +382,7 @@ lf_status laplacian_assemble(lf_mesh *M, const lf_laplacian_params *p, lf_ldu **
     }
     field_halo(M, M->T);
     ctx->launch(LF_K_ASSEMBLE, [&] {
-      launch_assemble(s, M->Lasm, md, M->ld, p->DT, 1.0 / p->dt, M->T, M->ws.recvT, false, M->ws, nullptr,
+      launch_assemble(s, M->Lasm, md, M->ld, p->DT, 1.0 / p->dt, M->T, M->haloT(), false, M->ws, nullptr,
                       lapSrc);
     });
     M->ldu.assembled = true;
@@ -413,7 +433,7 @@ lf_status ldu_amul(const lf_ldu *sys, const double *x, double *y) {
     lf_context *ctx = M->ctx;
     cudaStream_t s = ctx->stream;
     field_halo(M, x);
-    ctx->launch(LF_K_AMUL, [&] { launch_amul(s, M->Lamul, M->md, M->ld, M->ws.recvT, x, y); });
+    ctx->launch(LF_K_AMUL, [&] { launch_amul(s, M->Lamul, M->md, M->ld, M->haloT(), x, y); });
   }, M);
 }
 
@@ -523,7 +543,8 @@ lf_status lf_set_option(lf_context *ctx, lf_option opt, int value) {
     else if (opt == LF_OPT_SOLVE_VARIANT) {
       LF_REQUIRE(value >= 0 && value <= 2, "solve variant must be 0, 1 or 2");
       ctx->solveVariant = value;
-    }
+    } else if (opt == LF_OPT_COMPRESSED_LABELS)
+      ctx->compressedLabels = value != 0;
     else
       throw Error{LF_ERR_INVALID_ARG, "unknown option"};
   });

@@ -209,7 +209,7 @@ __device__ __forceinline__ void dic_apply(const MeshDev &m, const DicDev &d, con
         const double rc = dic_forward_cell<KS>(d, a, c, r, q, w, upd, alpha, wc, &stash[i * BS + threadIdx.x]);
         v[0] += fabs(rc);
         v[1] = fma(wc, rc, v[1]);
-        if (HALO && pp.P > 0) push_halo(m, pp.dstW, c, wc);
+        if (HALO && pp.P > 0) push_halo<HALO_W>(m, pp, c, wc);
       }
     }
     grid_barrier(bar);
@@ -220,7 +220,7 @@ __device__ __forceinline__ void dic_apply(const MeshDev &m, const DicDev &d, con
         const double rc = dic_backward_cell<KS>(d, a, c, true, r, q, w, upd, alpha, wc, &stash[i * BS + threadIdx.x]);
         v[0] += fabs(rc);
         v[1] = fma(wc, rc, v[1]);
-        if (HALO && pp.P > 0) push_halo(m, pp.dstW, c, wc);
+        if (HALO && pp.P > 0) push_halo<HALO_W>(m, pp, c, wc);
       }
     }
     grid_reduce_sync<2, HALO>(v, partials, bar, out, pp LF_DBG_ARG(0), idle);
@@ -234,7 +234,7 @@ __device__ __forceinline__ void dic_apply(const MeshDev &m, const DicDev &d, con
       v[0] += fabs(rc);
       if (l == L - 1) {  // no upper neighbours: final
         v[1] = fma(wc, rc, v[1]);
-        if (HALO && pp.P > 0) push_halo(m, pp.dstW, c, wc);
+        if (HALO && pp.P > 0) push_halo<HALO_W>(m, pp, c, wc);
       }
     };
     // two levels (LF_DIC_REVERSE): every pass starts where the previous one
@@ -253,7 +253,7 @@ __device__ __forceinline__ void dic_apply(const MeshDev &m, const DicDev &d, con
       const double rc = dic_backward_cell<KS>(d, a, c, l == 0, r, q, w, upd, alpha, wc);
       if (l == 0) v[0] += fabs(rc);
       v[1] = fma(wc, rc, v[1]);
-      if (HALO && pp.P > 0) push_halo(m, pp.dstW, c, wc);
+      if (HALO && pp.P > 0) push_halo<HALO_W>(m, pp, c, wc);
     };
     if (LF_DIC_REVERSE == 2 && L == 2 && odd)
       grid_range_rev(__ldg(d.lvlStart + l), __ldg(d.lvlStart + l + 1), bwd);

@@ -39,6 +39,7 @@ struct lf_context {
   bool useGraphs = true;   // replay iteration chunks as CUDA graphs
   bool persistent = true;  // single-rank, no processor patches: one cooperative launch per solve
   int solveVariant = 0;    // LF_OPT_SOLVE_VARIANT: 0 by mesh size, 1 L2-resident, 2 HBM-bound
+  bool compressedLabels = true;  // LF_OPT_COMPRESSED_LABELS (mesh_create)
   struct Pending {
     int kind;
     cudaEvent_t a, b;
@@ -100,12 +101,16 @@ struct lf_mesh {
   int persistentGrid = 0;     // co-resident grid of k_pcg_persistent
   bool l2Resident = false;    // an iteration's working set fits ~1.5x the L2 (mesh.cpp)
   bool stashOK = false;       // few enough trips per thread for the L2-resident variant
+  int32_t ell16Escapes = -1;  // escaped compressed-label entries (-1: not built)
   unsigned *gridBar = nullptr;  // device {count, generation}
   // peer-memory transport: one IPC-exportable block [flags | vals | recvT | recvW]
   char *p2pBlock = nullptr;
   size_t p2pBytes = 0, offFlags = 0, offVals = 0, offRecvT = 0, offRecvW = 0;
   std::vector<void *> ipcOpened;  // peer blocks mapped with cudaIpcOpenMemHandle
   bool p2pConnected = false;
+  int tPar = 0;  // parity of the last peer-memory T halo push (recvT double buffer)
+  // recvT half holding the current T halo (parity 0 for host-side exchanges)
+  double *haloT() { return ws.recvT + (p2pConnected ? (size_t)tPar * (size_t)nproc : 0); }
   // non-orthogonal correction path (full geometry given at mesh_create)
   bool hasGeom = false;
   lf::GeomDev geo{};

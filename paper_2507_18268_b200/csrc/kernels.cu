@@ -105,6 +105,18 @@ __device__ __forceinline__ double ld_relaxed_sys(const double *p) {
   return v;
 }
 
+// Blocks that stored halo values into peer memory (push_halo) note it here;
+// only they issue the system-scope fence before arriving at a reduction.
+__shared__ int lf_blockPushed;  // per block; may start as garbage (then one extra fence)
+// thread 0, after the block's bar.sync: make this block's peer stores
+// visible system-wide if it made any (and reset the note)
+__device__ __forceinline__ void fence_pushed() {
+  if (lf_blockPushed) {
+    __threadfence_system();
+    lf_blockPushed = 0;
+  }
+}
+
 // Spin-wait watchdog: a rank that never arrives must not hang the GPU —
 // after LF_SPIN_TIMEOUT_S seconds the kernel traps (the call returns
 // LF_ERR_CUDA) instead of spinning forever.
@@ -173,10 +185,8 @@ __device__ bool reduce_grid(double (&v)[NV], double *partials, unsigned *ticket,
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int k = 0; k < NV; ++k) partials[k * gridDim.x + blockIdx.x] = v[k];
-    if (P.P > 0)
-      __threadfence_system();  // this block's peer-memory halo stores precede the ticket
-    else
-      __threadfence();
+    if (P.P > 0) fence_pushed();  // this block's peer-memory halo stores precede the ticket
+    __threadfence();
     const unsigned t = atomicAdd(ticket, 1u);
     amLast = (t == gridDim.x - 1);
   }
@@ -224,7 +234,7 @@ __device__ bool reduce_grid(double (&v)[NV], double *partials, unsigned *ticket,
 // KE > 0: half ELL slices with KE slots per side; KE < 0: full-row ELL with
 // -KE slots (the DIC rows; meshes with more than 4 faces on a side), each
 // row in ascending neighbour label = the same summation order; KE == 0: CSR.
-template <int KE, class XF>
+template <int KE, class XF, bool E16 = false>
 __device__ __forceinline__ double row_offdiag(const MeshDev &m, const LduDev &a, int c, double acc,
                                               XF xval, double *sU = nullptr) {
   if constexpr (KE < 0) {
@@ -251,11 +261,26 @@ __device__ __forceinline__ double row_offdiag(const MeshDev &m, const LduDev &a,
     const int n = m.ldE;  // slab stride
     int lo[KE], nb[KE];
     double uo[KE];
+    if constexpr (E16) {  // compressed labels (see k_build_ell16), decoded to the same values
+      const int g = c >> 5;
 #pragma unroll
-    for (int k = 0; k < KE; ++k) {
-      lo[k] = __ldg(m.loE + k * n + c);
-      nb[k] = __ldg(m.nbrE + k * n + c);
-      uo[k] = a.upperE[k * n + c];
+      for (int k = 0; k < KE; ++k) {
+        const unsigned cw = __ldg(m.codeE + k * n + c);
+        const int2 o = __ldg(m.offE + k * m.ngE + g);
+        const unsigned nd = cw & 0xFFFFu, ldv = cw >> 16;
+        nb[k] = nd == 0xFFFFu ? -1 : nd == 0xFFFEu ? __ldg(m.nbrE + k * n + c) : c + o.x + (int)nd - 0x8000;
+        lo[k] = ldv == 0xFFFFu ? -1
+                : ldv == 0xFFFEu ? __ldg(m.loE + k * n + c)
+                                 : (int)((ldv >> 14) << ELL_SHIFT) | (c - o.y - (int)(ldv & 0x3FFFu) + 0x2000);
+        uo[k] = a.upperE[k * n + c];
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < KE; ++k) {
+        lo[k] = __ldg(m.loE + k * n + c);
+        nb[k] = __ldg(m.nbrE + k * n + c);
+        uo[k] = a.upperE[k * n + c];
+      }
     }
     double lu[KE], lx[KE], ox[KE];
 #pragma unroll
@@ -343,13 +368,25 @@ __device__ __forceinline__ double row_proc_p(const MeshDev &m, const double *__r
 
 // Peer-memory halo: store a cell's new value into the neighbour's halo slot
 // of each of its processor faces (remote store over NVLink; own buffer for
-// self pairs).  Made visible by the system fence before the reduction ticket.
-__device__ __forceinline__ void push_halo(const MeshDev &m, double *const *dst, int c, double val) {
+// self pairs): segment base + offset.  The block notes that it pushed
+// (lf_blockPushed); only such blocks issue the system-scope fence before
+// their arrival at the next reduction.
+enum { HALO_W = 0, HALO_T = 1 };
+template <int WHICH>
+__device__ __forceinline__ void push_halo(const MeshDev &m, const P2PDev &P, int c, double val) {
   if (m.hasProc) {
     const int k0 = m.pcStart[c], k1 = m.pcStart[c + 1];
-    for (int kk = k0; kk < k1; ++kk) *dst[m.bSlot[m.pcFace[kk]]] = val;
+    for (int kk = k0; kk < k1; ++kk) {
+      const int sl = m.bSlot[m.pcFace[kk]];
+      int g = 0;
+      while (g + 1 < P.nseg && sl >= P.segBeg[g + 1]) ++g;
+      double *base = WHICH == HALO_W ? P.dstW[g] : P.dstT[P.tPar][g];
+      base[sl - P.segBeg[g]] = val;
+    }
+    if (k1 > k0) lf_blockPushed = 1;
   }
 }
+
 
 // ------------------------------------------------------ L2 bulk prefetch
 // cp.async.bulk.prefetch.L2 (sm_90+ TMA engine): one instruction pulls a
@@ -394,7 +431,7 @@ __global__ void __launch_bounds__(BS, LF_MINB)
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < m.n; c += gridDim.x * blockDim.x) {
     const double xc = x[c];
     v[0] += xc;
-    if (push) push_halo(m, ws.p2p.dstT, c, xc);
+    if (push) push_halo<HALO_T>(m, ws.p2p, c, xc);
   }
   reduce_grid<1>(v, partials, ticket, out, ws.p2p);
 }
@@ -487,7 +524,7 @@ __global__ void __launch_bounds__(BS, LF_MINB)
       v[2] = fma(w, r, v[2]);
       ws.r[c] = r;
       ws.w[c] = w;
-      if (ws.p2p.P > 0) push_halo(m, ws.p2p.dstW, c, w);
+      if (ws.p2p.P > 0) push_halo<HALO_W>(m, ws.p2p, c, w);
     }
   }
   if (SETUP) {
@@ -535,7 +572,7 @@ __global__ void __launch_bounds__(BS, LF_MINB_G)
     v[2] = fma(w, r, v[2]);
     ws.r[c] = r;
     ws.w[c] = w;
-    if (ws.p2p.P > 0) push_halo(m, ws.p2p.dstW, c, w);
+    if (ws.p2p.P > 0) push_halo<HALO_W>(m, ws.p2p, c, w);
   }
   if (reduce_grid<3>(v, ws.partials, ws.tickets + T_SETUP, ws.lsum->setup, ws.p2p) && threadIdx.x == 0) {
     PcgCtl *ctl = ws.ctl;
@@ -708,7 +745,7 @@ __global__ void __launch_bounds__(BS, LF_MINB)
           const double w = (1.0 / d[u]) * rn;
           ws.r[c] = rn;
           ws.w[c] = w;
-          if (push) push_halo(m, ws.p2p.dstW, c, w);
+          if (push) push_halo<HALO_W>(m, ws.p2p, c, w);
           v[0] += fabs(rn);
           v[1] = fma(w, rn, v[1]);
         }
@@ -800,8 +837,9 @@ __device__ void grid_reduce_sync(double (&v)[NV], double *partials, unsigned *ba
 #endif
     unsigned t;
     if (PEER && P.P > 0) {
-      __threadfence_system();  // peer-memory halo stores of this block precede the arrival
-      t = atomicAdd(bar, 1u);
+      fence_pushed();  // peer-memory halo stores of this block (if any) precede the arrival
+      // acq_rel: the last arriver also acquires every block's partials
+      asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(t) : "l"(bar) : "memory");
     } else {
 #if LF_BAR_ACQREL
       // release: the block's writes (ordered by the bar.sync above) precede the
@@ -949,16 +987,23 @@ static size_t stash_fit(int n, int grid, size_t per) {
 // HALO = false: single rank without processor patches — the interface
 // term, halo puts and peer allreduce are compiled out of the hot loop
 // (they cost 13% at 100^3 even when branched around, r1o).
-template <int KE, bool HALO, bool IDLE = false>
+#ifndef LF_W88
+#define LF_W88 1   // HBM-bound variant: w not stored (SURVEY's 88n + 16F iteration): phase 1
+#endif             // recomputes w = (1/diag) r at the cell and its neighbours
+#ifndef LF_PSI2
+#define LF_PSI2 1  // HBM-bound variant: psi written every second iteration (two deferred
+#endif             // updates applied in sequence: bitwise the one-at-a-time psi), -4n/iteration
+template <int KE, bool HALO, bool IDLE = false, bool E16 = false>
 __global__ void __launch_bounds__(BS, LF_MINB_P)
     k_pcg_persistent(MeshDev m, LduDev a, Workspace ws, unsigned *bar) {
+  constexpr bool w88 = LF_W88 && !IDLE, psi2 = LF_PSI2 && !IDLE;
   PcgCtl *ctl = ws.ctl;
   if (!HALO) ws.p2p.P = 0;
   if (ctl->stop) return;
   // block-uniform solver state lives in shared memory (thread 0 updates it
   // between barriers) so it does not occupy registers across the phases
   struct St {
-    double nf, initRes, finRes, wArA, alpha, beta;
+    double nf, initRes, finRes, wArA, alpha, alphaPrev, beta;
     int k, cont, singular;
   };
   __shared__ St st;
@@ -969,10 +1014,18 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
     st.finRes = ctl->finRes;
     st.wArA = ctl->wArA;
     st.alpha = ctl->alpha;
+    st.alphaPrev = 0.0;
     st.singular = 0;
   }
   double *psi = ctl->psi;
   const double *__restrict__ w = ws.w;
+  const double *__restrict__ rr = ws.r;
+  // w at cell j: stored (w[j]) or, in the 88n variant, recomputed exactly as
+  // phase 2 / the setup formed it: (1/diag_j) r_j
+  auto wv = [&](int j) -> double {
+    if constexpr (w88) return (1.0 / a.diag[j]) * rr[j];
+    else return w[j];
+  };
   double psiSum = 0.0;  // LF_IDLE_FLUSH: this thread's sum of psi after its last flush
   // IDLE (L2-resident sizes, <= LF_STASH_TRIPS trips per thread): phase 1
   // keeps each cell's {q, diag} in shared memory (slot = trip) for phase 2,
@@ -1036,14 +1089,18 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
     __syncthreads();
     const int k = st.k;
     const bool first = (k == 0), cont = st.cont != 0;
-    const double beta = st.beta, alpha = st.alpha;
+    const double beta = st.beta, alpha = st.alpha, alphaPrev = st.alphaPrev;
     const double *__restrict__ pold = (k & 1) ? ws.p[0] : ws.p[1];
     double *__restrict__ pnew = (k & 1) ? ws.p[1] : ws.p[0];
+    // psi2: this pass writes psi when it is the last one or k is even (>= 2):
+    // psi += alpha_{k-2} p_{k-2} (still in pnew) then alpha_{k-1} p_{k-1}
+    const bool even2 = psi2 && k >= 2 && !(k & 1);
+    const bool psiPass = !psi2 || !cont || even2 || first;  // k = 0: sum(psi) for a singular stop
     auto pnb = [&](int j) {  // p at a neighbour cell (written by another block)
 #if LF_PERSIST_LDCG
       return first ? __ldcg(w + j) : fma(beta, __ldcg(pold + j), __ldcg(w + j));
 #else  // L1 was invalidated by the barrier's ld.acquire.gpu: cached loads are coherent
-      return first ? w[j] : fma(beta, pold[j], w[j]);
+      return first ? wv(j) : fma(beta, pold[j], wv(j));
 #endif
     };
     // ---- phase 1: flush psi, p = w + beta p_old, q = A p, sums
@@ -1060,8 +1117,9 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
 #endif
       if (idleF) {
         if (first) v1[1] += psi[c];
-      } else {
+      } else if (psiPass) {
         double ps = psi[c];
+        if (even2) ps = fma(alphaPrev, pnew[c], ps);  // read before pnew[c] is overwritten below
         if (!first) {
           ps = fma(alpha, pold[c], ps);
           psi[c] = ps;
@@ -1069,8 +1127,6 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
         v1[1] += ps;
       }
       if (cont) {
-        const double pc = first ? w[c] : fma(beta, pold[c], w[c]);
-        pnew[c] = pc;
 #if LF_TAIL
         // the L2-resident variant reads diag from HBM once per solve: later
         // iterations take it from the stash slot it stays in
@@ -1078,8 +1134,11 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
 #else
         const double dc = a.diag[c];
 #endif
+        const double wc = w88 ? (1.0 / dc) * rr[c] : w[c];
+        const double pc = first ? wc : fma(beta, pold[c], wc);
+        pnew[c] = pc;
         double q = dc * pc;
-        q = row_offdiag<KE>(m, a, c, q, pnb);
+        q = row_offdiag<KE, decltype(pnb), E16>(m, a, c, q, pnb);
         if (HALO) q -= row_proc_p(m, a.bBnd, ws, first, beta, k, c);
 #if LF_TAIL
         if (IDLE)
@@ -1098,7 +1157,10 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
     if (threadIdx.x == 0) {
       const double pq = __ldcg(&ws.gsum->p1[0]);
       st.singular = fabs(pq) / st.nf < 1e-300;
-      if (!st.singular) st.alpha = st.wArA / pq;
+      if (!st.singular) {
+        st.alphaPrev = st.alpha;
+        st.alpha = st.wArA / pq;
+      }
     }
     __syncthreads();
     if (st.singular) break;
@@ -1124,8 +1186,8 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
             const double rn = fma(-alpha2, q[u], r[u]);
             const double wc = (1.0 / d[u]) * rn;
             ws.r[c] = rn;
-            ws.w[c] = wc;
-            if (HALO && ws.p2p.P > 0) push_halo(m, ws.p2p.dstW, c, wc);
+            if (!w88) ws.w[c] = wc;
+            if (HALO && ws.p2p.P > 0) push_halo<HALO_W>(m, ws.p2p, c, wc);
             v2[0] += fabs(rn);
             v2[1] = fma(wc, rn, v2[1]);
           }
@@ -1150,7 +1212,7 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
             const double wc = (1.0 / qd.y) * rn;
             ws.r[c] = rn;
             ws.w[c] = wc;
-            if (HALO && ws.p2p.P > 0) push_halo(m, ws.p2p.dstW, c, wc);
+            if (HALO && ws.p2p.P > 0) push_halo<HALO_W>(m, ws.p2p, c, wc);
             v2[0] += fabs(rn);
             v2[1] = fma(wc, rn, v2[1]);
           }
@@ -1204,6 +1266,25 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
     if (threadIdx.x == 0) ++st.k;
   }
   const int k = st.k;
+  if (psi2 && st.singular && (k & 1)) {
+    // singular break after a phase 1 that deferred alpha_{k-1} p_{k-1}: apply
+    // it (OpenFOAM's psi at the break) and re-form sum(psi) for the next setup
+    const double *__restrict__ pold = ws.p[0];  // odd k: p_{k-1} in p[0]
+    const double alpha = st.alpha;
+    double vs[2] = {0.0, 0.0};
+#if LF_TAIL
+    for (int i = 0; i <= nFull; ++i) {
+      const int c = i < nFull ? cstart + i * cstep : tailC;
+      if (c < 0) break;
+#else
+    for (int c = cstart; c < cend; c += cstep) {
+#endif
+      const double ps = fma(alpha, pold[c], psi[c]);
+      psi[c] = ps;
+      vs[1] += ps;
+    }
+    grid_reduce_sync<2, HALO>(vs, ws.partials, bar, ws.gsum->p1, ws.p2p LF_DBG_ARG(LF_DBG_N - 1));
+  }
 #if LF_TIMING
   if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x / 2) && k > 0)
     printf("LF_TIMING block %d iters %d: phase1 %.2f us, bar1 %.2f us, phase2 %.2f us, bar2 %.2f us\n",
@@ -1257,15 +1338,17 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
 
 // co-resident grid for every persistent variant that may be launched on a
 // mesh (any row layout: the full-row rows are chosen after this call)
-template <int KE>
+template <int KE, bool E16 = false>
 static void persistent_occupancy(int &best) {
   int nb = 0;
-  for (const void *fn : {(const void *)k_pcg_persistent<KE, false>, (const void *)k_pcg_persistent<KE, true>}) {
+  for (const void *fn : {(const void *)k_pcg_persistent<KE, false, false, E16>,
+                         (const void *)k_pcg_persistent<KE, true, false, E16>}) {
     LF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, BS, 0));
     best = std::min(best, nb);
   }
   // the L2-resident variants with the shared-memory stash
-  for (const void *fi : {(const void *)k_pcg_persistent<KE, false, true>, (const void *)k_pcg_persistent<KE, true, true>}) {
+  for (const void *fi : {(const void *)k_pcg_persistent<KE, false, true, E16>,
+                         (const void *)k_pcg_persistent<KE, true, true, E16>}) {
     LF_CUDA(cudaFuncSetAttribute(fi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stash_bytes()));
     LF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fi, BS, stash_bytes()));
     best = std::min(best, nb);
@@ -1276,10 +1359,13 @@ int persistent_grid(int device, int K) {
   int sms = 0;
   LF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
   int best = 1 << 30;
-  if (K == 4)
+  if (K == 4) {
     persistent_occupancy<4>(best);
-  else if (K > 0)
+    persistent_occupancy<4, true>(best);
+  } else if (K > 0) {
     persistent_occupancy<3>(best);
+    persistent_occupancy<3, true>(best);
+  }
   else {
     persistent_occupancy<0>(best);
     persistent_occupancy<-6>(best);
@@ -1290,8 +1376,11 @@ int persistent_grid(int device, int K) {
 
 template <bool HALO, bool IDLE = false>
 static const void *persistent_fn(const MeshDev &m) {
-  return (!LF_NO_ELL && m.K == 4) ? (const void *)k_pcg_persistent<4, HALO, IDLE>
-         : (!LF_NO_ELL && m.K > 0) ? (const void *)k_pcg_persistent<3, HALO, IDLE>
+  const bool e16 = m.codeE != nullptr;
+  return (!LF_NO_ELL && m.K == 4) ? (e16 ? (const void *)k_pcg_persistent<4, HALO, IDLE, true>
+                                         : (const void *)k_pcg_persistent<4, HALO, IDLE>)
+         : (!LF_NO_ELL && m.K > 0) ? (e16 ? (const void *)k_pcg_persistent<3, HALO, IDLE, true>
+                                          : (const void *)k_pcg_persistent<3, HALO, IDLE>)
          : m.KS == 6               ? (const void *)k_pcg_persistent<-6, HALO, IDLE>
          : m.KS == 8               ? (const void *)k_pcg_persistent<-8, HALO, IDLE>
                                    : (const void *)k_pcg_persistent<0, HALO, IDLE>;
@@ -1467,6 +1556,67 @@ __global__ void k_build_ell(MeshDev m, const int32_t *__restrict__ owner, int32_
 void launch_build_ell(cudaStream_t s, const MeshDev &m, const int32_t *owner, int32_t K, int32_t *nbrE,
                       int32_t *loE) {
   k_build_ell<<<grid_for(m.n), BS, 0, s>>>(m, owner, K, nbrE, loE);
+}
+
+// ------------------------------------------------ compressed ELL labels
+// The solve is HBM-bound and the two int32 labels of an ELL slot are a third
+// of its face bytes.  Within 32 consecutive cells (one warp of a grid-stride
+// trip) the label offsets nbr - c and c - owner of a slot take few distinct
+// values on any locally numbered mesh (+1, +N, +N^2 on a block mesh), so each
+// slot stores them as 16-bit codes relative to the group's most frequent
+// offset (one u32 per slot and cell: low half owner side, high half
+// neighbour side = 2 bits of owner-slot kk + 14-bit offset):
+//   nb:  0xFFFF none, 0xFFFE escape (label in nbrE), else c + off.x + d - 0x8000
+//   lo:  0xFFFF none, 0xFFFE escape (packed in loE),
+//        else kk = d >> 14, owner = c - off.y - (d & 0x3FFF) + 0x2000
+// 12 B per face slot instead of 16 B; the escape arrays are touched only by
+// the (rare) lanes that need them.  Decoded labels are bitwise the int32 ones.
+__device__ __forceinline__ int warp_mode(int v, bool valid) {
+  // most frequent valid value among the 32 lanes (ties: lowest lane); 0 if none
+  const unsigned same = __match_any_sync(FULL, valid ? v : INT_MIN);
+  const int lane = threadIdx.x & 31;
+  int key = valid ? (__popc(same) << 5) | (31 - lane) : -1;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) key = max(key, __shfl_xor_sync(FULL, key, o));
+  const int src = key < 0 ? 0 : 31 - (key & 31);
+  const int mv = __shfl_sync(FULL, v, src);
+  return key < 0 ? 0 : mv;
+}
+
+__global__ void k_build_ell16(MeshDev m, uint32_t *__restrict__ codeE, int2 *__restrict__ offE,
+                              int32_t *nEsc) {
+  const int lane = threadIdx.x & 31, ld = m.ldE;
+  const long nw = (long)m.K * m.ngE;
+  int esc = 0;
+  for (long wi = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; wi < nw;
+       wi += ((long)gridDim.x * blockDim.x) >> 5) {
+    const int k = (int)(wi / m.ngE), g = (int)(wi % m.ngE), c = g * 32 + lane;
+    const bool in = c < m.n;
+    const int nb = in ? m.nbrE[k * ld + c] : -1, lo = in ? m.loE[k * ld + c] : -1;
+    const int vn = nb - c, vl = c - (lo & ELL_MASK);
+    const int on = warp_mode(vn, nb >= 0), ol = warp_mode(vl, lo >= 0);
+    unsigned cn = 0xFFFFu, cl = 0xFFFFu;
+    if (nb >= 0) {
+      const long d = (long)vn - on + 0x8000;
+      cn = (d >= 0 && d <= 0xFFFD) ? (unsigned)d : 0xFFFEu;
+    }
+    if (lo >= 0) {
+      const long d = (long)vl - ol + 0x2000;
+      const unsigned kk = (unsigned)lo >> ELL_SHIFT;
+      const unsigned code = (unsigned)(kk << 14) | (unsigned)d;
+      cl = (d >= 0 && d <= 0x3FFF && code < 0xFFFEu) ? code : 0xFFFEu;
+    }
+    esc += (cn == 0xFFFEu) + (cl == 0xFFFEu);
+    if (in) codeE[k * ld + c] = cn | (cl << 16);
+    if (lane == 0) offE[(long)k * m.ngE + g] = make_int2(on, ol);
+  }
+  if (esc) atomicAdd(nEsc, esc);  // integer statistic only
+}
+
+void launch_build_ell16(cudaStream_t s, const MeshDev &m, uint32_t *codeE, int2 *offE, int32_t *nEsc) {
+  LF_CUDA(cudaMemsetAsync(nEsc, 0, sizeof(int32_t), s));
+  const long threads = (long)m.K * m.ngE * 32;
+  k_build_ell16<<<grid_for(threads), BS, 0, s>>>(m, codeE, offE, nEsc);
 }
 
 // ------------------------------------------------------------- CUB sorts

@@ -91,6 +91,13 @@ struct MeshDev {
   // slot k of cell c at k*n + c.  See kernels.cu header.
   int32_t K, ldE;  // ldE: slab stride (n rounded up to 4: 16-byte aligned slabs)
   const int32_t *nbrE, *loE;
+  // the same labels compressed to 16 bits each (one u32 per slot and cell,
+  // kernels.cu "compressed ELL labels"): codeE[k*ldE + c], per-(slot, 32-cell
+  // group) offsets offE[k*ngE + c/32]; escapes fall back to nbrE/loE.  null:
+  // not built (the persistent solve then gathers through nbrE/loE)
+  const uint32_t *codeE;
+  const int2 *offE;
+  int32_t ngE;
   // full-row ELL (the DIC rows, DicDev): used by the Amul gathers of meshes
   // with more than 4 faces on a side (K == 0) and at most 8 neighbours
   int32_t KS, ldS;
@@ -134,13 +141,21 @@ struct Launch {
 // (f64) in one IPC-exported allocation; every rank holds mapped pointers to
 // all mailboxes.  P == 0: transport off.
 constexpr int LF_MAXP = 16;
+constexpr int LF_MAXSEG = 16;  // processor patches (halo segments) per rank
 struct P2PDev {
   int32_t P, rank;
   unsigned *seq;              // own allreduce sequence counter (device)
   unsigned *flags[LF_MAXP];   // mailbox flags of every rank (mapped)
   double *vals[LF_MAXP];      // mailbox values of every rank (mapped)
-  double **dstW, **dstT;      // [n_proc] destination of each send slot in the
-                              // neighbour's recvW / recvT (own buffer for self pairs)
+  // halo destinations, base + offset per segment: local send slots
+  // [segBeg[g], segBeg[g+1]) go to dstW[g][slot - segBeg[g]] in the
+  // neighbour's recvW (own buffer for self pairs), likewise recvT, which is
+  // double-buffered by the parity tPar of the push (a standalone ldu_amul on
+  // one rank may still read parity p while a faster rank pushes p ^ 1)
+  int32_t nseg, tPar;
+  int32_t segBeg[LF_MAXSEG + 1];
+  double *dstW[LF_MAXSEG];
+  double *dstT[2][LF_MAXSEG];
 };
 
 struct Workspace {
@@ -152,7 +167,7 @@ struct Workspace {
   RedSlots *lsum;       // local sums (== gsum when single rank or P2P)
   // processor-patch halos (slot = flat processor-face index, n_proc slots)
   double *sendBuf;      // staging for NCCL / local copies
-  double *recvT, *recvW;  // neighbour T (assembly) and w (PCG) at each slot
+  double *recvT, *recvW;  // neighbour T (assembly; [2][n_proc] by push parity) and w (PCG) at each slot
   double *pH[2];        // p at the halo slots, recomputed locally (double-buffered like p)
   int32_t *sendCell;    // [n_proc] local cell of each send slot
   int maxGrid;
@@ -236,6 +251,9 @@ void launch_gather_i32(cudaStream_t s, int64_t n, const int32_t *idx, const int3
                        int32_t *out);
 void launch_build_ell(cudaStream_t s, const MeshDev &m, const int32_t *owner, int32_t K, int32_t *nbrE,
                       int32_t *loE);
+// compressed labels from nbrE/loE (md.K, md.ldE, md.nbrE, md.loE set);
+// *nEsc (device int, zeroed here) receives the number of escaped entries
+void launch_build_ell16(cudaStream_t s, const MeshDev &m, uint32_t *codeE, int2 *offE, int32_t *nEsc);
 // CUB wrappers (kernels.cu): stable radix sort of (key, value) pairs.
 void sort_pairs_u64(cudaStream_t s, uint64_t *keys, int32_t *vals, int64_t m, int end_bit);
 void sort_pairs_i32(cudaStream_t s, int32_t *keys, int32_t *vals, int64_t m, int end_bit);

@@ -475,6 +475,9 @@ static void build_mesh(lf_context *ctx, const lf_mesh_desc *d, lf_mesh *M) {
   // packed owner-slot label fits (n < 2^29), else the CSR gather is used.
   md.K = 0;
   md.nbrE = md.loE = nullptr;
+  md.codeE = nullptr;
+  md.offE = nullptr;
+  md.ngE = 0;
   L.upperE = nullptr;
   md.KS = md.ldS = 0;  // full-row ELL: built at the end for K > 4 meshes
   md.symN = nullptr;
@@ -497,6 +500,18 @@ static void build_mesh(lf_context *ctx, const lf_mesh_desc *d, lf_mesh *M) {
       launch_build_ell(s, md, owner, KE, nbrE, loE);
       md.nbrE = nbrE;
       md.loE = loE;
+      if (ctx->compressedLabels) {
+        // 16-bit label codes for the HBM-bound gathers (kernels.cu, k_build_ell16)
+        md.ngE = (n + 31) / 32;
+        uint32_t *codeE = A.alloc<uint32_t>((size_t)KE * ld);
+        int2 *offE = A.alloc<int2>((size_t)KE * md.ngE);
+        int32_t *dEsc = A.alloc<int32_t>(1);
+        launch_build_ell16(s, md, codeE, offE, dEsc);
+        LF_CUDA(cudaMemcpyAsync(&M->ell16Escapes, dEsc, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        LF_CUDA(cudaStreamSynchronize(s));
+        md.codeE = codeE;
+        md.offE = offE;
+      }
     }
   }
 
@@ -567,13 +582,13 @@ static void build_mesh(lf_context *ctx, const lf_mesh_desc *d, lf_mesh *M) {
   ws.pH[0] = A.alloc<double>(nproc);
   ws.pH[1] = A.alloc<double>(nproc);
   // one cudaMalloc block (IPC-exportable for the peer-memory transport):
-  // [mailbox flags 2*MAXP u32 | mailbox vals 2*MAXP*4 f64 | recvT | recvW]
+  // [mailbox flags 2*MAXP u32 | mailbox vals 2*MAXP*4 f64 | recvT[2] | recvW]
   {
     auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
     M->offFlags = 0;
     M->offVals = up(2 * LF_MAXP * sizeof(unsigned));
     M->offRecvT = up(M->offVals + 2 * LF_MAXP * 4 * sizeof(double));
-    M->offRecvW = up(M->offRecvT + sizeof(double) * std::max(nproc, 1));
+    M->offRecvW = up(M->offRecvT + 2 * sizeof(double) * std::max(nproc, 1));  // recvT[2][nproc]
     M->p2pBytes = up(M->offRecvW + sizeof(double) * std::max(nproc, 1));
     M->p2pBlock = A.alloc<char>(M->p2pBytes);
     LF_CUDA(cudaMemsetAsync(M->p2pBlock, 0, M->p2pBytes, s));

@@ -1,7 +1,7 @@
 // Peer-memory transport (SURVEY.md §8(e) "Halo, option A: P2P").
 //
 // Every rank exports ONE cudaMalloc block per mesh with cudaIpcGetMemHandle:
-//   [mailbox flags | mailbox values | recvT | recvW]
+//   [mailbox flags | mailbox values | recvT[2] | recvW]
 // and maps every other rank's block with cudaIpcOpenMemHandle (over NVLink
 // between GPUs; the same physical memory for ranks sharing a GPU).  The
 // kernels then
@@ -92,14 +92,20 @@ void p2p_connect(lf_mesh *M, int nranks, int rank, const void *handles) {
     P.flags[q] = reinterpret_cast<unsigned *>(base[q] + H[q].offFlags);
     P.vals[q] = reinterpret_cast<double *>(base[q] + H[q].offVals);
   }
-  // destination of every send slot: the matching slot of the neighbour's
-  // segment towards us (i-th patch to s <-> s's i-th patch to us), or the
-  // partner segment of a self pair
-  std::vector<double *> dstW(std::max(M->nproc, 1)), dstT(std::max(M->nproc, 1));
+  // destination of every segment: the matching segment of the neighbour's
+  // halo towards us (i-th patch to s <-> s's i-th patch to us), or the
+  // partner segment of a self pair — one base pointer per segment (and per
+  // parity of the double-buffered recvT); a slot adds its offset in the segment
+  LF_REQUIRE((int)M->segs.size() <= LF_MAXSEG,
+             "more than " + std::to_string(LF_MAXSEG) + " processor patches on one rank");
   std::vector<int> used(nranks, 0);
+  P.nseg = (int32_t)M->segs.size();
+  P.tPar = 0;
   for (size_t g = 0; g < M->segs.size(); ++g) {
     const HaloSeg &sg = M->segs[g];
-    int32_t off;
+    LF_REQUIRE(g == 0 ? sg.offset == 0 : sg.offset == M->segs[g - 1].offset + M->segs[g - 1].count,
+               "processor segments must tile the send slots in order");
+    int32_t off, rn;
     char *b;
     int64_t oT, oW;
     if (sg.peer == rank) {
@@ -108,6 +114,7 @@ void p2p_connect(lf_mesh *M, int nranks, int rank, const void *handles) {
       b = base[rank];
       oT = (int64_t)M->offRecvT;
       oW = (int64_t)M->offRecvW;
+      rn = M->nproc;
     } else {
       const Handle &hs = H[sg.peer];
       int found = -1, k = 0;
@@ -125,19 +132,16 @@ void p2p_connect(lf_mesh *M, int nranks, int rank, const void *handles) {
       b = base[sg.peer];
       oT = hs.offRecvT;
       oW = hs.offRecvW;
+      rn = hs.nproc;
     }
-    for (int32_t i = 0; i < sg.count; ++i) {
-      dstT[sg.offset + i] = reinterpret_cast<double *>(b + oT) + off + i;
-      dstW[sg.offset + i] = reinterpret_cast<double *>(b + oW) + off + i;
-    }
+    P.segBeg[g] = sg.offset;
+    P.dstW[g] = reinterpret_cast<double *>(b + oW) + off;
+    P.dstT[0][g] = reinterpret_cast<double *>(b + oT) + off;
+    P.dstT[1][g] = reinterpret_cast<double *>(b + oT) + rn + off;  // parity-1 half of its recvT
   }
-  double **dW = M->arena.alloc<double *>(dstW.size()), **dT = M->arena.alloc<double *>(dstT.size());
-  LF_CUDA(cudaMemcpyAsync(dW, dstW.data(), sizeof(double *) * dstW.size(), cudaMemcpyHostToDevice, s));
-  LF_CUDA(cudaMemcpyAsync(dT, dstT.data(), sizeof(double *) * dstT.size(), cudaMemcpyHostToDevice, s));
+  P.segBeg[P.nseg] = M->nproc;
   P.seq = M->arena.alloc<unsigned>(1);
   LF_CUDA(cudaMemsetAsync(P.seq, 0, sizeof(unsigned), s));
-  P.dstW = dW;
-  P.dstT = dT;
   P.P = nranks;
   P.rank = rank;
   double total = 0.0;  // gAverage denominator: rank-ordered sum of the cell counts

@@ -85,8 +85,10 @@ static void exchange_field(lf_mesh *M, const double *x, double *recv) {
 void field_halo(lf_mesh *M, const double *x) {
   if (M->nproc == 0) return;
   lf_context *ctx = M->ctx;
-  if (M->p2pConnected)
+  if (M->p2pConnected) {
+    M->ws.p2p.tPar = M->tPar ^= 1;  // the other recvT half: a slower rank may still read this one
     ctx->launch(LF_K_SUMPSI, [&] { launch_sum(ctx->stream, M->Lsum, M->md, x, M->ws, M->scratch); });
+  }
   else
     exchange_field(M, x, M->ws.recvT);
 }
@@ -203,6 +205,7 @@ static void run_iterations(lf_mesh *M, lf_solver_perf *out) {
 
 static void sum_psi(lf_mesh *M, const double *psi) {
   lf_context *ctx = M->ctx;
+  if (M->p2pConnected) M->ws.p2p.tPar = M->tPar ^= 1;  // this launch also pushes the T halo
   ctx->launch(LF_K_SUMPSI, [&] { launch_sum(ctx->stream, M->Lsum, M->md, psi, M->ws, &M->ws.lsum->p1[1]); });
   allreduce(M, M->ws.lsum->p1, M->ws.gsum->p1, 2);
 }
@@ -242,11 +245,11 @@ void solve_loop(lf_mesh *M, const lf_solver_controls *c, double *psi, bool fromA
   if (host_halo(M)) exchange_field(M, psi, ws.recvT);
   if (fromAssembly) {
     ctx->launch(LF_K_ASSEMBLE, [&] {
-      launch_assemble(s, M->Lasm, mesh_for(M, p), M->ld, p->DT, 1.0 / p->dt, psi, ws.recvT, true, ws, T0,
+      launch_assemble(s, M->Lasm, mesh_for(M, p), M->ld, p->DT, 1.0 / p->dt, psi, M->haloT(), true, ws, T0,
                       lapSrc);
     });
   } else {
-    ctx->launch(LF_K_SETUP, [&] { launch_pcg_setup(s, M->Lsetup, M->md, M->ld, ws.recvT, ws); });
+    ctx->launch(LF_K_SETUP, [&] { launch_pcg_setup(s, M->Lsetup, M->md, M->ld, M->haloT(), ws); });
   }
   if (host_halo(M)) exchange_field(M, ws.w, ws.recvW);  // w of the setup for iteration 0
   allreduce(M, ws.lsum->setup, ws.gsum->setup, 3);

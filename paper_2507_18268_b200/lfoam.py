@@ -29,7 +29,7 @@ KERNELS = {"assemble": 0, "setup": 1, "phase1": 2, "phase2": 3, "amul": 4, "sump
 PRECONDITIONERS = {"diagonal": 0, "DIC": 1, "DILU": 2}
 # lf_mesh_desc.renumber
 RENUMBER = {False: 0, True: 1, 0: 0, 1: 1, 2: 2, "none": 0, "rcm": 1, "colour": 2}
-OPTIONS = {"persistent": 0, "graphs": 1, "variant": 2}
+OPTIONS = {"persistent": 0, "graphs": 1, "variant": 2, "compressed_labels": 3}
 
 
 class LfoamError(RuntimeError):
@@ -86,6 +86,7 @@ SIGNATURES = {
     "mesh_create": (C.c_int, [_vp, C.POINTER(MeshDesc), C.POINTER(_vp)]),
     "mesh_destroy": (C.c_int, [_vp]),
     "lf_mesh_info": (C.c_int, [_vp, C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i64)]),
+    "lf_mesh_layout": (C.c_int, [_vp, C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i32)]),
     "lf_mesh_export_addressing": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "lf_permute": (C.c_int, [_vp, C.c_int, _vp, _vp]),
     "field_set": (C.c_int, [_vp, C.c_int, _i32, _vp, _i64, C.c_int]),
@@ -164,6 +165,13 @@ def _check_dev(t, n):
     if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64
             and t.is_contiguous() and t.numel() == n):
         raise ValueError(f"expected a contiguous float64 CUDA tensor with {n} elements")
+
+
+def _check_host_out(a, n):
+    """A host output buffer must be a writable C-contiguous float64 array of n."""
+    if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.c_contiguous
+            and a.flags.writeable and a.size == n):
+        raise ValueError(f"expected a writable C-contiguous float64 numpy array with {n} elements")
 
 
 class Context:
@@ -283,6 +291,12 @@ class Mesh:
         _check(lib().lf_mesh_info(self.h, C.byref(n), C.byref(F), C.byref(B), C.byref(b)))
         return dict(n_cells=n.value, n_faces=F.value, n_boundary_faces=B.value, device_bytes=b.value)
 
+    def layout(self):
+        """Gather layout of the mesh (lf_mesh_layout)."""
+        k, ks, esc = C.c_int32(), C.c_int32(), C.c_int32()
+        _check(lib().lf_mesh_layout(self.h, C.byref(k), C.byref(ks), C.byref(esc)))
+        return dict(ell_width=k.value, row_width=ks.value, label_escapes=esc.value)
+
     def p2p_export(self) -> bytes:
         buf = C.create_string_buffer(P2P_HANDLE_BYTES)
         _check(lib().lf_p2p_export(self.h, buf))
@@ -318,6 +332,7 @@ class Mesh:
             _device_sync()
             return out
         a = np.zeros(self.n_cells) if out is None else out
+        _check_host_out(a, self.n_cells)
         _check(lib().field_get(self.h, FIELD_T, -1, _ptr(a), self.n_cells, 0))
         return a
 
@@ -326,6 +341,7 @@ class Mesh:
         use it unless called with variable_DT=False."""
         if _is_device(v):
             _check_dev(v, self.n_cells)
+            _device_sync()   # torch's producer stream before the library reads v
             _check(lib().field_set(self.h, FIELD_DT, -1, _ptr(v), self.n_cells, 1))
         else:
             a = _host(v, np.float64)

@@ -16,6 +16,12 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "gpurun_out")
 PROF = os.environ.get("NCU_SUMMARY_DIR", os.path.join(ROOT, "profiles"))
+sys.path.insert(0, ROOT)
+from bench import build_id  # noqa: E402
+
+# the build the reports were captured on: NCU_BUILD (written by the profiling
+# script on the box), else the current sources
+BUILD = os.environ.get("NCU_BUILD") or build_id()
 
 DETAILS = ["Duration", "Elapsed Cycles", "SM Active Cycles", "DRAM Throughput", "Memory Throughput",
            "L2 Hit Rate", "L1/TEX Hit Rate", "Achieved Occupancy", "Registers Per Thread", "Grid Size",
@@ -82,7 +88,7 @@ def main(tag):
     tj_path = os.path.join(PROF, "ncu_traffic.json")
     tj = json.load(open(tj_path)) if os.path.exists(tj_path) else {}
     for rep in sorted(glob.glob(os.path.join(OUT, f"prof_{tag}_cfg*_k_*.ncu-rep"))):
-        m = re.search(r"cfg(\d+(?:-corr\d+)?(?:-dt)?(?:-dic)?)_(k_\w+)\.ncu-rep", rep)
+        m = re.search(r"cfg(\d+(?:-corr\d+)?(?:-dt)?(?:-dic)?(?:-gamg)?(?:-rcm)?)_(k_\w+)\.ncu-rep", rep)
         cfg, kern = m.group(1), m.group(2)
         det, rd, traffic = summarise(rep)
         lines.append(f"## config {cfg} — `{kern}`")
@@ -94,10 +100,11 @@ def main(tag):
             lines.append(f"- `{k}`: {v} {u}")
         if traffic is not None:
             lines.append(f"- traffic (DRAM read+write): {traffic / 1e6:.1f} MB per launch")
-            tj.setdefault(f"config{cfg}", {})[kern] = traffic
+            # tied to the device-code build it was captured on (bench.py drops stale figures)
+            tj.setdefault(f"config{cfg}", {})[kern] = {"bytes": traffic, "build": BUILD, "tag": tag}
         lines.append("")
     for path in sorted(glob.glob(os.path.join(OUT, f"launches_{tag}_cfg*.csv"))):
-        cfg = re.search(r"cfg(\d+(?:-corr\d+)?(?:-dt)?(?:-dic)?)", path).group(1)
+        cfg = re.search(r"cfg(\d+(?:-corr\d+)?(?:-dt)?(?:-dic)?(?:-gamg)?(?:-rcm)?)", path).group(1)
         agg = launch_table(path)
         lines.append(f"## config {cfg} — launch list (`--metrics gpu__time_duration.sum,dram__bytes_*`)")
         lines.append("")

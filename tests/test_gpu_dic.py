@@ -320,3 +320,54 @@ def test_dic_multicolour_8_neighbours(ctx):
     np.testing.assert_array_equal(rD.cpu().numpy(), rD_o)
     np.testing.assert_array_equal(w.cpu().numpy(), w_o)
     mesh.close()
+
+
+@pytest.mark.parametrize("name", ["cube8", "box_mixed", "colour9"])
+@pytest.mark.parametrize("variant", [1, 2])
+def test_step_dic_forced_variants(name, variant):
+    """Both persistent DIC variants forced on small colour-numbered meshes:
+    variant 2 is the HBM-bound one (two contiguous colours interleaved in the
+    Amul phase, the `pair` path the 200^3/400^3 benches run), variant 1 the
+    L2-resident one (stash) — 5 steps vs the oracle in the same numbering."""
+    import paper_2507_18268_b200 as _P
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    m = MESHES[name]()
+    order = meshgen.colour_order(m)
+    mo = meshgen.relabel_mesh(m, order)
+    T0 = meshgen.multimode_field(m)
+    To, _, po = oracle.laplacian_foam(mo, T0[order], 5, precond="DIC")
+    c = _P.Context(0)
+    c.set_option("variant", variant)
+    mesh = _P.Mesh(c, m, renumber="colour")
+    mesh.set_T(T0)
+    pg = mesh.step(5, precond="DIC")
+    T = mesh.get_T()[order]
+    assert np.max(np.abs(T - To)) <= 1e-8 * np.max(np.abs(To))
+    assert all(abs(a["n_iterations"] - b["n_iterations"]) <= 1 for a, b in zip(pg, po)), (pg, po)
+    assert all(a["converged"] == b["converged"] for a, b in zip(pg, po))
+    mesh.close()
+    c.close()
+
+
+def test_config3_dic_hbm_vs_oracle_and_closed_form(ctx, canonical_constants):
+    """The DIC bench workload at config 3 (200^3, colour numbering) through the
+    HBM-bound DIC path it is benched with: step 0 against the oracle on every
+    cell (same numbering), then 5 steps against T^5 = g^5 s."""
+    row = [r for r in canonical_constants["rows"] if r["N"] == 200][0]
+    m = meshgen.block_mesh(200)
+    order = meshgen.colour_order(m)
+    mo = meshgen.relabel_mesh(m, order)
+    s = meshgen.canonical_field(m)
+    To, _, po = oracle.laplacian_foam(mo, s[order], 1, precond="DIC")
+    mesh = P.Mesh(ctx, m, renumber="colour")
+    mesh.set_T(s)
+    pg = mesh.step(1, precond="DIC")
+    T = mesh.get_T()
+    assert np.max(np.abs(T[order] - To)) <= 1e-8 * np.max(np.abs(To))
+    assert abs(pg[0]["n_iterations"] - po[0]["n_iterations"]) <= 1, (pg, po)
+    pg += mesh.step(4, precond="DIC")
+    ref = row["g"] ** 5 * s
+    assert np.max(np.abs(mesh.get_T() - ref)) <= 1e-8 * np.max(np.abs(ref))
+    assert all(p["converged"] for p in pg)
+    mesh.close()

@@ -200,3 +200,82 @@ def test_p2p_two_processes_one_gpu_dic(P):
         assert np.max(np.abs(Tr - To)) <= 1e-8 * np.max(np.abs(To))
         assert all(abs(a - b) <= 1 for a, b in zip(its, its_o)), (its, its_o)
     assert res[0][3] == res[1][3]
+
+
+def _amul_rank_main(rank, world, port, out):
+    """Back-to-back standalone ldu_amul calls with different x through the
+    peer-memory halo (the T halo of call i+1 must not overwrite
+    the one a slower rank still reads in call i — recvT is double-buffered by
+    push parity).  Rank 1 is slowed down between calls."""
+    import time
+    import torch.distributed as dist
+    import paper_2507_18268_b200 as P
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    try:
+        g = meshgen.block_mesh(24, 20, 22, bc={"xmax": "zeroGradient"})
+        part = decompose.slab_partition(g, world)
+        m, cells = decompose.local_mesh(g, part, rank)
+        ctx = P.Context(0)
+        ctx.p2p_init(world, rank)
+        mesh = P.Mesh(ctx, m)
+        hs = [None] * world
+        dist.all_gather_object(hs, mesh.p2p_export())
+        mesh.p2p_connect(hs, rank)
+        T0 = meshgen.multimode_field(g)[cells]
+        mesh.set_T(T0)
+        ldu = mesh.assemble(1.0, 0.2)
+        ys = []
+        for i in range(12):
+            x = torch.as_tensor(meshgen.random_field(g, seed=100 + i)[cells], device="cuda")
+            y = torch.empty_like(x)
+            if rank == 1 and i % 2:
+                time.sleep(0.02)
+            ldu.amul(x, y)
+            ys.append(y.cpu().numpy())
+        # and a solve right after an Amul (same halo buffers)
+        psi = torch.as_tensor(T0, device="cuda")
+        perf = ldu.pcg_solve(psi)
+        out[rank] = ("ok", cells, ys, psi.cpu().numpy(), perf["n_iterations"])
+        dist.barrier()
+        ctx.close()
+    except Exception as e:
+        out[rank] = ("error", repr(e))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_p2p_two_processes_back_to_back_amul(P):
+    import torch.multiprocessing as mp
+    world = 2
+    mctx = mp.get_context("spawn")
+    out = mctx.Manager().dict()
+    port = _free_port()
+    procs = [mctx.Process(target=_amul_rank_main, args=(r, world, port, out)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+    for p in procs:
+        if p.is_alive():
+            p.kill()
+    res = dict(out)
+    assert len(res) == world, res
+    for r in range(world):
+        assert res[r][0] == "ok", res[r]
+    g = meshgen.block_mesh(24, 20, 22, bc={"xmax": "zeroGradient"})
+    T0 = meshgen.multimode_field(g)
+    ref = oracle.assemble(g, 1.0, 0.2, T0)
+    for i in range(12):
+        x = meshgen.random_field(g, seed=100 + i)
+        y_ref = oracle.amul(g, ref["diag"], ref["upper"], x)
+        scale = np.abs(ref["diag"] * x) + 6 * np.abs(ref["upper"]).max() * np.abs(x).max()
+        for r in range(world):
+            _, cells, ys, _, _ = res[r]
+            assert np.max(np.abs(ys[i] - y_ref[cells]) / scale[cells]) <= 1e-12, (i, r)
+    x_ref, p_ref = oracle.pcg(g, ref, T0)
+    for r in range(world):
+        _, cells, _, psi, it = res[r]
+        assert np.max(np.abs(psi - x_ref[cells])) <= 1e-8 * np.max(np.abs(x_ref))
+        assert abs(it - p_ref["n_iterations"]) <= 1
