@@ -56,11 +56,12 @@ def parse():
                     help="N>1 data path: peer memory (CUDA IPC over NVLink, fused into the kernels) or NCCL")
     ap.add_argument("--renumber", type=int, default=-1,
                     help="0 none, 1 RCM, 2 multicolour (default: 2 with --precond DIC, else 0)")
-    ap.add_argument("--precond", default="diagonal", choices=["diagonal", "DIC"],
+    ap.add_argument("--precond", default="diagonal", choices=["diagonal", "DIC", "GAMG"],
                     help="PCG preconditioner: the paper's diagonal (P:608), or SURVEY §8(f) row 3's DIC "
-                         "(level-scheduled sweeps; 2 levels under the multicolour numbering)")
-    ap.add_argument("--labels", default="compressed", choices=["compressed", "int32"],
-                    help="gather labels of ELL meshes: 16-bit codes (default) or the int32 labels")
+                         "(level-scheduled sweeps; 2 levels under the multicolour numbering) or GAMG "
+                         "(agglomeration multigrid V-cycle, P:773, reading A43)")
+    ap.add_argument("--labels", default="int32", choices=["compressed", "int32"],
+                    help="gather labels of ELL meshes: the int32 labels (default) or 16-bit codes")
     ap.add_argument("--variant", type=int, default=0,
                     help="persistent solve variant: 0 by mesh size, 1 L2-resident, 2 HBM-bound")
     ap.add_argument("--mode", default="persistent", choices=["persistent", "graphs", "direct"],
@@ -291,9 +292,37 @@ def l2_resident(n, F, device):
 def impl_iter_bytes(n, F, l2res):
     """What the shipped persistent solve moves per iteration by its own
     design (DESIGN.md §5): L2-resident variant {q, diag} on chip, 72n + 16F;
-    HBM-bound variant 96n + 16F (w stored)."""
-    return (72 * n + 16 * F) if l2res else (96 * n + 16 * F)
+    HBM-bound variant 88n + 16F (w stored, psi read and written every second
+    iteration: 96n - 8n)."""
+    return (72 * n + 16 * F) if l2res else (88 * n + 16 * F)
 
+
+
+def gamg_vcycle_bytes(h):
+    """Algorithmic bytes of one V-cycle (DESIGN.md §5 GAMG): per level l < L
+    down pass b, rD, D (24n) + faces (coefficient + 2 labels, 16F) + member
+    labels (4n) + b_{l+1} written (8n'); up pass b, rD, D (24n) + faces (16F)
+    + agg (4n) + x_{l+1} (8n') + x written (8n); the coarsest solve reads its
+    dense inverse (8 n_L^2) and b, writes x (16 n_L)."""
+    n, nf = h["n"], h["nf"]
+    L = len(n) - 1
+    b = sum(68 * n[l] + 32 * nf[l] + 16 * n[l + 1] for l in range(L))
+    return b + 8 * n[L] ** 2 + 16 * n[L]
+
+
+def gamg_iter_bytes(h):
+    n0, f0 = h["n"][0], h["nf"][0]
+    return 56 * n0 + 16 * f0 + 24 * n0 + gamg_vcycle_bytes(h)
+
+
+def gamg_launch_bytes(h):
+    """Galerkin set-up per level (members' D, internal faces' U, fine faces'
+    U with their labels read: 12n + 24F; D, rD, U written: 16n' + 8F'),
+    rD_0 (16n), the final psi flush (24n)."""
+    n, nf = h["n"], h["nf"]
+    L = len(n) - 1
+    b = sum(12 * n[l] + 24 * nf[l] + 16 * n[l + 1] + 8 * nf[l + 1] for l in range(L))
+    return b + 16 * n[0] + 24 * n[0]
 
 
 def run_ours(args):
@@ -404,6 +433,7 @@ def run_ours(args):
     n_as, ms_as = ctx.kernel_stats("assemble")
     n_pcg, ms_pcg = ctx.kernel_stats("pcg")
     n_dic, ms_dic = ctx.kernel_stats("pcg_dic")
+    n_gamg, ms_gamg = ctx.kernel_stats("pcg_gamg")
     n_no, ms_no = ctx.kernel_stats("nonorth")
     B_local = sum(p.n_faces for p in m.patches)
     # grad gather (40n + 40F + 37B) + correction gather (40n + 48F), per pass
@@ -416,7 +446,16 @@ def run_ours(args):
     bytes_p2 = 32 * n_local
     peak, peak_kind = measured_peak()
     l2res = l2_resident(n_local, F_local, device)
-    if n_dic > 0:
+    if n_gamg > 0:
+        # persistent GAMG-PCG solve (DESIGN.md §5 GAMG): per iteration phase 1
+        # (56n + 16F), r update (24n) and one V-cycle; per launch the Galerkin
+        # set-up and the psi flush (24n)
+        kernel = "k_pcg_gamg"
+        gh = mesh.gamg_hierarchy()
+        total_bytes = iters * gamg_iter_bytes(gh) + n_gamg * gamg_launch_bytes(gh)
+        impl_bytes = total_bytes
+        k_launches, k_ms = n_gamg, ms_gamg
+    elif n_dic > 0:
         # persistent DIC solve (SURVEY §8(d) has no DIC row, so the
         # implementation's count is the algorithmic one): per iteration the Amul
         # phase (56n + 16F) + r update and both sweeps (r, q, rD read, r and w
@@ -509,13 +548,17 @@ def run_ours(args):
                    "global_batch": 1, "seq_len": 0, "parallelism": "1gpu" if ws == 1 else f"domain{ws}-{args.transport}",
                    "renumber": args.renumber, "mode": args.mode, "precond": args.precond,
                    "variant": args.variant, "labels": args.labels,
+                   **({"gamg_levels": mesh.gamg_hierarchy()["n"]} if args.precond == "GAMG" else {}),
                    "l2": "flushed between timed steps (256 MiB write)", "tol": TOL,
                    "pcg_iterations_per_step": {"min": min(its), "max": max(its), "mean": sum(its) / len(its)}},
         "roofline": {"bound": "l2/barrier" if l2res else "hbm", "kernel": kernel, "achieved": achieved,
                      "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None,
-                     "bytes_model": "SURVEY §8(d): 88n+16F per PCG iteration + 24n per launch"
-                                    if kernel != "k_pcg_dic" else "DESIGN.md §5 DIC: 96n+40F per iteration + 64n+36F per launch",
+                     "bytes_model": {"k_pcg_persistent": "SURVEY §8(d): 88n+16F per PCG iteration + 24n per launch",
+                                     "k_phase1": "SURVEY §8(d) phase 1: 56n+16F per iteration",
+                                     "k_pcg_dic": "DESIGN.md §5 DIC: 96n+40F per iteration + 64n+36F per launch",
+                                     "k_pcg_gamg": "DESIGN.md §5 GAMG: 80n+16F + V-cycle per iteration "
+                                                   "+ Galerkin set-up per launch"}[kernel],
                      "traffic": traffic, "traffic_ncu_tag": traffic_tag, "dram_frac": dram_frac,
                      "bytes_per_launch": total_bytes / max(k_launches, 1),
                      "impl_bytes_per_launch": impl_bytes / max(k_launches, 1),
@@ -553,7 +596,7 @@ def run_ours(args):
 def main():
     args = parse()
     if args.renumber < 0:
-        args.renumber = 2 if args.precond != "diagonal" else 0
+        args.renumber = 2 if args.precond == "DIC" else 0
     if args.impl == "reference":
         run_reference(args)
     else:

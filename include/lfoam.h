@@ -268,8 +268,21 @@ LF_API lf_status ldu_amul(const lf_ldu *sys, const double *x_dev, double *y_dev)
  *                        says; cells may have at most 8 neighbours.
  *   LF_PRECOND_DILU      OpenFOAM DILUPreconditioner; on this symmetric matrix
  *                        (lower == upper) its recurrences are DIC's term for
- *                        term, so it runs the DIC kernels. */
-typedef enum { LF_PRECOND_DIAGONAL = 0, LF_PRECOND_DIC = 1, LF_PRECOND_DILU = 2 } lf_preconditioner;
+ *                        term, so it runs the DIC kernels.
+ *   LF_PRECOND_GAMG      algebraic multigrid (P:773 names
+ *                        AMG "a better alternative"; reading A43):
+ *                        pairwise face agglomeration of the mesh graph (built
+ *                        once per mesh on first use, weights |Sf| delta),
+ *                        Galerkin coarse matrices P^T A P formed per solve,
+ *                        one symmetric V-cycle per application (weighted
+ *                        Jacobi omega = 0.9 before and after the coarse
+ *                        correction, exact dense solve of the coarsest level
+ *                        of <= 64 cells).  Single rank: a mesh with processor
+ *                        patches is INVALID_ARG; coarsening that stalls above
+ *                        2048 cells is INVALID_ARG; cells may have at most 8
+ *                        neighbours (the level-0 rows). */
+typedef enum { LF_PRECOND_DIAGONAL = 0, LF_PRECOND_DIC = 1, LF_PRECOND_DILU = 2,
+               LF_PRECOND_GAMG = 3 } lf_preconditioner;
 
 typedef struct {
   double tolerance;   /* absolute on the normalised L1 residual (1e-10)   */
@@ -291,6 +304,21 @@ typedef struct {
  * reciprocal (DIC) diagonal, or NULL.  Stream-ordered.  Errors as pcg_solve. */
 LF_API lf_status ldu_precondition(const lf_ldu *sys, int32_t preconditioner, const double *r_dev,
                                   double *w_dev, double *rD_dev);
+
+/* GAMG hierarchy of a mesh (LF_PRECOND_GAMG; builds it if needed), for
+ * tests and inspection: *n_levels = L + 1; cells[l], faces[l] for l <= L
+ * (arrays of >= 31 entries); agg: the level l -> l+1 maps concatenated
+ * (sum of cells[l] for l < L entries), internal numbering.  Any pointer may
+ * be NULL.  INVALID_ARG where GAMG cannot run (see LF_PRECOND_GAMG). */
+LF_API lf_status lf_gamg_hierarchy(lf_mesh *mesh, int32_t *n_levels, int32_t *cells, int32_t *faces,
+                                   int32_t *agg);
+
+/* Host copies of the Galerkin matrix of GAMG level 1 <= level <= L as the
+ * last GAMG solve or ldu_precondition formed it: D[cells], U[faces] with the
+ * faces' lower / upper cells (face_l < face_u, faces sorted).  Any pointer
+ * may be NULL.  STATE before the first GAMG use. */
+LF_API lf_status lf_gamg_export(const lf_ldu *sys, int32_t level, double *D, double *U, int32_t *face_l,
+                                int32_t *face_u);
 
 /* OpenFOAM PCG, preconditioner from c:
  * psi_dev (device [n_cells], internal numbering) is the initial guess and
@@ -321,7 +349,8 @@ typedef enum {
   LF_K_NONORTH = 8,  /* gradient / non-orthogonal correction kernels (lf_fvc_grad, corrected) */
   LF_K_PCG_DIC = 9,  /* persistent whole-solve kernel with the DIC preconditioner */
   LF_K_PRECOND = 10, /* standalone preconditioner kernels (ldu_precondition, DIC set-up) */
-  LF_K_COUNT = 11
+  LF_K_PCG_GAMG = 11,/* persistent whole-solve kernel with the GAMG preconditioner */
+  LF_K_COUNT = 12
 } lf_kernel_kind;
 
 /* Execution options of a context:
@@ -339,13 +368,15 @@ typedef enum {
  *                      thread, else variant 2 runs), 2 the HBM-bound one (psi
  *                      update deferred into the Amul phase); mesh_create picks
  *                      1 when an iteration's working set fits ~1.5x the L2
- *   LF_OPT_COMPRESSED_LABELS (default 1; read by mesh_create) ELL meshes also
+ *   LF_OPT_COMPRESSED_LABELS (default 0; read by mesh_create) ELL meshes also
  *                      store their gather labels as 16-bit codes relative to a
  *                      per-32-cell offset (4 B instead of 8 B per face slot,
  *                      escapes to the int32 labels where a code does not fit);
  *                      the persistent diagonal solve gathers through them.
  *                      0 = int32 labels only.  Decoded labels are identical,
- *                      so results are bitwise the same either way.
+ *                      so results are bitwise the same either way.  Measured
+ *                      slower (200^3: 53.8 vs 40.5 ms/step: the decode adds
+ *                      dependent integer work to every gather), hence off.
  * Results are identical up to reduction grid size (all are deterministic). */
 typedef enum { LF_OPT_PERSISTENT = 0, LF_OPT_GRAPHS = 1, LF_OPT_SOLVE_VARIANT = 2,
                LF_OPT_COMPRESSED_LABELS = 3 } lf_option;

@@ -457,8 +457,30 @@ lf_status ldu_precondition(const lf_ldu *sys, int32_t precond, const double *r, 
     LF_REQUIRE(sys && M && r && w, "NULL argument");
     LF_REQUIRE(r != w && r != rD && w != rD, "r, w and rD must not alias");
     LF_REQUIRE(sys->assembled, "ldu not assembled");
-    LF_REQUIRE(precond >= LF_PRECOND_DIAGONAL && precond <= LF_PRECOND_DILU, "unknown preconditioner");
-    precondition(M, precond, r, w, rD);
+    LF_REQUIRE(precond >= LF_PRECOND_DIAGONAL && precond <= LF_PRECOND_GAMG, "unknown preconditioner");
+    if (precond == LF_PRECOND_GAMG)
+      gamg_precondition(M, r, w, rD);
+    else
+      precondition(M, precond, r, w, rD);
+  }, M);
+}
+
+// ------------------------------------------------------------------ GAMG
+lf_status lf_gamg_hierarchy(lf_mesh *M, int32_t *n_levels, int32_t *cells, int32_t *faces, int32_t *agg) {
+  return guard([&] {
+    LF_REQUIRE(M != nullptr, "mesh is NULL");
+    gamg_hierarchy(M, n_levels, cells, faces, agg);
+  }, M);
+}
+
+lf_status lf_gamg_export(const lf_ldu *sys, int32_t level, double *D, double *U, int32_t *face_l,
+                         int32_t *face_u) {
+  lf_mesh *M = sys ? sys->mesh : nullptr;
+  return guard([&] {
+    LF_REQUIRE(sys && M, "NULL ldu");
+    if (!M->gamgBuilt) throw Error{LF_ERR_STATE, "no GAMG solve or application yet"};
+    LF_CUDA(cudaStreamSynchronize(M->ctx->stream));
+    gamg_export(M, level, D, U, face_l, face_u);
   }, M);
 }
 

@@ -39,7 +39,7 @@ struct lf_context {
   bool useGraphs = true;   // replay iteration chunks as CUDA graphs
   bool persistent = true;  // single-rank, no processor patches: one cooperative launch per solve
   int solveVariant = 0;    // LF_OPT_SOLVE_VARIANT: 0 by mesh size, 1 L2-resident, 2 HBM-bound
-  bool compressedLabels = true;  // LF_OPT_COMPRESSED_LABELS (mesh_create)
+  bool compressedLabels = false;  // LF_OPT_COMPRESSED_LABELS (mesh_create; r4d: slower, off)
   struct Pending {
     int kind;
     cudaEvent_t a, b;
@@ -127,6 +127,13 @@ struct lf_mesh {
   lf::DicDev dic{};
   int dicGrid = 0;            // co-resident grid of k_pcg_dic
   std::vector<int32_t> hLvlStart;  // host copy of the level starts
+  // GAMG preconditioner (reading A43): agglomeration
+  // hierarchy built on first use (gamg.cpp); hGamg holds the device pointers
+  bool gamgBuilt = false;
+  lf::GamgDev hGamg{};
+  lf::GamgDev *dGamg = nullptr;  // device copy (kernel argument)
+  int gamgGrid = 0;              // co-resident grid of k_pcg_gamg
+  std::vector<std::array<int32_t, 2>> gamgLevels;  // {cells, faces} per level
   ~lf_mesh();
 };
 
@@ -153,6 +160,12 @@ void ensure_dic(lf_mesh *M);  // build the DIC levels / rows (once), fill symU i
 void build_rows(lf_mesh *M);  // the same without the DIC transport check (mesh_create, K > 4)
 void require_dic(const lf_mesh *M);  // INVALID_ARG where the DIC kernels cannot run
 void precondition(lf_mesh *M, int precond, const double *r, double *w, double *rD);
+// gamg.cpp
+void require_gamg(const lf_mesh *M);  // INVALID_ARG where the GAMG kernels cannot run
+void ensure_gamg(lf_mesh *M);         // build the hierarchy (once) and the level-0 rows
+void gamg_precondition(lf_mesh *M, const double *r, double *w, double *rD);
+void gamg_export(lf_mesh *M, int32_t level, double *D, double *U, int32_t *fl, int32_t *fu);
+void gamg_hierarchy(lf_mesh *M, int32_t *n_levels, int32_t *cells, int32_t *faces, int32_t *agg);
 // mesh.cpp: resident grid with equal grid-stride trips per block
 int balanced_grid(int64_t n, int g0);
 }  // namespace lf

@@ -988,15 +988,21 @@ static size_t stash_fit(int n, int grid, size_t per) {
 // term, halo puts and peer allreduce are compiled out of the hot loop
 // (they cost 13% at 100^3 even when branched around, r1o).
 #ifndef LF_W88
-#define LF_W88 1   // HBM-bound variant: w not stored (SURVEY's 88n + 16F iteration): phase 1
-#endif             // recomputes w = (1/diag) r at the cell and its neighbours
+#define LF_W88 0   // 1: HBM-bound variant does not store w (SURVEY's 88n + 16F iteration): phase 1
+#endif             // recomputes w = (1/diag) r at the cell and its neighbours.  Measured (r4d,
+                   // 200^3): 53.8 vs 40.5 ms/step — 7 FP64 divisions per cell cost more than 8n bytes.
+                   // 2: the same with rD = 1/diag stored once per solve (ws.rDiag): neighbours
+                   // form w = rD r (no division), the own cell (1/diag) r (one), phase 2 reads rD
+                   // instead of diag: 80n + 16F per iteration
 #ifndef LF_PSI2
 #define LF_PSI2 1  // HBM-bound variant: psi written every second iteration (two deferred
 #endif             // updates applied in sequence: bitwise the one-at-a-time psi), -4n/iteration
+                   // (r4d, 200^3: 40.13 vs 40.52 ms/step)
 template <int KE, bool HALO, bool IDLE = false, bool E16 = false>
 __global__ void __launch_bounds__(BS, LF_MINB_P)
     k_pcg_persistent(MeshDev m, LduDev a, Workspace ws, unsigned *bar) {
-  constexpr bool w88 = LF_W88 && !IDLE, psi2 = LF_PSI2 && !IDLE;
+  constexpr int w88 = IDLE ? 0 : LF_W88;
+  constexpr bool psi2 = LF_PSI2 && !IDLE;
   PcgCtl *ctl = ws.ctl;
   if (!HALO) ws.p2p.P = 0;
   if (ctl->stop) return;
@@ -1022,8 +1028,10 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
   const double *__restrict__ rr = ws.r;
   // w at cell j: stored (w[j]) or, in the 88n variant, recomputed exactly as
   // phase 2 / the setup formed it: (1/diag_j) r_j
+  const double *__restrict__ rDg = ws.rDiag;
   auto wv = [&](int j) -> double {
-    if constexpr (w88) return (1.0 / a.diag[j]) * rr[j];
+    if constexpr (w88 == 2) return rDg[j] * rr[j];
+    else if constexpr (w88 == 1) return (1.0 / a.diag[j]) * rr[j];
     else return w[j];
   };
   double psiSum = 0.0;  // LF_IDLE_FLUSH: this thread's sum of psi after its last flush
@@ -1068,6 +1076,11 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
   do {               \
   } while (0)
 #endif
+  if constexpr (w88 == 2) {
+    // rD = 1/diag once per solve (the value phase 2 / the setup divide by)
+    for (int c = cstart; c < cend; c += cstep) ws.rDiag[c] = 1.0 / a.diag[c];
+    grid_barrier(bar);
+  }
   for (;;) {
     // ---- derive (OpenFOAM loop condition) from the previous totals
     if (threadIdx.x == 0) {
@@ -1177,14 +1190,14 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
           const bool ok = c >= 0;
           q[u] = ok ? ws.q[c] : 0.0;
           r[u] = ok ? ws.r[c] : 0.0;
-          d[u] = ok ? a.diag[c] : 1.0;
+          d[u] = ok ? (w88 == 2 ? rDg[c] : a.diag[c]) : 1.0;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int c = cs[u];
           if (c >= 0) {
             const double rn = fma(-alpha2, q[u], r[u]);
-            const double wc = (1.0 / d[u]) * rn;
+            const double wc = (w88 == 2 ? d[u] : 1.0 / d[u]) * rn;
             ws.r[c] = rn;
             if (!w88) ws.w[c] = wc;
             if (HALO && ws.p2p.P > 0) push_halo<HALO_W>(m, ws.p2p, c, wc);
@@ -1652,6 +1665,9 @@ void sort_pairs_i32(cudaStream_t s, int32_t *keys, int32_t *vals, int64_t m, int
 
 // ----------------------------------------------------- DIC preconditioner
 #include "dic.cuh"
+
+// ---------------------------------------------------- GAMG preconditioner
+#include "gamg.cuh"
 
 // ------------------------------------------------------------- occupancy
 int occupancy_grid(int kernel_id, int device) {

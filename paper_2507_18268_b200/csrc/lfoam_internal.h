@@ -65,6 +65,7 @@ struct PcgCtl {
   double wArA, alpha;
   int32_t it, stop, converged, singular;
   int32_t precond;      // lf_preconditioner of the current solve (host side)
+  int32_t fault;        // set by a kernel: the GAMG coarsest matrix is not SPD
 };
 
 // Global sums consumed by the next launch (after the allreduce in multi-GPU).
@@ -131,6 +132,35 @@ struct DicDev {
   double *rD, *rDu;        // reciprocal DIC diagonal; unreciprocated (levels >= 1)
 };
 
+// GAMG preconditioner (reading A43 in DESIGN.md;
+// gamg.cpp builds the hierarchy once per mesh, gamg.cuh runs it).  Level 0
+// is the mesh: its rows are the full-row ELL (DicDev.symN / LduDev.symU),
+// D = LduDev.diag, U = LduDev.upper; only rD is stored here.  Levels >= 1
+// hold CSR rows (neighbours ascending, entry -> face of the level).
+constexpr int GAMG_MAXL = 30;
+struct GamgLevelDev {
+  int32_t n, nf;
+  const int32_t *rowStart, *rowCol, *rowFace;  // levels >= 1: [n+1], [2nf], [2nf]
+  const int32_t *faceL, *faceU;                // coarsest level only: [nf]
+  double *D, *rD, *U;                          // [n], [n], [nf] (level 0: D, U alias the system)
+  double *b, *x;                               // V-cycle right-hand side / correction (levels >= 1)
+  // restriction to level l+1 (l < L): cell -> coarse cell; coarse cell ->
+  // members (ascending) and internal faces (ascending); coarse face -> fine
+  // faces (ascending)
+  const int32_t *agg;
+  const int32_t *memStart, *mem;
+  const int32_t *inStart, *inFace;
+  const int32_t *cfStart, *cfFace;
+};
+struct GamgDev {
+  int32_t L;     // index of the coarsest level (levels 0..L)
+  int32_t tail;  // levels >= tail (>= 1) run in one block (no grid barriers)
+  double *inv;   // [nL*nL] inverse of the coarsest matrix (row major)
+  double *chol;  // [nL*nL] its Cholesky factor (scratch)
+  double *ycol;  // [nL*nL] forward-substitution scratch, column k at k*nL
+  GamgLevelDev lv[GAMG_MAXL + 1];
+};
+
 // ---------------------------------------------------------------- kernels
 struct Launch {
   int grid, block;
@@ -160,6 +190,7 @@ struct P2PDev {
 
 struct Workspace {
   double *r, *w, *q, *p[2];
+  double *rDiag;        // 1/diag of the current solve (LF_W88 == 2 variant only)
   double *partials;     // [4 * maxGrid]
   unsigned *tickets;    // [16]
   PcgCtl *ctl;
@@ -232,6 +263,14 @@ void launch_dic_sweep_level(cudaStream_t s, const Launch &L, const MeshDev &m, c
                             const DicDev &d, int l, bool forward, const double *r, double *w);
 void launch_diag_precondition(cudaStream_t s, const Launch &L, int32_t n, const double *diag,
                               const double *r, double *w);
+// GAMG (gamg.cuh): co-resident grid; the persistent GAMG-PCG solve; one
+// application w = M^-1 r (Galerkin set-up + V-cycle) as a cooperative launch.
+// g: device copy of the hierarchy, hg: the same on the host.
+int gamg_grid(int device, int KS);
+void launch_pcg_gamg(cudaStream_t s, int grid, const MeshDev &m, const LduDev &a, const DicDev &d,
+                     const GamgDev *g, const GamgDev &hg, const Workspace &ws, unsigned *bar);
+void launch_gamg_apply(cudaStream_t s, int grid, const LduDev &a, const DicDev &d, const GamgDev *g,
+                       const GamgDev &hg, const double *r, double *w, const Workspace &ws, unsigned *bar);
 void launch_pack_x(cudaStream_t s, int32_t nsend, const int32_t *cells, const double *x,
                    double *buf);
 void launch_set_ctl(cudaStream_t s, PcgCtl *ctl, const PcgCtl &value);  // *ctl = value, stream-ordered

@@ -567,6 +567,9 @@ static void build_mesh(lf_context *ctx, const lf_mesh_desc *d, lf_mesh *M) {
   ws.r = A.alloc<double>(n);
   ws.w = A.alloc<double>(n);
   ws.q = A.alloc<double>(n);
+#if defined(LF_W88) && LF_W88 == 2
+  ws.rDiag = A.alloc<double>(n);
+#endif
   ws.p[0] = A.alloc<double>(n);
   ws.p[1] = A.alloc<double>(n);
   ws.partials = A.alloc<double>(4 * (size_t)maxGrid);

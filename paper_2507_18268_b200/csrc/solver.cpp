@@ -48,9 +48,12 @@ void upload_controls(lf_mesh *M, const lf_solver_controls *c, double *psi) {
   LF_REQUIRE(c != nullptr, "controls is NULL");
   LF_REQUIRE(c->tolerance >= 0.0 && c->rel_tol >= 0.0, "tolerances must be >= 0");
   LF_REQUIRE(c->max_iter >= 0 && c->min_iter >= 0, "max_iter/min_iter must be >= 0");
-  LF_REQUIRE(c->preconditioner >= LF_PRECOND_DIAGONAL && c->preconditioner <= LF_PRECOND_DILU,
+  LF_REQUIRE(c->preconditioner >= LF_PRECOND_DIAGONAL && c->preconditioner <= LF_PRECOND_GAMG,
              "unknown preconditioner");
-  if (c->preconditioner != LF_PRECOND_DIAGONAL) require_dic(M);
+  if (c->preconditioner == LF_PRECOND_GAMG)
+    require_gamg(M);
+  else if (c->preconditioner != LF_PRECOND_DIAGONAL)
+    require_dic(M);
   PcgCtl *h = M->hctl;
   std::memset(h, 0, sizeof(PcgCtl));
   h->tol = c->tolerance;
@@ -162,7 +165,17 @@ static void run_iterations(lf_mesh *M, lf_solver_perf *out) {
   // persistent variant: L2-resident (idle psi flush) or HBM-bound (TMA)
   // (the L2-resident variant needs few enough trips per thread for its stash)
   M->ws.idleFlush = M->stashOK && (ctx->solveVariant == 0 ? M->l2Resident : ctx->solveVariant == 1) ? 1 : 0;
-  if (M->hctl->precond != LF_PRECOND_DIAGONAL) {
+  if (M->hctl->precond == LF_PRECOND_GAMG) {
+    // GAMG: one persistent launch (Galerkin set-up, V-cycles; single rank)
+    ctx->launch(LF_K_PCG_GAMG, [&] {
+      launch_pcg_gamg(s, M->gamgGrid, M->md, M->ld, M->dic, M->dGamg, M->hGamg, M->ws, M->gridBar);
+    });
+    LF_CUDA(cudaMemcpyAsync(M->hctl, M->ws.ctl, sizeof(PcgCtl), cudaMemcpyDeviceToHost, s));
+    LF_CUDA(cudaStreamSynchronize(s));
+    ctx->harvest();
+    if (M->hctl->fault) throw Error{LF_ERR_INVALID_ARG, "GAMG: the coarsest matrix is not positive definite"};
+    chunk = 0;
+  } else if (M->hctl->precond != LF_PRECOND_DIAGONAL) {
     // DIC (DILU = DIC on this symmetric matrix): one persistent launch with
     // the level-scheduled sweeps (single rank, checked in upload_controls)
     ctx->launch(LF_K_PCG_DIC, [&] { launch_pcg_dic(s, M->dicGrid, M->md, M->ld, M->dic, M->ws, M->gridBar); });
@@ -238,7 +251,10 @@ void solve_loop(lf_mesh *M, const lf_solver_controls *c, double *psi, bool fromA
   cudaStream_t s = ctx->stream;
   const Workspace &ws = M->ws;
   const bool psiIsT = (psi == M->T);
-  if (M->hctl->precond != LF_PRECOND_DIAGONAL) ensure_dic(M);  // before the assembly writes the rows
+  if (M->hctl->precond == LF_PRECOND_GAMG)
+    ensure_gamg(M);  // hierarchy + level-0 rows, before the assembly writes the rows
+  else if (M->hctl->precond != LF_PRECOND_DIAGONAL)
+    ensure_dic(M);  // before the assembly writes the rows
   // sum(psi) for normFactor; with the peer-memory transport the same launch
   // puts psi at the processor-face cells into the neighbours' recvT
   if (!(psiIsT && M->sumPsiValid) || M->p2pConnected) sum_psi(M, psi);

@@ -24,9 +24,10 @@ STATUS = {0: "LF_OK", 1: "LF_ERR_INVALID_ARG", 2: "LF_ERR_STATE", 3: "LF_ERR_OOM
 PATCH_TYPES = {"fixedValue": 0, "zeroGradient": 1, "processor": 2}
 FIELD_T, FIELD_PATCH_VALUE, FIELD_DT = 0, 1, 2
 KERNELS = {"assemble": 0, "setup": 1, "phase1": 2, "phase2": 3, "amul": 4, "sumpsi": 5, "pack": 6, "pcg": 7,
-           "nonorth": 8, "pcg_dic": 9, "precond": 10}
+           "nonorth": 8, "pcg_dic": 9, "precond": 10, "pcg_gamg": 11}
 # lf_preconditioner (OpenFOAM fvSolution names)
-PRECONDITIONERS = {"diagonal": 0, "DIC": 1, "DILU": 2}
+PRECONDITIONERS = {"diagonal": 0, "DIC": 1, "DILU": 2, "GAMG": 3}
+GAMG_MAXL = 30
 # lf_mesh_desc.renumber
 RENUMBER = {False: 0, True: 1, 0: 0, 1: 1, 2: 2, "none": 0, "rcm": 1, "colour": 2}
 OPTIONS = {"persistent": 0, "graphs": 1, "variant": 2, "compressed_labels": 3}
@@ -105,6 +106,8 @@ SIGNATURES = {
     "lf_p2p_init": (C.c_int, [_vp, C.c_int, C.c_int]),
     "lf_p2p_export": (C.c_int, [_vp, _vp]),
     "lf_p2p_connect": (C.c_int, [_vp, C.c_int, C.c_int, _vp]),
+    "lf_gamg_hierarchy": (C.c_int, [_vp, C.POINTER(_i32), _vp, _vp, _vp]),
+    "lf_gamg_export": (C.c_int, [_vp, _i32, _vp, _vp, _vp, _vp]),
 }
 P2P_HANDLE_BYTES = 1024
 
@@ -297,6 +300,22 @@ class Mesh:
         _check(lib().lf_mesh_layout(self.h, C.byref(k), C.byref(ks), C.byref(esc)))
         return dict(ell_width=k.value, row_width=ks.value, label_escapes=esc.value)
 
+    def gamg_hierarchy(self):
+        """GAMG levels of the mesh (lf_gamg_hierarchy): dict(n=[cells per
+        level], nf=[faces per level], agg=[level l -> l+1 maps])."""
+        nl = C.c_int32()
+        cells = np.zeros(GAMG_MAXL + 1, np.int32)
+        faces = np.zeros(GAMG_MAXL + 1, np.int32)
+        _check(lib().lf_gamg_hierarchy(self.h, C.byref(nl), cells.ctypes.data, faces.ctypes.data, None))
+        L = nl.value
+        agg = np.zeros(max(int(cells[:L - 1].sum()), 1), np.int32)
+        _check(lib().lf_gamg_hierarchy(self.h, C.byref(nl), None, None, agg.ctypes.data))
+        maps, off = [], 0
+        for l in range(L - 1):
+            maps.append(agg[off:off + cells[l]].copy())
+            off += int(cells[l])
+        return dict(n=[int(x) for x in cells[:L]], nf=[int(x) for x in faces[:L]], agg=maps)
+
     def p2p_export(self) -> bytes:
         buf = C.create_string_buffer(P2P_HANDLE_BYTES)
         _check(lib().lf_p2p_export(self.h, buf))
@@ -446,6 +465,16 @@ class Ldu:
         _check(lib().ldu_precondition(self.h, PRECONDITIONERS[precond], _ptr(r), _ptr(w), _ptr(rD)))
         _device_sync()
         return w
+
+    def gamg_level(self, level: int) -> Dict[str, np.ndarray]:
+        """Galerkin matrix of GAMG level `level` from the last GAMG use
+        (lf_gamg_export): dict(D, U, l, u)."""
+        h = self.mesh.gamg_hierarchy()
+        n, nf = h["n"][level], h["nf"][level]
+        D, U = np.zeros(n), np.zeros(max(nf, 1))
+        fl, fu = np.zeros(max(nf, 1), np.int32), np.zeros(max(nf, 1), np.int32)
+        _check(lib().lf_gamg_export(self.h, level, D.ctypes.data, U.ctypes.data, fl.ctypes.data, fu.ctypes.data))
+        return dict(D=D, U=U[:nf], l=fl[:nf], u=fu[:nf])
 
     def pcg_solve(self, psi, **ctl) -> Dict:
         _check_dev(psi, self.mesh.n_cells)
