@@ -478,7 +478,7 @@ lf_status lf_gamg_export(const lf_ldu *sys, int32_t level, double *D, double *U,
   lf_mesh *M = sys ? sys->mesh : nullptr;
   return guard([&] {
     LF_REQUIRE(sys && M, "NULL ldu");
-    if (!M->gamgBuilt) throw Error{LF_ERR_STATE, "no GAMG solve or application yet"};
+    if (!M->gamgFormed) throw Error{LF_ERR_STATE, "no GAMG solve or application yet"};
     LF_CUDA(cudaStreamSynchronize(M->ctx->stream));
     gamg_export(M, level, D, U, face_l, face_u);
   }, M);

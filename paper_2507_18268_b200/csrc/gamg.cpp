@@ -222,6 +222,7 @@ void ensure_gamg(lf_mesh *M) {
     v.nf = g.nf();
     M->gamgLevels.push_back({g.n, g.nf()});
     v.rD = A.alloc<double>(g.n);
+    if (L > 0) v.x = A.alloc<double>(g.n);  // pre-smoothed x, then z (in place)
     if (l >= 1) {
       const Adj adj = adjacency(g);
       std::vector<int32_t> col(adj.face.size());
@@ -233,7 +234,6 @@ void ensure_gamg(lf_mesh *M) {
       v.D = A.alloc<double>(g.n);
       v.U = A.alloc<double>(g.nf());
       v.b = A.alloc<double>(g.n);
-      v.x = A.alloc<double>(g.n);
     }
     if (l == L) {
       v.faceL = upload(A, g.l, s);
@@ -265,7 +265,7 @@ void ensure_gamg(lf_mesh *M) {
   LF_CUDA(cudaStreamSynchronize(s));  // host vectors are released on return
   M->hGamg = h;
   M->dGamg = d;
-  M->gamgGrid = std::max(1, std::min(gamg_grid(M->ctx->device, M->dic.KS),
+  M->gamgGrid = std::max(1, std::min(gamg_grid(M->ctx->device, M->md),
                                      (n + kernel_block_size() - 1) / kernel_block_size()));
   if (M->gamgGrid > M->ws.maxGrid) {  // partials sized for the largest grid
     M->ws.partials = A.alloc<double>(4 * (size_t)M->gamgGrid);
@@ -280,15 +280,16 @@ void gamg_precondition(lf_mesh *M, const double *r, double *w, double *rD) {
   lf_context *ctx = M->ctx;
   cudaStream_t s = ctx->stream;
   ctx->launch(LF_K_PRECOND, [&] {
-    launch_gamg_apply(s, M->gamgGrid, M->ld, M->dic, M->dGamg, M->hGamg, r, w, M->ws, M->gridBar);
+    launch_gamg_apply(s, M->gamgGrid, M->md, M->ld, M->dGamg, r, w, M->ws, M->gridBar);
   });
+  M->gamgFormed = true;
   if (rD) LF_CUDA(cudaMemcpyAsync(rD, M->hGamg.lv[0].rD, sizeof(double) * M->n, cudaMemcpyDeviceToDevice, s));
 }
 
 // host copies of level `level`'s coarse matrix (after a GAMG solve or
 // application) and of the hierarchy
 void gamg_export(lf_mesh *M, int32_t level, double *D, double *U, int32_t *fl, int32_t *fu) {
-  LF_REQUIRE(M->gamgBuilt, "no GAMG hierarchy yet (run a GAMG solve or ldu_precondition first)");
+  LF_REQUIRE(M->gamgFormed, "no GAMG solve or application yet");
   const GamgDev &h = M->hGamg;
   LF_REQUIRE(level >= 1 && level <= h.L, "GAMG level out of range");
   cudaStream_t s = M->ctx->stream;

@@ -31,24 +31,90 @@
 // oracle's (tests/test_gpu_gamg.py).
 
 constexpr double GAMG_OMEGA = 0.9;  // reading A43
+#ifndef LF_GAMG_TIMING
+#define LF_GAMG_TIMING 0  // 1: block 0 prints the pass boundaries of iteration 5 (debug builds)
+#endif
+#if LF_GAMG_TIMING
+__device__ unsigned long long g_gt[128];
+__device__ int g_gtn, g_gton;
+#define GT()                                                                       \
+  do {                                                                             \
+    if (blockIdx.x == 0 && threadIdx.x == 0 && g_gton && g_gtn < 128) g_gt[g_gtn++] = gtime_ns(); \
+  } while (0)
+#else
+#define GT() \
+  do {       \
+  } while (0)
+#endif
+#ifndef LF_GAMG_QREC
+#define LF_GAMG_QREC 1  // phase 1 forms q = A p by the recurrence A w + beta q_old (see LF_QREC)
+#endif
 
-// level-0 row: y += sum over the full row (ascending neighbour label) of U x_j
-template <int KS, class XF>
-__device__ __forceinline__ double gamg_row0(const DicDev &d, const LduDev &a, int c, double y, XF xf) {
+// level-0 row: y += U x_j over the cell's neighbours in ascending label with
+// explicit _rn operations.  RW > 0: the half-ELL slices (lower neighbours in
+// the loE slots — ascending owner — then upper neighbours in the nbrE slots;
+// the lower side's coefficient is re-read from its owner's slot); RW < 0:
+// the full-row ELL (DIC rows, -RW slots, already ascending).
+template <int RW, class XF>
+__device__ __forceinline__ double gamg_row0(const MeshDev &m, const LduDev &a, int c, double y, XF xf) {
+  if constexpr (RW < 0) {
+    constexpr int KS = -RW;
+    int lab[KS];
+    double u[KS], x[KS];
 #pragma unroll
-  for (int k = 0; k < KS; ++k) {
-    const int lab = __ldg(d.symN + k * d.ldS + c);
-    if (lab >= 0) y = __dadd_rn(y, __dmul_rn(__ldg(a.symU + k * d.ldS + c), xf(sym_cell(lab))));
+    for (int k = 0; k < KS; ++k) {
+      lab[k] = __ldg(m.symN + k * m.ldS + c);
+      u[k] = __ldg(a.symU + k * m.ldS + c);
+    }
+#pragma unroll
+    for (int k = 0; k < KS; ++k) x[k] = lab[k] >= 0 ? xf(sym_cell(lab[k])) : 0.0;
+#pragma unroll
+    for (int k = 0; k < KS; ++k)
+      if (lab[k] >= 0) y = __dadd_rn(y, __dmul_rn(u[k], x[k]));
+    return y;
+  } else {
+    const int n = m.ldE;
+    int lo[RW], nb[RW];
+    double uo[RW], lu[RW], lx[RW], ox[RW];
+#pragma unroll
+    for (int k = 0; k < RW; ++k) {
+      lo[k] = __ldg(m.loE + k * n + c);
+      nb[k] = __ldg(m.nbrE + k * n + c);
+      uo[k] = a.upperE[k * n + c];
+    }
+#pragma unroll
+    for (int k = 0; k < RW; ++k) {
+      const int oc = lo[k] & ELL_MASK;
+      lu[k] = lo[k] >= 0 ? a.upperE[(lo[k] >> ELL_SHIFT) * n + oc] : 0.0;
+      lx[k] = lo[k] >= 0 ? xf(oc) : 0.0;
+      ox[k] = nb[k] >= 0 ? xf(nb[k]) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < RW; ++k)
+      if (lo[k] >= 0) y = __dadd_rn(y, __dmul_rn(lu[k], lx[k]));
+#pragma unroll
+    for (int k = 0; k < RW; ++k)
+      if (nb[k] >= 0) y = __dadd_rn(y, __dmul_rn(uo[k], ox[k]));
+    return y;
   }
-  return y;
 }
 
-// coarse-level row (CSR, ascending neighbour label)
+// coarse-level row (CSR, ascending neighbour label): the products of a
+// chunk of 8 entries are formed with their loads in flight together, then
+// added in order (the sum stays the sequential one)
 template <class XF>
 __device__ __forceinline__ double gamg_rowc(const GamgLevelDev &L, int c, double y, XF xf) {
+  constexpr int B = 8;
   const int e1 = __ldg(L.rowStart + c + 1);
-  for (int e = __ldg(L.rowStart + c); e < e1; ++e)
-    y = __dadd_rn(y, __dmul_rn(L.U[__ldg(L.rowFace + e)], xf(__ldg(L.rowCol + e))));
+  for (int e0 = __ldg(L.rowStart + c); e0 < e1; e0 += B) {
+    double pr[B];
+#pragma unroll
+    for (int k = 0; k < B; ++k)
+      pr[k] = e0 + k < e1 ? __dmul_rn(L.U[__ldg(L.rowFace + e0 + k)], xf(__ldg(L.rowCol + e0 + k))) : 0.0;
+#pragma unroll
+    for (int k = 0; k < B; ++k)
+      if (e0 + k < e1) y = __dadd_rn(y, pr[k]);
+  }
   return y;
 }
 
@@ -147,14 +213,22 @@ __device__ void gamg_galerkin(const GamgLevelDev *lv, int L, const GamgDev *g, c
 }
 
 // ------------------------------------------------------------- V-cycle
-// w = M^-1 r.  reduce: ends in the reducing barrier publishing sum w.r to
-// *out (NV = 1), else in a plain grid barrier.
-template <int KS>
-__device__ void gamg_vcycle(const GamgLevelDev *lv, int L, int tail, const double *inv, const DicDev &d,
+// w = M^-1 r.  On entry lv[0].x holds x_0 = omega rD_0 r (phase 2 of the
+// solve writes it with r; gamg_prep otherwise).  Every pass gathers ONE
+// stored value per neighbour:
+//   down pass l (per coarse cell I): b_{l+1}[I] = sum over members c of
+//     b_c - (A_l x_l)_c, and x_{l+1}[I] = omega rD b_{l+1}[I] (stored);
+//   coarsest / up pass l (per cell c): the post-smoothed x_l[c] is added
+//     to x_{l-1} of c's members in place: lv[l-1].x becomes
+//     z_{l-1} = x_{l-1} + P x_l (each member has one aggregate: no race);
+//   up pass 0: w = z_0 + omega rD_0 (r - A z_0).
+// reduce: ends in the reducing barrier publishing sum w.r to *out (NV = 1),
+// else in a plain grid barrier.
+template <int RW>
+__device__ void gamg_vcycle(const GamgLevelDev *lv, int L, int tail, const double *inv, const MeshDev &m,
                             const LduDev &a, const double *__restrict__ r, double *__restrict__ w, unsigned *bar,
                             double *partials, double *out, bool reduce) {
   const double *rD0 = lv[0].rD;
-  auto x0 = [&](int j) { return __dmul_rn(GAMG_OMEGA, __dmul_rn(rD0[j], r[j])); };
   double v[1] = {0.0};
   if (L == 0) {  // one level: the coarsest solve is the whole preconditioner
     if (blockIdx.x == 0) {
@@ -170,47 +244,61 @@ __device__ void gamg_vcycle(const GamgLevelDev *lv, int L, int tail, const doubl
     // down pass of level l (restriction to l+1) by the grid or by block 0
     auto down = [&](int l, bool blk) {
       const GamgLevelDev &F = lv[l], &C = lv[l + 1];
-      if (l == 0) {
-        gamg_range(C.n, blk, [&](int I) {
-          double acc = 0.0;
-          const int m1 = __ldg(F.memStart + I + 1);
-          for (int e = __ldg(F.memStart + I); e < m1; ++e) {
-            const int c = __ldg(F.mem + e);
-            const double y = gamg_row0<KS>(d, a, c, __dmul_rn(a.diag[c], x0(c)), x0);
-            acc = __dadd_rn(acc, __dsub_rn(r[c], y));
+      const double *__restrict__ xf = F.x;
+      auto xg = [&](int j) { return xf[j]; };
+      gamg_range(C.n, blk, [&](int I) {
+        double acc = 0.0;
+        const int m1 = __ldg(F.memStart + I + 1);
+        if (l == 0) {
+          // two members per step: their rows' loads are in flight together
+          for (int e = __ldg(F.memStart + I); e < m1; e += 2) {
+            const int c0 = __ldg(F.mem + e), c1 = e + 1 < m1 ? __ldg(F.mem + e + 1) : -1;
+            const double y0 = gamg_row0<RW>(m, a, c0, __dmul_rn(a.diag[c0], xf[c0]), xg);
+            const double b0 = r[c0];
+            double y1 = 0.0, b1 = 0.0;
+            if (c1 >= 0) {
+              y1 = gamg_row0<RW>(m, a, c1, __dmul_rn(a.diag[c1], xf[c1]), xg);
+              b1 = r[c1];
+            }
+            acc = __dadd_rn(acc, __dsub_rn(b0, y0));
+            if (c1 >= 0) acc = __dadd_rn(acc, __dsub_rn(b1, y1));
           }
-          C.b[I] = acc;
-        });
-      } else {
-        auto xl = [&](int j) { return __dmul_rn(GAMG_OMEGA, __dmul_rn(F.rD[j], F.b[j])); };
-        gamg_range(C.n, blk, [&](int I) {
-          double acc = 0.0;
-          const int m1 = __ldg(F.memStart + I + 1);
+        } else {
           for (int e = __ldg(F.memStart + I); e < m1; ++e) {
             const int c = __ldg(F.mem + e);
-            const double y = gamg_rowc(F, c, __dmul_rn(F.D[c], xl(c)), xl);
+            const double y = gamg_rowc(F, c, __dmul_rn(F.D[c], xf[c]), xg);
             acc = __dadd_rn(acc, __dsub_rn(F.b[c], y));
           }
-          C.b[I] = acc;
-        });
+        }
+        C.b[I] = acc;
+        C.x[I] = __dmul_rn(GAMG_OMEGA, __dmul_rn(C.rD[I], acc));
+      });
+    };
+    // z_{l-1} += x_l[c] on the members of cell c of level l
+    auto prolong = [&](int l, int c, double xc) {
+      const GamgLevelDev &P = lv[l - 1];
+      const int m1 = __ldg(P.memStart + c + 1);
+      for (int e = __ldg(P.memStart + c); e < m1; ++e) {
+        const int mm = __ldg(P.mem + e);
+        P.x[mm] = __dadd_rn(P.x[mm], xc);
       }
     };
-    // up pass of level l >= 1: x_l = z + omega rD (b - A z), z = x_l + P x_{l+1}
+    // up pass of level l >= 1: x_l = z + omega rD (b - A z), prolonged
     auto up = [&](int l, bool blk) {
-      const GamgLevelDev &F = lv[l], &C = lv[l + 1];
-      auto z = [&](int j) {
-        return __dadd_rn(__dmul_rn(GAMG_OMEGA, __dmul_rn(F.rD[j], F.b[j])), C.x[__ldg(F.agg + j)]);
-      };
+      const GamgLevelDev &F = lv[l];
+      const double *__restrict__ zf = F.x;
+      auto zg = [&](int j) { return zf[j]; };
       gamg_range(F.n, blk, [&](int c) {
-        const double zc = z(c);
-        const double y = gamg_rowc(F, c, __dmul_rn(F.D[c], zc), z);
-        F.x[c] = __dadd_rn(zc, __dmul_rn(GAMG_OMEGA, __dmul_rn(F.rD[c], __dsub_rn(F.b[c], y))));
+        const double zc = zf[c];
+        const double y = gamg_rowc(F, c, __dmul_rn(F.D[c], zc), zg);
+        prolong(l, c, __dadd_rn(zc, __dmul_rn(GAMG_OMEGA, __dmul_rn(F.rD[c], __dsub_rn(F.b[c], y)))));
       });
     };
     const int t = tail < 1 ? 1 : (tail > L ? L : tail);  // first level run by block 0
     for (int l = 0; l < t; ++l) {
       down(l, false);
       grid_barrier(bar);
+      GT();
     }
     if (blockIdx.x == 0) {
       for (int l = t; l < L; ++l) {
@@ -222,7 +310,7 @@ __device__ void gamg_vcycle(const GamgLevelDev *lv, int L, int tail, const doubl
       for (int c = threadIdx.x; c < n; c += blockDim.x) {
         double s = 0.0;
         for (int k = 0; k < n; ++k) s = __dadd_rn(s, __dmul_rn(inv[c * n + k], Z.b[k]));
-        Z.x[c] = s;
+        prolong(L, c, s);
       }
       __syncthreads();
       for (int l = L - 1; l >= t; --l) {
@@ -231,19 +319,21 @@ __device__ void gamg_vcycle(const GamgLevelDev *lv, int L, int tail, const doubl
       }
     }
     grid_barrier(bar);
+    GT();
     for (int l = t - 1; l >= 1; --l) {
       up(l, false);
       grid_barrier(bar);
+      GT();
     }
-    // level 0: w = z + omega rD0 (r - A z), z = x0 + x_1[agg]
-    const GamgLevelDev &F = lv[0], &C = lv[1];
-    auto z = [&](int j) { return __dadd_rn(x0(j), C.x[__ldg(F.agg + j)]); };
-    gamg_range(F.n, false, [&](int c) {
-      const double zc = z(c);
-      const double y = gamg_row0<KS>(d, a, c, __dmul_rn(a.diag[c], zc), z);
-      const double wc = __dadd_rn(zc, __dmul_rn(GAMG_OMEGA, __dmul_rn(rD0[c], __dsub_rn(r[c], y))));
+    // level 0: w = z_0 + omega rD0 (r - A z_0)
+    const double *__restrict__ z0 = lv[0].x;
+    auto zg = [&](int j) { return z0[j]; };
+    gamg_range(lv[0].n, false, [&](int c) {
+      const double zc = z0[c], rc = r[c];
+      const double y = gamg_row0<RW>(m, a, c, __dmul_rn(a.diag[c], zc), zg);
+      const double wc = __dadd_rn(zc, __dmul_rn(GAMG_OMEGA, __dmul_rn(rD0[c], __dsub_rn(rc, y))));
       w[c] = wc;
-      v[0] = fma(wc, r[c], v[0]);
+      v[0] = fma(wc, rc, v[0]);
     });
   }
   if (reduce) {
@@ -252,6 +342,15 @@ __device__ void gamg_vcycle(const GamgLevelDev *lv, int L, int tail, const doubl
   } else {
     grid_barrier(bar);
   }
+}
+
+// x_0 = omega rD_0 r for every cell (before a V-cycle whose r was not
+// formed by the solve's phase 2); ends in a grid barrier
+__device__ __forceinline__ void gamg_prep(const GamgLevelDev *lv, const double *__restrict__ r, unsigned *bar) {
+  const double *rD0 = lv[0].rD;
+  double *x0 = lv[0].x;
+  gamg_range(lv[0].n, false, [&](int c) { x0[c] = __dmul_rn(GAMG_OMEGA, __dmul_rn(rD0[c], r[c])); });
+  grid_barrier(bar);
 }
 
 // level table -> shared memory (read at every pass)
@@ -273,9 +372,9 @@ __device__ __forceinline__ void gamg_load_levels(const GamgDev *g, GamgLevelDev 
 //              full rows, sum p.q, sum psi) | r -= alpha q, sum|r| | stop test
 //              | w = M^-1 r, sum w.r
 // Single rank (no processor interfaces on the coarse levels, A43).
-template <int KS>
+template <int RW>
 __global__ void __launch_bounds__(BS, LF_MINB_P)
-    k_pcg_gamg(MeshDev m, LduDev a, DicDev d, const GamgDev *g, Workspace ws, unsigned *bar) {
+    k_pcg_gamg(MeshDev m, LduDev a, const GamgDev *g, Workspace ws, unsigned *bar) {
   PcgCtl *ctl = ws.ctl;
   if (ctl->stop) return;
   __shared__ GamgLevelDev lv[GAMG_MAXL + 1];
@@ -300,7 +399,8 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
   __syncthreads();
   if (st.cont) {
     gamg_galerkin(lv, L, g, a, bar, ctl);
-    gamg_vcycle<KS>(lv, L, tail, g->inv, d, a, r, w, bar, ws.partials, &ws.gsum->p2[1], true);
+    if (L > 0) gamg_prep(lv, r, bar);
+    gamg_vcycle<RW>(lv, L, tail, g->inv, m, a, r, w, bar, ws.partials, &ws.gsum->p2[1], true);
   }
   P2PDev none{};
   for (;;) {
@@ -321,10 +421,40 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
     const double *pold = (k & 1) ? ws.p[0] : ws.p[1];
     double *pnew = (k & 1) ? ws.p[1] : ws.p[0];
     double v1[2] = {0.0, 0.0};
+#if LF_GAMG_QREC
+    // deferred psi update; p = w + beta p_old; q = A p by the recurrence
+    // q_k = A w_k + beta q_{k-1} (one gather per neighbour: w)
+    auto wg = [&](int j) { return w[j]; };
     grid_range(0, m.n, [&](int c) {
-      dic_amul_cell<KS, false>(m, a, d, ws, k, c, first, cont, alpha, beta, psi, w, pold, pnew, q, v1, false);
+      double ps = psi[c];
+      if (!first) {
+        ps = fma(alpha, pold[c], ps);
+        psi[c] = ps;
+      }
+      v1[1] += ps;
+      if (cont) {
+        const double wc = w[c];
+        const double pc = first ? wc : fma(beta, pold[c], wc);
+        pnew[c] = pc;
+        const double qo = first ? 0.0 : q[c];
+        double qc = row_offdiag<RW>(m, a, c, a.diag[c] * wc, wg);
+        if (!first) qc = fma(beta, qo, qc);
+        q[c] = qc;
+        v1[0] = fma(pc, qc, v1[0]);
+      }
     });
+#else
+#error "LF_GAMG_QREC = 0 is not supported with the half-ELL rows"
+#endif
+#if LF_GAMG_TIMING
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      g_gton = (k == 5);
+      if (k == 5) g_gtn = 0;
+    }
+#endif
+    GT();
     grid_reduce_sync<2, false>(v1, ws.partials, bar, ws.gsum->p1, none LF_DBG_ARG(0));
+    GT();
     if (!cont) break;
     if (threadIdx.x == 0) {
       const double pq = __ldcg(&ws.gsum->p1[0]);
@@ -335,20 +465,56 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
     if (st.singular) break;
     const double alphaK = st.alpha;
     double v2[1] = {0.0};
-    grid_range(0, m.n, [&](int c) {
-      const double rn = fma(-alphaK, q[c], r[c]);
-      r[c] = rn;
-      v2[0] += fabs(rn);
-    });
+    const double *__restrict__ rD0 = lv[0].rD;
+    double *__restrict__ x0 = lv[0].x;
+    {
+      // a pure stream: two consecutive cells per thread and trip (16-byte accesses)
+      auto cell2 = [&](int c) {
+        const double2 q2 = *reinterpret_cast<const double2 *>(q + c), r2 = *reinterpret_cast<const double2 *>(r + c);
+        double2 rn;
+        rn.x = fma(-alphaK, q2.x, r2.x);
+        rn.y = fma(-alphaK, q2.y, r2.y);
+        *reinterpret_cast<double2 *>(r + c) = rn;
+        if (L > 0) {
+          const double2 d2 = *reinterpret_cast<const double2 *>(rD0 + c);
+          double2 xv;
+          xv.x = __dmul_rn(GAMG_OMEGA, __dmul_rn(d2.x, rn.x));  // the V-cycle's x_0
+          xv.y = __dmul_rn(GAMG_OMEGA, __dmul_rn(d2.y, rn.y));
+          *reinterpret_cast<double2 *>(x0 + c) = xv;
+        }
+        v2[0] += fabs(rn.x);
+        v2[0] += fabs(rn.y);
+      };
+      const int npair = m.n >> 1, S = gridDim.x * blockDim.x;
+      for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < npair; i += S) cell2(2 * i);
+      if ((m.n & 1) && blockIdx.x == gridDim.x - 1 && threadIdx.x == blockDim.x - 1) {
+        const int c = m.n - 1;
+        const double rn = fma(-alphaK, q[c], r[c]);
+        r[c] = rn;
+        if (L > 0) x0[c] = __dmul_rn(GAMG_OMEGA, __dmul_rn(rD0[c], rn));
+        v2[0] += fabs(rn);
+      }
+    }
+    GT();
     grid_reduce_sync<1, false>(v2, ws.partials, bar, &ws.gsum->p2[0], none LF_DBG_ARG(0));
+    GT();
     if (threadIdx.x == 0) {
       ++st.k;
       st.finRes = __ldcg(&ws.gsum->p2[0]) / st.nf;
       st.cont = (st.k < ctl->maxIter && !conv(st.finRes, st.initRes, ctl)) || st.k < ctl->minIter;
     }
     __syncthreads();
-    if (st.cont) gamg_vcycle<KS>(lv, L, tail, g->inv, d, a, r, w, bar, ws.partials, &ws.gsum->p2[1], true);
+    if (st.cont) gamg_vcycle<RW>(lv, L, tail, g->inv, m, a, r, w, bar, ws.partials, &ws.gsum->p2[1], true);
+    GT();
   }
+#if LF_GAMG_TIMING
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    printf("LF_GAMG_TIMING iteration 5, %d marks (us from the phase-1 end):", g_gtn);
+    for (int i = 1; i < g_gtn; ++i) printf(" %.1f", (g_gt[i] - g_gt[0]) * 1e-3);
+    printf("\n");
+    g_gton = 0;
+  }
+#endif
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     ctl->it = st.k;
     ctl->stop = 1;
@@ -363,27 +529,49 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
 }
 
 // One application (ldu_precondition): Galerkin set-up + V-cycle.
-template <int KS>
+template <int RW>
 __global__ void __launch_bounds__(BS, LF_MINB_P)
-    k_gamg_apply(LduDev a, DicDev d, const GamgDev *g, const double *r, double *w, PcgCtl *ctl, double *partials,
-                 unsigned *bar) {
+    k_gamg_apply(MeshDev m, LduDev a, const GamgDev *g, const double *r, double *w, PcgCtl *ctl,
+                 double *partials, unsigned *bar) {
   __shared__ GamgLevelDev lv[GAMG_MAXL + 1];
   int L, tail;
   gamg_load_levels(g, lv, L, tail);
   gamg_galerkin(lv, L, g, a, bar, ctl);
-  gamg_vcycle<KS>(lv, L, tail, g->inv, d, a, r, w, bar, partials, nullptr, false);
+  if (L > 0) gamg_prep(lv, r, bar);
+  gamg_vcycle<RW>(lv, L, tail, g->inv, m, a, r, w, bar, partials, nullptr, false);
 }
 
-template <int KS>
-static const void *gamg_solve_fn() {
-  return (const void *)k_pcg_gamg<KS>;
+// level-0 row layout of a mesh: the half-ELL slices when it has them, else
+// the full rows (built by ensure_gamg)
+static int gamg_rw(const MeshDev &m) {
+  if (!LF_NO_ELL && m.K > 0 && m.K <= 3) return 3;
+  if (!LF_NO_ELL && m.K == 4) return 4;
+  return m.KS <= 6 ? -6 : -8;
 }
 
-int gamg_grid(int device, int KS) {
+static const void *gamg_solve_fn(int rw) {
+  switch (rw) {
+    case 3: return (const void *)k_pcg_gamg<3>;
+    case 4: return (const void *)k_pcg_gamg<4>;
+    case -6: return (const void *)k_pcg_gamg<-6>;
+    default: return (const void *)k_pcg_gamg<-8>;
+  }
+}
+
+static const void *gamg_apply_fn(int rw) {
+  switch (rw) {
+    case 3: return (const void *)k_gamg_apply<3>;
+    case 4: return (const void *)k_gamg_apply<4>;
+    case -6: return (const void *)k_gamg_apply<-6>;
+    default: return (const void *)k_gamg_apply<-8>;
+  }
+}
+
+int gamg_grid(int device, const MeshDev &m) {
   int sms = 0, best = 1 << 30;
   LF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-  for (const void *fn : {KS <= 6 ? (const void *)k_pcg_gamg<6> : (const void *)k_pcg_gamg<8>,
-                         KS <= 6 ? (const void *)k_gamg_apply<6> : (const void *)k_gamg_apply<8>}) {
+  const int rw = gamg_rw(m);
+  for (const void *fn : {gamg_solve_fn(rw), gamg_apply_fn(rw)}) {
     int nb = 0;
     LF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, BS, 0));
     best = std::min(best, nb);
@@ -391,21 +579,17 @@ int gamg_grid(int device, int KS) {
   return sms * (best < 1 ? 1 : best);
 }
 
-void launch_pcg_gamg(cudaStream_t s, int grid, const MeshDev &m, const LduDev &a, const DicDev &d,
-                     const GamgDev *g, const GamgDev &hg, const Workspace &ws, unsigned *bar) {
-  (void)hg;
-  void *args[] = {(void *)&m, (void *)&a, (void *)&d, (void *)&g, (void *)&ws, (void *)&bar};
-  const void *fn = d.KS <= 6 ? (const void *)k_pcg_gamg<6> : (const void *)k_pcg_gamg<8>;
-  LF_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(BS), args, 0, s));
+void launch_pcg_gamg(cudaStream_t s, int grid, const MeshDev &m, const LduDev &a, const GamgDev *g,
+                     const Workspace &ws, unsigned *bar) {
+  void *args[] = {(void *)&m, (void *)&a, (void *)&g, (void *)&ws, (void *)&bar};
+  LF_CUDA(cudaLaunchCooperativeKernel(gamg_solve_fn(gamg_rw(m)), dim3(grid), dim3(BS), args, 0, s));
 }
 
-void launch_gamg_apply(cudaStream_t s, int grid, const LduDev &a, const DicDev &d, const GamgDev *g,
-                       const GamgDev &hg, const double *r, double *w, const Workspace &ws, unsigned *bar) {
-  (void)hg;
+void launch_gamg_apply(cudaStream_t s, int grid, const MeshDev &m, const LduDev &a, const GamgDev *g,
+                       const double *r, double *w, const Workspace &ws, unsigned *bar) {
   PcgCtl *ctl = ws.ctl;
   double *partials = ws.partials;
-  void *args[] = {(void *)&a, (void *)&d, (void *)&g, (void *)&r, (void *)&w, (void *)&ctl, (void *)&partials,
+  void *args[] = {(void *)&m, (void *)&a, (void *)&g, (void *)&r, (void *)&w, (void *)&ctl, (void *)&partials,
                   (void *)&bar};
-  const void *fn = d.KS <= 6 ? (const void *)k_gamg_apply<6> : (const void *)k_gamg_apply<8>;
-  LF_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(BS), args, 0, s));
+  LF_CUDA(cudaLaunchCooperativeKernel(gamg_apply_fn(gamg_rw(m)), dim3(grid), dim3(BS), args, 0, s));
 }

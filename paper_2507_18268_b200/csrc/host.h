@@ -130,6 +130,7 @@ struct lf_mesh {
   // GAMG preconditioner (reading A43): agglomeration
   // hierarchy built on first use (gamg.cpp); hGamg holds the device pointers
   bool gamgBuilt = false;
+  bool gamgFormed = false;       // a GAMG solve / application formed the coarse matrices
   lf::GamgDev hGamg{};
   lf::GamgDev *dGamg = nullptr;  // device copy (kernel argument)
   int gamgGrid = 0;              // co-resident grid of k_pcg_gamg

@@ -994,6 +994,47 @@ static size_t stash_fit(int n, int grid, size_t per) {
                    // 2: the same with rD = 1/diag stored once per solve (ws.rDiag): neighbours
                    // form w = rD r (no division), the own cell (1/diag) r (one), phase 2 reads rD
                    // instead of diag: 80n + 16F per iteration
+#ifndef LF_CPASYNC
+#define LF_CPASYNC 0  // HBM-bound variant: phase 1 streams each thread's own-cell operands of the
+#endif                // NEXT trip into shared memory with cp.async while the current trip gathers
+constexpr int CPA_D = 9, CPA_I = 6;  // per-thread slots: 9 doubles, 6 labels (SoA over the block)
+constexpr size_t CPA_BYTES = (size_t)BS * (CPA_D * sizeof(double) + CPA_I * sizeof(int));
+__device__ __forceinline__ void cpa8(void *smem, const void *g) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cpa4(void *smem, const void *g) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cpa_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// half-ELL row with the slot data already loaded (row_offdiag<KE > 0>)
+template <int KE, class XF>
+__device__ __forceinline__ double row_pre(const LduDev &a, int n, const int (&lo)[KE], const int (&nb)[KE],
+                                          const double (&uo)[KE], double acc, XF xval) {
+  double lu[KE], lx[KE], ox[KE];
+#pragma unroll
+  for (int k = 0; k < KE; ++k) {
+    const int oc = lo[k] & ELL_MASK;
+    lu[k] = lo[k] >= 0 ? a.upperE[(lo[k] >> ELL_SHIFT) * n + oc] : 0.0;
+    lx[k] = lo[k] >= 0 ? xval(oc) : 0.0;
+    ox[k] = nb[k] >= 0 ? xval(nb[k]) : 0.0;
+  }
+#pragma unroll
+  for (int k = 0; k < KE; ++k)
+    if (lo[k] >= 0) acc = fma(lu[k], lx[k], acc);
+#pragma unroll
+  for (int k = 0; k < KE; ++k)
+    if (nb[k] >= 0) acc = fma(uo[k], ox[k], acc);
+  return acc;
+}
+
+#ifndef LF_QREC
+#define LF_QREC 0  // HBM-bound variant: q = A p by the recurrence q_k = A w_k + beta q_{k-1}
+#endif             // (p_k = w_k + beta p_{k-1}): ONE gather per neighbour (w) instead of two
+                   // (w, p_old), for one more stream (q_{k-1}, 8n)
 #ifndef LF_PSI2
 #define LF_PSI2 1  // HBM-bound variant: psi written every second iteration (two deferred
 #endif             // updates applied in sequence: bitwise the one-at-a-time psi), -4n/iteration
@@ -1003,6 +1044,8 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
     k_pcg_persistent(MeshDev m, LduDev a, Workspace ws, unsigned *bar) {
   constexpr int w88 = IDLE ? 0 : LF_W88;
   constexpr bool psi2 = LF_PSI2 && !IDLE;
+  constexpr bool qrec = LF_QREC && !IDLE && !HALO && w88 == 0;
+  constexpr bool cpa = LF_CPASYNC && LF_TAIL && !IDLE && KE > 0 && !E16 && w88 == 0;
   PcgCtl *ctl = ws.ctl;
   if (!HALO) ws.p2p.P = 0;
   if (ctl->stop) return;
@@ -1121,7 +1164,78 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
     LF_TSTAMP(0);
     constexpr bool idleF = IDLE;  // psi flush in the beta-barrier wait (Workspace.idleFlush)
     if (idleF) v1[1] = psiSum;  // sum psi after the flush done in the previous barrier's wait
+    bool piped = false;  // phase 1 done by the cp.async pipeline
 #if LF_TAIL
+    if constexpr (cpa) if (cont) {
+      piped = true;
+      // cp.async pipeline: the own-cell operands of trip i+1 (labels, owner-
+      // side coefficients, w, p_old, diag, psi, p_{k-2}, q_old) land in this
+      // thread's shared-memory slots while trip i's neighbour gathers run
+      // (per-thread groups: no block synchronisation)
+      double *sD = reinterpret_cast<double *>(lf_stash);
+      int *sI = reinterpret_cast<int *>(sD + CPA_D * BS);
+      const int t = threadIdx.x, n = m.ldE;
+      auto cell_of = [&](int i) { return i < nFull ? cstart + i * cstep : (i == nFull ? tailC : -1); };
+      auto fetch = [&](int c) {
+        if (c >= 0) {
+#pragma unroll
+          for (int kk = 0; kk < KE; ++kk) {
+            cpa4(sI + kk * BS + t, m.loE + kk * n + c);
+            cpa4(sI + (KE + kk) * BS + t, m.nbrE + kk * n + c);
+            cpa8(sD + kk * BS + t, a.upperE + kk * n + c);
+          }
+          cpa8(sD + 3 * BS + t, w + c);
+          cpa8(sD + 5 * BS + t, a.diag + c);
+          if (!first) cpa8(sD + 4 * BS + t, pold + c);
+          if (psiPass) cpa8(sD + 6 * BS + t, psi + c);
+          if (even2) cpa8(sD + 7 * BS + t, pnew + c);
+          if (qrec && !first) cpa8(sD + 8 * BS + t, ws.q + c);
+        }
+        cpa_commit();
+      };
+      fetch(cell_of(0));
+      for (int i = 0; i <= nFull; ++i) {
+        const int c = cell_of(i);
+        cpa_wait_all();
+        if (c < 0) break;
+        int lo[KE], nb[KE];
+        double uo[KE];
+#pragma unroll
+        for (int kk = 0; kk < KE; ++kk) {
+          lo[kk] = sI[kk * BS + t];
+          nb[kk] = sI[(KE + kk) * BS + t];
+          uo[kk] = sD[kk * BS + t];
+        }
+        const double wc = sD[3 * BS + t], dc = sD[5 * BS + t];
+        const double po = first ? 0.0 : sD[4 * BS + t];
+        const double ps0 = psiPass ? sD[6 * BS + t] : 0.0, pn2 = even2 ? sD[7 * BS + t] : 0.0;
+        const double qo = (qrec && !first) ? sD[8 * BS + t] : 0.0;
+        fetch(cell_of(i + 1));
+        if (psiPass) {
+          double ps = ps0;
+          if (even2) ps = fma(alphaPrev, pn2, ps);
+          if (!first) {
+            ps = fma(alpha, po, ps);
+            psi[c] = ps;
+          }
+          v1[1] += ps;
+        }
+        const double pc = first ? wc : fma(beta, po, wc);
+        pnew[c] = pc;
+        double q;
+        if constexpr (qrec) {
+          q = row_pre<KE>(a, n, lo, nb, uo, dc * wc, [&](int j) { return w[j]; });
+          if (!first) q = fma(beta, qo, q);
+        } else {
+          q = row_pre<KE>(a, n, lo, nb, uo, dc * pc, pnb);
+        }
+        if (HALO) q -= row_proc_p(m, a.bBnd, ws, first, beta, k, c);
+        ws.q[c] = q;
+        v1[0] = fma(pc, q, v1[0]);
+      }
+      cpa_wait_all();
+    }
+    if (!piped)
     for (int i = 0; i <= nFull; ++i) {
       const int c = i < nFull ? cstart + i * cstep : tailC;
       if (c < 0) break;
@@ -1150,8 +1264,16 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
         const double wc = w88 ? (1.0 / dc) * rr[c] : w[c];
         const double pc = first ? wc : fma(beta, pold[c], wc);
         pnew[c] = pc;
-        double q = dc * pc;
-        q = row_offdiag<KE, decltype(pnb), E16>(m, a, c, q, pnb);
+        double q;
+        if constexpr (qrec) {
+          auto wnb = [&](int j) { return w[j]; };
+          const double qo = first ? 0.0 : ws.q[c];
+          q = row_offdiag<KE, decltype(wnb), E16>(m, a, c, dc * wc, wnb);
+          if (!first) q = fma(beta, qo, q);
+        } else {
+          q = dc * pc;
+          q = row_offdiag<KE, decltype(pnb), E16>(m, a, c, q, pnb);
+        }
         if (HALO) q -= row_proc_p(m, a.bBnd, ws, first, beta, k, c);
 #if LF_TAIL
         if (IDLE)
@@ -1356,7 +1478,9 @@ static void persistent_occupancy(int &best) {
   int nb = 0;
   for (const void *fn : {(const void *)k_pcg_persistent<KE, false, false, E16>,
                          (const void *)k_pcg_persistent<KE, true, false, E16>}) {
-    LF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, BS, 0));
+    if (LF_CPASYNC)
+      LF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CPA_BYTES));
+    LF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, BS, LF_CPASYNC ? CPA_BYTES : 0));
     best = std::min(best, nb);
   }
   // the L2-resident variants with the shared-memory stash
@@ -1408,7 +1532,7 @@ void launch_pcg_persistent(cudaStream_t s, int grid, const MeshDev &m, const Ldu
   const void *fn = halo ? (idle ? persistent_fn<true, true>(m) : persistent_fn<true>(m))
                         : (idle ? persistent_fn<false, true>(m) : persistent_fn<false>(m));
   LF_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(BS), args,
-                                      idle ? stash_fit(m.n, grid, sizeof(double2)) : 0, s));
+                                      idle ? stash_fit(m.n, grid, sizeof(double2)) : (LF_CPASYNC ? CPA_BYTES : 0), s));
 }
 
 // ------------------------------------------------------------------ Amul

@@ -265,12 +265,12 @@ void launch_diag_precondition(cudaStream_t s, const Launch &L, int32_t n, const 
                               const double *r, double *w);
 // GAMG (gamg.cuh): co-resident grid; the persistent GAMG-PCG solve; one
 // application w = M^-1 r (Galerkin set-up + V-cycle) as a cooperative launch.
-// g: device copy of the hierarchy, hg: the same on the host.
-int gamg_grid(int device, int KS);
-void launch_pcg_gamg(cudaStream_t s, int grid, const MeshDev &m, const LduDev &a, const DicDev &d,
-                     const GamgDev *g, const GamgDev &hg, const Workspace &ws, unsigned *bar);
-void launch_gamg_apply(cudaStream_t s, int grid, const LduDev &a, const DicDev &d, const GamgDev *g,
-                       const GamgDev &hg, const double *r, double *w, const Workspace &ws, unsigned *bar);
+// g: device copy of the hierarchy.
+int gamg_grid(int device, const MeshDev &m);
+void launch_pcg_gamg(cudaStream_t s, int grid, const MeshDev &m, const LduDev &a, const GamgDev *g,
+                     const Workspace &ws, unsigned *bar);
+void launch_gamg_apply(cudaStream_t s, int grid, const MeshDev &m, const LduDev &a, const GamgDev *g,
+                       const double *r, double *w, const Workspace &ws, unsigned *bar);
 void launch_pack_x(cudaStream_t s, int32_t nsend, const int32_t *cells, const double *x,
                    double *buf);
 void launch_set_ctl(cudaStream_t s, PcgCtl *ctl, const PcgCtl &value);  // *ctl = value, stream-ordered

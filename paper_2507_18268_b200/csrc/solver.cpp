@@ -168,11 +168,12 @@ static void run_iterations(lf_mesh *M, lf_solver_perf *out) {
   if (M->hctl->precond == LF_PRECOND_GAMG) {
     // GAMG: one persistent launch (Galerkin set-up, V-cycles; single rank)
     ctx->launch(LF_K_PCG_GAMG, [&] {
-      launch_pcg_gamg(s, M->gamgGrid, M->md, M->ld, M->dic, M->dGamg, M->hGamg, M->ws, M->gridBar);
+      launch_pcg_gamg(s, M->gamgGrid, M->md, M->ld, M->dGamg, M->ws, M->gridBar);
     });
     LF_CUDA(cudaMemcpyAsync(M->hctl, M->ws.ctl, sizeof(PcgCtl), cudaMemcpyDeviceToHost, s));
     LF_CUDA(cudaStreamSynchronize(s));
     ctx->harvest();
+    M->gamgFormed = true;
     if (M->hctl->fault) throw Error{LF_ERR_INVALID_ARG, "GAMG: the coarsest matrix is not positive definite"};
     chunk = 0;
   } else if (M->hctl->precond != LF_PRECOND_DIAGONAL) {
