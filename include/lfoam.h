@@ -92,6 +92,15 @@ typedef struct {
                                   names the own rank (self pairs, a loopback used by tests). */
   const double *sf;            /* host [n_faces][3] outward area vectors, or NULL; required by
                                   lf_fvc_grad / the corrected laplacian (with lf_mesh_desc.sf) */
+  const double *cf;            /* processor patches of a full-geometry mesh: host [n_faces][3]
+                                  face centres, and                                         */
+  const double *cn;            /* host [n_faces][3] centres of the coupled cells across the
+                                  interface (OpenFOAM's patchNeighbourField of C).  Both or
+                                  neither; with them the interface gets interpolation weights
+                                  w = |Sf.(C_N-Cf)| / (|Sf.(Cf-C_P)| + |Sf.(C_N-Cf)|) and
+                                  correction vectors n - delta (C_N - C_P), and the corrected
+                                  laplacian and DT fields run across processor patches
+                                  (their halos: T, the gradient, DT).  NULL elsewhere.      */
 } lf_patch_desc;
 
 typedef struct {
@@ -184,9 +193,12 @@ typedef enum {
                                 n_cells, patch = -1).  Setting it
                                 computes the face diffusivities once, on the device:
                                 gamma_f = w (DT_P - DT_N) + DT_N with the geometric
-                                weights, boundary DT[faceCell] (reading A38).
-                                Needs the full geometry and no processor patches;
-                                used by solves with lf_laplacian_params.variable_DT. */
+                                weights, boundary DT[faceCell] (reading A38),
+                                processor faces w (DT_P - DT_N) + DT_N with the coupled
+                                cell's DT (a halo exchange; collective across ranks).
+                                Needs the full geometry (and the processor patches'
+                                cf / cn); used by solves with
+                                lf_laplacian_params.variable_DT. */
   LF_FIELD_PATCH_VALUE = 1   /* boundary values of patch `patch`, n = n_faces.
                                 fixedValue: T_b (set/get).  zeroGradient: get
                                 returns T[faceCells] (correctBoundaryConditions);
@@ -205,7 +217,8 @@ typedef struct {
   int32_t corrected;   /* 0: orthogonal two-point laplacian (A4).  1: Gauss linear
                           corrected — adds the explicit non-orthogonal correction
                           +V div(DT|Sf| corrVec . interpolate(grad T)) to the source
-                          (needs full geometry; no processor patches)            */
+                          (needs full geometry; processor patches need their cf/cn
+                          and exchange the T and gradient halos — collective)    */
   int32_t n_non_orth_correctors;  /* laplacianFoam_step: extra corrector passes per
                           step (simple.correctNonOrthogonal()); each pass
                           re-evaluates the correction from the current T and solves
@@ -223,7 +236,7 @@ typedef struct lf_ldu lf_ldu;   /* owned by its mesh, reused every step */
  * source = (T0/dt)*V (+ fixedValue boundaryCoeffs), with p->corrected the
  * explicit non-orthogonal correction of T as well.  One kernel, a per-cell
  * gather (no float atomics); deterministic.  Errors: DT/dt <= 0, corrected
- * without geometry or with processor patches -> INVALID_ARG. */
+ * without geometry or with processor patches lacking cf/cn -> INVALID_ARG. */
 LF_API lf_status laplacian_assemble(lf_mesh *mesh, const lf_laplacian_params *p, lf_ldu **sys);
 
 /* fvc::grad(x) with gaussGrad + linear interpolation — the kernels the paper
@@ -233,7 +246,9 @@ LF_API lf_status laplacian_assemble(lf_mesh *mesh, const lf_laplacian_params *p,
  * (P:539-556).  x_dev: device [n_cells] (internal numbering); boundary values
  * from the mesh's patches (fixedValue T_b, zeroGradient x[faceCell]).
  * grad_dev: device [n_cells][3]; bgrad_dev: device [boundary faces][3] (patch
- * order) or NULL.  Needs full geometry and no processor patches. */
+ * order) or NULL; processor faces interpolate with the coupled cell's x
+ * (halo exchange, collective) and are not corrected (coupled patches).
+ * Needs full geometry (processor patches: their cf/cn). */
 LF_API lf_status lf_fvc_grad(lf_mesh *mesh, const double *x_dev, double *grad_dev, double *bgrad_dev);
 
 /* Host copies in the CALLER's numbering and face order; any pointer may be

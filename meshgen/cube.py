@@ -37,6 +37,7 @@ class Patch:
     global_faces: Optional[np.ndarray] = None  # processor: global face ids (ordering key)
     Sf: Optional[np.ndarray] = None  # [nf,3] outward face area vectors (full-geometry meshes)
     Cf: Optional[np.ndarray] = None  # [nf,3] face centres
+    Cn: Optional[np.ndarray] = None  # processor patches: [nf,3] centres of the coupled cells
 
     @property
     def n_faces(self) -> int:

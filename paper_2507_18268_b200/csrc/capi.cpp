@@ -270,7 +270,7 @@ lf_status field_set(lf_mesh *M, lf_field f, int32_t patch, const double *v, int6
       LF_REQUIRE(patch == -1, "patch must be -1 for LF_FIELD_DT");
       LF_REQUIRE(n == M->n, "n must equal n_cells");
       LF_REQUIRE(M->hasGeom, "a DT field needs the full geometry (interpolation weights)");
-      LF_REQUIRE(M->nproc == 0, "a DT field is not supported with processor patches");
+      LF_REQUIRE(M->nproc == 0 || M->procGeom, "a DT field across processor patches needs the patches' cf and cn");
       {
         // validated on the host either way (a device field is copied back once:
         // DT is set once per case, not per step)
@@ -296,8 +296,9 @@ lf_status field_set(lf_mesh *M, lf_field f, int32_t patch, const double *v, int6
         LF_CUDA(cudaMemcpyAsync(M->scratch, v, sizeof(double) * n, kind, s));
         launch_permute(s, M->n, M->cellPerm, M->scratch, M->DTc, false);
       }
+      vector_halo(M, M->DTc, M->n, 1);  // the coupled cells' DT (collective)
       M->ctx->launch(LF_K_NONORTH, [&] {
-        launch_face_gamma(s, M->md, M->geo, M->ownerInt, M->bCell, M->DTc, M->gammaF, M->gammaB);
+        launch_face_gamma(s, M->md, M->geo, M->ownerInt, M->bCell, M->DTc, M->ws.recvX, M->gammaF, M->gammaB);
       });
       M->mdVar = M->md;
       M->mdVar.gammaF = M->gammaF;
@@ -444,7 +445,8 @@ lf_status lf_fvc_grad(lf_mesh *M, const double *x, double *grad, double *bgrad) 
     require_corrected(M);
     lf_context *ctx = M->ctx;
     cudaStream_t s = ctx->stream;
-    ctx->launch(LF_K_NONORTH, [&] { launch_grad(s, M->Lasm, M->md, M->geo, x, M->gradS, grad); });
+    field_halo(M, x);
+    ctx->launch(LF_K_NONORTH, [&] { launch_grad(s, M->Lasm, M->md, M->geo, x, M->haloT(), M->gradS, grad); });
     if (bgrad)
       ctx->launch(LF_K_NONORTH, [&] { launch_grad_bc(s, M->md, M->geo, M->bCell, x, M->gradS, bgrad); });
   }, M);

@@ -105,7 +105,7 @@ struct lf_mesh {
   unsigned *gridBar = nullptr;  // device {count, generation}
   // peer-memory transport: one IPC-exportable block [flags | vals | recvT | recvW]
   char *p2pBlock = nullptr;
-  size_t p2pBytes = 0, offFlags = 0, offVals = 0, offRecvT = 0, offRecvW = 0;
+  size_t p2pBytes = 0, offFlags = 0, offVals = 0, offRecvT = 0, offRecvW = 0, offRecvX = 0;
   std::vector<void *> ipcOpened;  // peer blocks mapped with cudaIpcOpenMemHandle
   bool p2pConnected = false;
   int tPar = 0;  // parity of the last peer-memory T halo push (recvT double buffer)
@@ -113,6 +113,7 @@ struct lf_mesh {
   double *haloT() { return ws.recvT + (p2pConnected ? (size_t)tPar * (size_t)nproc : 0); }
   // non-orthogonal correction path (full geometry given at mesh_create)
   bool hasGeom = false;
+  bool procGeom = false;     // processor patches carry cf/cn (corrected / DT paths across ranks)
   lf::GeomDev geo{};
   double *gradS = nullptr;   // [3][n] fvc::grad(T), SoA
   double *lapSrc = nullptr;  // [n] explicit laplacian correction source
@@ -150,6 +151,7 @@ void require_corrected(const lf_mesh *M);
 const MeshDev &mesh_for(const lf_mesh *M, const lf_laplacian_params *p);
 void halo_exchange(lf_mesh *M, const double *send, double *recv);
 void field_halo(lf_mesh *M, const double *x);
+void vector_halo(lf_mesh *M, const double *x, int64_t stride, int ncomp);  // -> ws.recvX
 // p2p.cpp
 void p2p_init(lf_context *ctx, int nranks, int rank);
 void p2p_export(lf_mesh *M, void *handle);

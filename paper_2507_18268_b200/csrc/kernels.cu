@@ -436,6 +436,31 @@ __global__ void __launch_bounds__(BS, LF_MINB)
   reduce_grid<1>(v, partials, ticket, out, ws.p2p);
 }
 
+// Vector halo over the peer-memory transport (the gradient and the DT field
+// of the corrected / variable-DT paths): component k of every send slot's
+// cell into the neighbour's recvX, then an (empty) allreduce that orders the
+// stores before the neighbour's next kernel.
+__global__ void __launch_bounds__(BS, LF_MINB)
+    k_push_x(MeshDev m, const double *__restrict__ x, int64_t stride, int ncomp, double *partials,
+             unsigned *ticket, double *out, Workspace ws) {
+  const P2PDev &P = ws.p2p;
+  const int nslot = P.segBeg[P.nseg];
+  for (int sl = blockIdx.x * blockDim.x + threadIdx.x; sl < nslot; sl += gridDim.x * blockDim.x) {
+    const int cell = ws.sendCell[sl];
+    int g = 0;
+    while (g + 1 < P.nseg && sl >= P.segBeg[g + 1]) ++g;
+    for (int k = 0; k < ncomp; ++k) P.dstX[g][(size_t)k * P.xStr[g] + (sl - P.segBeg[g])] = x[k * stride + cell];
+    lf_blockPushed = 1;
+  }
+  double v[1] = {0.0};
+  reduce_grid<1>(v, partials, ticket, out, ws.p2p);
+}
+
+void launch_push_x(cudaStream_t s, const Launch &L, const MeshDev &m, const double *x, int64_t stride, int ncomp,
+                   const Workspace &ws, double *out) {
+  k_push_x<<<L.grid, BS, 0, s>>>(m, x, stride, ncomp, ws.partials, ws.tickets + T_SUM, out, ws);
+}
+
 void launch_sum(cudaStream_t s, const Launch &L, const MeshDev &m, const double *x, const Workspace &ws,
                 double *out) {
   k_sum<<<L.grid, BS, 0, s>>>(m, x, ws.partials, ws.tickets + T_SUM, out, ws);
@@ -1031,6 +1056,10 @@ __device__ __forceinline__ double row_pre(const LduDev &a, int n, const int (&lo
   return acc;
 }
 
+#ifndef LF_IDLE_PF
+#define LF_IDLE_PF 0  // HBM-bound variant: trips whose own-cell streams a block prefetches into
+#endif                // L2 (cp.async.bulk.prefetch.L2) while it waits at a grid barrier — phase 2's
+                      // first trips at the alpha barrier, the next phase 1's at the beta barrier
 #ifndef LF_QREC
 #define LF_QREC 0  // HBM-bound variant: q = A p by the recurrence q_k = A w_k + beta q_{k-1}
 #endif             // (p_k = w_k + beta p_{k-1}): ONE gather per neighbour (w) instead of two
@@ -1285,7 +1314,22 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
       }
     }
     LF_TSTAMP(1);
-    grid_reduce_sync<2, HALO>(v1, ws.partials, bar, ws.gsum->p1, ws.p2p LF_DBG_ARG(2 * k));
+    // idle-time prefetch (LF_IDLE_PF): r and diag of phase 2's first trips
+    // (phase 2 walks the trips backwards, LF_REVERSE): this block's 512-cell
+    // run of trip i starts at blockIdx.x * BS + i * cstep
+    auto pf1 = [&]() {
+      if constexpr (LF_IDLE_PF > 0 && !IDLE && LF_TAIL && LF_REVERSE) {
+        const int j = threadIdx.x;
+        if (j < 2 * LF_IDLE_PF) {
+          const int i = nFull - 1 - (j >> 1);
+          if (i >= 0) {
+            const long c0 = (long)blockIdx.x * BS + (long)i * cstep;
+            l2_prefetch((j & 1) ? (const void *)(a.diag + c0) : (const void *)(ws.r + c0), BS * sizeof(double));
+          }
+        }
+      }
+    };
+    grid_reduce_sync<2, HALO>(v1, ws.partials, bar, ws.gsum->p1, ws.p2p LF_DBG_ARG(2 * k), pf1);
     LF_TSTAMP(2);
     if (!cont) break;
     // ---- phase 2: singularity, alpha, r -= alpha q, w = r/diag, sums
@@ -1383,6 +1427,28 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
     // singularity check of the same iteration).
     psiSum = 0.0;
     auto flush = [&]() {
+      if constexpr (LF_IDLE_PF > 0 && !IDLE && LF_TAIL && KE > 0 && !E16) {
+        // the next phase 1's first trips: w, p (next p_old), diag, psi and the ELL slices
+        constexpr int NA = 4 + 3 * KE;
+        const int j = threadIdx.x;
+        if (j < NA * LF_IDLE_PF) {
+          const int i = j / NA, f = j % NA;
+          if (i < nFull) {
+            const long c0 = (long)blockIdx.x * BS + (long)i * cstep;
+            const long ld = m.ldE;
+            const void *pa;
+            unsigned bytes = BS * sizeof(double);
+            if (f == 0) pa = ws.w + c0;
+            else if (f == 1) pa = pnew + c0;
+            else if (f == 2) pa = a.diag + c0;
+            else if (f == 3) pa = psi + c0;
+            else if (f < 4 + KE) pa = a.upperE + (f - 4) * ld + c0;
+            else if (f < 4 + 2 * KE) { pa = m.loE + (f - 4 - KE) * ld + c0; bytes = BS * sizeof(int); }
+            else { pa = m.nbrE + (f - 4 - 2 * KE) * ld + c0; bytes = BS * sizeof(int); }
+            l2_prefetch(pa, bytes);
+          }
+        }
+      }
       if (!idleF) return;
 #if LF_TAIL
       for (int i = 0; i <= nFull; ++i) {

@@ -186,6 +186,11 @@ struct P2PDev {
   int32_t segBeg[LF_MAXSEG + 1];
   double *dstW[LF_MAXSEG];
   double *dstT[2][LF_MAXSEG];
+  // vector halo (the gradient, the DT field): component k of send slot s of
+  // segment g goes to dstX[g][k * xStr[g] + (s - segBeg[g])] (xStr = the
+  // destination rank's processor-face count)
+  double *dstX[LF_MAXSEG];
+  int32_t xStr[LF_MAXSEG];
 };
 
 struct Workspace {
@@ -200,6 +205,7 @@ struct Workspace {
   double *sendBuf;      // staging for NCCL / local copies
   double *recvT, *recvW;  // neighbour T (assembly; [2][n_proc] by push parity) and w (PCG) at each slot
   double *pH[2];        // p at the halo slots, recomputed locally (double-buffered like p)
+  double *recvX;        // [3][n_proc] vector halo (gradient, DT field)
   int32_t *sendCell;    // [n_proc] local cell of each send slot
   int maxGrid;
   int idleFlush;        // persistent solve: psi flush in the beta-barrier wait (see mesh.cpp)
@@ -224,18 +230,27 @@ struct GeomDev {
   const double *Sf;       // [3][F] area vectors (owner -> neighbour)
   const double *bSf;      // [3][B] boundary area vectors (outward), patch order
   const int32_t *abStart, *abFace;  // per-cell groups of ALL boundary faces
+  // processor faces (meshes whose processor patches carry cf/cn; else null):
+  // owner-side interpolation weight [B] and correction vectors [3][B]
+  // (flat boundary order; 1 / 0 on non-coupled faces)
+  const double *bW, *bCorr;
 };
 void launch_weights_corr(cudaStream_t s, int32_t F, const int32_t *owner, const int32_t *nbr,
                          const double *SfA, const double *CfA, const double *CA, const double *magSf,
                          const double *delta, double *w, double *corr, double *SfS);
 void launch_grad(cudaStream_t s, const Launch &L, const MeshDev &m, const GeomDev &g, const double *x,
-                 double *gradS, double *gradA);
+                 const double *halo, double *gradS, double *gradA);
 void launch_grad_bc(cudaStream_t s, const MeshDev &m, const GeomDev &g, const int32_t *bCell,
                     const double *x, const double *gradS, double *bgradA);
 void launch_face_gamma(cudaStream_t s, const MeshDev &m, const GeomDev &g, const int32_t *owner,
-                       const int32_t *bCell, const double *DTc, double *gammaF, double *gammaB);
+                       const int32_t *bCell, const double *DTc, const double *haloDT, double *gammaF,
+                       double *gammaB);
 void launch_lap_corr(cudaStream_t s, const Launch &L, const MeshDev &m, const GeomDev &g, double DT,
-                     const double *gradS, double *lapSrc);
+                     const double *gradS, const double *haloG, int32_t nproc, double *lapSrc);
+// vector halo through the peer-memory transport: x[k*stride + cell] of the
+// processor-face cells into the neighbours' recvX, ordered by an allreduce
+void launch_push_x(cudaStream_t s, const Launch &L, const MeshDev &m, const double *x, int64_t stride, int ncomp,
+                   const Workspace &ws, double *out);
 void launch_pcg_setup(cudaStream_t s, const Launch &L, const MeshDev &m, const LduDev &a,
                       const double *halo, const Workspace &ws);
 void launch_phase1(cudaStream_t s, const Launch &L, const MeshDev &m, const LduDev &a,

@@ -174,9 +174,16 @@ static void validate(const lf_mesh_desc *d, int rank) {
   // full geometry (non-orthogonal path): all or nothing
   if (d->sf || d->cf || d->c) {
     LF_REQUIRE(d->c && (d->n_faces == 0 || (d->sf && d->cf)), "sf, cf and c must be given together");
-    for (int32_t p = 0; p < d->n_patches; ++p)
-      LF_REQUIRE(d->patches[p].n_faces == 0 || d->patches[p].sf,
-                 "patch " + std::to_string(p) + ": sf required with full geometry");
+    for (int32_t p = 0; p < d->n_patches; ++p) {
+      const lf_patch_desc &P = d->patches[p];
+      LF_REQUIRE(P.n_faces == 0 || P.sf, "patch " + std::to_string(p) + ": sf required with full geometry");
+      LF_REQUIRE((P.cf == nullptr) == (P.cn == nullptr), "patch " + std::to_string(p) + ": cf and cn go together");
+      if (P.cf) {
+        LF_REQUIRE(P.type == LF_PATCH_PROCESSOR, "patch " + std::to_string(p) + ": cf/cn are for processor patches");
+        for (int64_t i = 0; i < 3 * (int64_t)P.n_faces; ++i)
+          LF_REQUIRE(std::isfinite(P.cf[i]) && std::isfinite(P.cn[i]), "cf/cn must be finite");
+      }
+    }
     for (int64_t i = 0; i < 3 * (int64_t)d->n_faces; ++i)
       LF_REQUIRE(std::isfinite(d->sf[i]) && std::isfinite(d->cf[i]), "sf/cf must be finite");
     for (int64_t i = 0; i < 3 * (int64_t)n; ++i) LF_REQUIRE(std::isfinite(d->c[i]), "c must be finite");
@@ -462,6 +469,45 @@ static void build_mesh(lf_context *ctx, const lf_mesh_desc *d, lf_mesh *M) {
     g.corr = corr;
     g.Sf = SfS;
     g.bSf = bSf;
+    g.bW = g.bCorr = nullptr;
+    // processor faces with cf/cn: the owner-side interpolation weight and the
+    // correction vector of the coupled face (the internal-face formulas of
+    // k_weights_corr with C_N = the coupled cell's centre), flat boundary order
+    bool anyProc = false, allGeo = true;
+    for (int32_t p = 0; p < d->n_patches; ++p)
+      if (d->patches[p].type == LF_PATCH_PROCESSOR && d->patches[p].n_faces > 0) {
+        anyProc = true;
+        allGeo = allGeo && d->patches[p].cf != nullptr;
+      }
+    if (anyProc && allGeo) {
+      std::vector<double> bw(B, 1.0), bc(3 * (size_t)B, 0.0);
+      for (int32_t p = 0, off = 0; p < d->n_patches; ++p) {
+        const lf_patch_desc &P = d->patches[p];
+        if (P.type == LF_PATCH_PROCESSOR)
+          for (int32_t i = 0; i < P.n_faces; ++i) {
+            const double *Cp = d->c + 3 * (size_t)P.face_cells[i], *Cn = P.cn + 3 * (size_t)i;
+            const double *Cf = P.cf + 3 * (size_t)i, *S = P.sf + 3 * (size_t)i;
+            double so = 0.0, sn = 0.0;
+            for (int k = 0; k < 3; ++k) {
+              so = so + S[k] * (Cf[k] - Cp[k]);
+              sn = sn + S[k] * (Cn[k] - Cf[k]);
+            }
+            so = std::fabs(so);
+            sn = std::fabs(sn);
+            const double sum = so + sn;
+            bw[off + i] = std::fabs(sum) > 1e-150 ? sn / sum : 0.5;
+            for (int k = 0; k < 3; ++k)
+              bc[(size_t)k * B + off + i] = S[k] / P.mag_sf[i] - (Cn[k] - Cp[k]) * P.delta_coeffs[i];
+          }
+        off += P.n_faces;
+      }
+      double *dW = A.alloc<double>(B), *dC = A.alloc<double>(3 * (size_t)B);
+      LF_CUDA(cudaMemcpyAsync(dW, bw.data(), sizeof(double) * B, cudaMemcpyHostToDevice, s));
+      LF_CUDA(cudaMemcpyAsync(dC, bc.data(), sizeof(double) * 3 * B, cudaMemcpyHostToDevice, s));
+      g.bW = dW;
+      g.bCorr = dC;
+      M->procGeom = true;
+    }
     g.abStart = abStart;
     g.abFace = abFace;
     M->gradS = A.alloc<double>(3 * (size_t)n);
@@ -592,11 +638,13 @@ static void build_mesh(lf_context *ctx, const lf_mesh_desc *d, lf_mesh *M) {
     M->offVals = up(2 * LF_MAXP * sizeof(unsigned));
     M->offRecvT = up(M->offVals + 2 * LF_MAXP * 4 * sizeof(double));
     M->offRecvW = up(M->offRecvT + 2 * sizeof(double) * std::max(nproc, 1));  // recvT[2][nproc]
-    M->p2pBytes = up(M->offRecvW + sizeof(double) * std::max(nproc, 1));
+    M->offRecvX = up(M->offRecvW + sizeof(double) * std::max(nproc, 1));      // recvW[nproc]
+    M->p2pBytes = up(M->offRecvX + 3 * sizeof(double) * std::max(nproc, 1));  // recvX[3][nproc]
     M->p2pBlock = A.alloc<char>(M->p2pBytes);
     LF_CUDA(cudaMemsetAsync(M->p2pBlock, 0, M->p2pBytes, s));
     ws.recvT = reinterpret_cast<double *>(M->p2pBlock + M->offRecvT);
     ws.recvW = reinterpret_cast<double *>(M->p2pBlock + M->offRecvW);
+    ws.recvX = reinterpret_cast<double *>(M->p2pBlock + M->offRecvX);
   }
   std::memset(&ws.p2p, 0, sizeof(ws.p2p));
   ws.sendCell = A.alloc<int32_t>(nproc);

@@ -70,7 +70,8 @@ __global__ void __launch_bounds__(NB) k_weights_corr(int32_t F, const int32_t *_
 // Sf * (lambda (x_P - x_N) + x_N) (P:293-299 interpolation, P:435-452 gradf
 // gathers), + boundary Sf * x_b, / V.
 __global__ void __launch_bounds__(NB) k_grad(MeshDev m, GeomDev g, const double *__restrict__ x,
-                                             double *__restrict__ gradS, double *__restrict__ gradA) {
+                                             const double *__restrict__ halo, double *__restrict__ gradS,
+                                             double *__restrict__ gradA) {
   const int32_t n = m.n, F = g.F, B = g.B;
   for (int32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
     const double xc = x[c];
@@ -91,7 +92,18 @@ __global__ void __launch_bounds__(NB) k_grad(MeshDev m, GeomDev g, const double 
     }
     for (int32_t j = g.abStart[c], e = g.abStart[c + 1]; j < e; ++j) {
       const int32_t i = g.abFace[j];
-      const double pssf = m.bType[i] == LF_PATCH_FIXED_VALUE ? m.bValue[i] : xc;
+      const int t = m.bType[i];
+      double pssf;
+      if (t == LF_PATCH_FIXED_VALUE) {
+        pssf = m.bValue[i];
+      } else if (t == LF_PATCH_PROCESSOR && g.bW) {
+        // coupled face: linear interpolation with the neighbour rank's cell
+        // value (halo), the internal-face formula with this cell as owner
+        const double xN = halo[m.bSlot[i]];
+        pssf = add(mul(g.bW[i], sub(xc, xN)), xN);
+      } else {
+        pssf = xc;
+      }
       a0 = add(a0, mul(g.bSf[i], pssf));
       a1 = add(a1, mul(g.bSf[(size_t)B + i], pssf));
       a2 = add(a2, mul(g.bSf[2 * (size_t)B + i], pssf));
@@ -161,14 +173,31 @@ __device__ __forceinline__ double face_flux(const GeomDev &g, const MeshDev &m, 
 // (surfaceIntegrate: owner +, neighbour -; non-coupled boundary faces carry
 // no correction).
 __global__ void __launch_bounds__(NB) k_lap_corr(MeshDev m, GeomDev g, double DT,
-                                                 const double *__restrict__ gradS, double *__restrict__ lapSrc) {
-  const int32_t n = m.n;
+                                                 const double *__restrict__ gradS,
+                                                 const double *__restrict__ haloG, int32_t nproc,
+                                                 double *__restrict__ lapSrc) {
+  const int32_t n = m.n, B = g.B;
   for (int32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
     double acc = 0.0;
     for (int32_t j = m.losortStart[c], e = m.losortStart[c + 1]; j < e; ++j)
       acc = sub(acc, face_flux(g, m, DT, m.losort[j], gradS, m.losortOwner[j], c));
     for (int32_t f = m.ownerStart[c], e = m.ownerStart[c + 1]; f < e; ++f)
       acc = add(acc, face_flux(g, m, DT, f, gradS, c, m.nbr[f]));
+    if (m.hasProc && g.bW) {
+      // coupled faces (outward from this cell): corrVec . (w grad_P + (1-w)
+      // grad_N) with the neighbour rank's gradient (halo)
+      for (int32_t kk = m.pcStart[c], e = m.pcStart[c + 1]; kk < e; ++kk) {
+        const int32_t i = m.pcFace[kk], sl = m.bSlot[i];
+        const double w = g.bW[i];
+        double cs = 0.0;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const double gP = gradS[(size_t)k * n + c], gN = haloG[(size_t)k * nproc + sl];
+          cs = add(cs, mul(g.bCorr[(size_t)k * B + i], add(mul(w, sub(gP, gN)), gN)));
+        }
+        acc = add(acc, mul(mul(m.gammaB ? m.gammaB[i] : DT, m.bMagSf[i]), cs));
+      }
+    }
     const double V = m.V[c];
     lapSrc[c] = -mul(V, dvd(acc, V));
   }
@@ -177,16 +206,24 @@ __global__ void __launch_bounds__(NB) k_lap_corr(MeshDev m, GeomDev g, double DT
 // Face diffusivity of a cell DT field (§8(f) row 2): linear interpolation
 // gamma_f = w (DT_P - DT_N) + DT_N (P:293-299 with the weights of P:321-334),
 // boundary faces DT[faceCell].
-__global__ void __launch_bounds__(NB) k_face_gamma(int32_t F, int32_t B, const int32_t *__restrict__ owner,
-                                                   const int32_t *__restrict__ nbr, const int32_t *__restrict__ bCell,
-                                                   const double *__restrict__ w, const double *__restrict__ DTc,
+__global__ void __launch_bounds__(NB) k_face_gamma(MeshDev m, GeomDev g, const int32_t *__restrict__ owner,
+                                                   const int32_t *__restrict__ bCell,
+                                                   const double *__restrict__ DTc,
+                                                   const double *__restrict__ haloDT,
                                                    double *__restrict__ gammaF, double *__restrict__ gammaB) {
+  const int32_t F = g.F, B = g.B;
   for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < F + B; i += gridDim.x * blockDim.x) {
     if (i < F) {
-      const double dN = DTc[nbr[i]];
-      gammaF[i] = add(mul(w[i], sub(DTc[owner[i]], dN)), dN);
+      const double dN = DTc[m.nbr[i]];
+      gammaF[i] = add(mul(g.w[i], sub(DTc[owner[i]], dN)), dN);
     } else {
-      gammaB[i - F] = DTc[bCell[i - F]];
+      const int32_t b = i - F;
+      if (g.bW && m.bType[b] == LF_PATCH_PROCESSOR) {  // the coupled cell's DT (halo)
+        const double dN = haloDT[m.bSlot[b]];
+        gammaB[b] = add(mul(g.bW[b], sub(DTc[bCell[b]], dN)), dN);
+      } else {
+        gammaB[b] = DTc[bCell[b]];
+      }
     }
   }
 }
@@ -205,8 +242,8 @@ void launch_weights_corr(cudaStream_t s, int32_t F, const int32_t *owner, const 
 }
 
 void launch_grad(cudaStream_t s, const Launch &L, const MeshDev &m, const GeomDev &g, const double *x,
-                 double *gradS, double *gradA) {
-  k_grad<<<L.grid, NB, 0, s>>>(m, g, x, gradS, gradA);
+                 const double *halo, double *gradS, double *gradA) {
+  k_grad<<<L.grid, NB, 0, s>>>(m, g, x, halo, gradS, gradA);
 }
 
 void launch_grad_bc(cudaStream_t s, const MeshDev &m, const GeomDev &g, const int32_t *bCell,
@@ -216,15 +253,15 @@ void launch_grad_bc(cudaStream_t s, const MeshDev &m, const GeomDev &g, const in
 }
 
 void launch_face_gamma(cudaStream_t s, const MeshDev &m, const GeomDev &g, const int32_t *owner,
-                       const int32_t *bCell, const double *DTc, double *gammaF, double *gammaB) {
+                       const int32_t *bCell, const double *DTc, const double *haloDT, double *gammaF,
+                       double *gammaB) {
   if (g.F + g.B <= 0) return;
-  k_face_gamma<<<grid_for((int64_t)g.F + g.B), NB, 0, s>>>(g.F, g.B, owner, m.nbr, bCell, g.w, DTc, gammaF,
-                                                             gammaB);
+  k_face_gamma<<<grid_for((int64_t)g.F + g.B), NB, 0, s>>>(m, g, owner, bCell, DTc, haloDT, gammaF, gammaB);
 }
 
 void launch_lap_corr(cudaStream_t s, const Launch &L, const MeshDev &m, const GeomDev &g, double DT,
-                     const double *gradS, double *lapSrc) {
-  k_lap_corr<<<L.grid, NB, 0, s>>>(m, g, DT, gradS, lapSrc);
+                     const double *gradS, const double *haloG, int32_t nproc, double *lapSrc) {
+  k_lap_corr<<<L.grid, NB, 0, s>>>(m, g, DT, gradS, haloG, nproc, lapSrc);
 }
 
 }  // namespace lf

@@ -1,7 +1,7 @@
 // Peer-memory transport (SURVEY.md §8(e) "Halo, option A: P2P").
 //
 // Every rank exports ONE cudaMalloc block per mesh with cudaIpcGetMemHandle:
-//   [mailbox flags | mailbox values | recvT[2] | recvW]
+//   [mailbox flags | mailbox values | recvT[2] | recvW | recvX[3]]
 // and maps every other rank's block with cudaIpcOpenMemHandle (over NVLink
 // between GPUs; the same physical memory for ranks sharing a GPU).  The
 // kernels then
@@ -23,7 +23,7 @@ constexpr int kMaxSeg = 32;
 struct Handle {
   cudaIpcMemHandle_t ipc;  // 64 bytes
   int32_t magic, rank, nranks, n_cells, nproc, nseg;
-  int64_t offFlags, offVals, offRecvT, offRecvW;
+  int64_t offFlags, offVals, offRecvT, offRecvW, offRecvX;
   struct Seg {
     int32_t peer, offset, count, pad;
   } seg[kMaxSeg];
@@ -57,6 +57,7 @@ void p2p_export(lf_mesh *M, void *out) {
   h.offVals = (int64_t)M->offVals;
   h.offRecvT = (int64_t)M->offRecvT;
   h.offRecvW = (int64_t)M->offRecvW;
+  h.offRecvX = (int64_t)M->offRecvX;
   for (int g = 0; g < h.nseg; ++g) h.seg[g] = {M->segs[g].peer, M->segs[g].offset, M->segs[g].count, 0};
   std::memset(out, 0, LF_P2P_HANDLE_BYTES);
   std::memcpy(out, &h, sizeof(h));
@@ -107,13 +108,14 @@ void p2p_connect(lf_mesh *M, int nranks, int rank, const void *handles) {
                "processor segments must tile the send slots in order");
     int32_t off, rn;
     char *b;
-    int64_t oT, oW;
+    int64_t oT, oW, oX;
     if (sg.peer == rank) {
       LF_REQUIRE(sg.partner >= 0, "unpaired self processor patch");
       off = M->segs[sg.partner].offset;
       b = base[rank];
       oT = (int64_t)M->offRecvT;
       oW = (int64_t)M->offRecvW;
+      oX = (int64_t)M->offRecvX;
       rn = M->nproc;
     } else {
       const Handle &hs = H[sg.peer];
@@ -132,12 +134,15 @@ void p2p_connect(lf_mesh *M, int nranks, int rank, const void *handles) {
       b = base[sg.peer];
       oT = hs.offRecvT;
       oW = hs.offRecvW;
+      oX = hs.offRecvX;
       rn = hs.nproc;
     }
     P.segBeg[g] = sg.offset;
     P.dstW[g] = reinterpret_cast<double *>(b + oW) + off;
     P.dstT[0][g] = reinterpret_cast<double *>(b + oT) + off;
     P.dstT[1][g] = reinterpret_cast<double *>(b + oT) + rn + off;  // parity-1 half of its recvT
+    P.dstX[g] = reinterpret_cast<double *>(b + oX) + off;             // component k at + k * rn
+    P.xStr[g] = rn;
   }
   P.segBeg[P.nseg] = M->nproc;
   P.seq = M->arena.alloc<unsigned>(1);

@@ -226,16 +226,41 @@ static void sum_psi(lf_mesh *M, const double *psi) {
 
 void require_corrected(const lf_mesh *M) {
   LF_REQUIRE(M->hasGeom, "the non-orthogonal path needs the full geometry (lf_mesh_desc.sf/cf/c)");
-  LF_REQUIRE(M->nproc == 0, "the non-orthogonal path does not support processor patches");
+  LF_REQUIRE(M->nproc == 0 || M->procGeom,
+             "the non-orthogonal path across processor patches needs the patches' cf and cn");
+}
+
+// Vector halo: x[k*stride + cell] at every send slot -> ws.recvX[k*nproc +
+// slot] of the coupled rank (peer memory: pushed by a kernel; NCCL /
+// loopback: packed and exchanged component by component).
+void vector_halo(lf_mesh *M, const double *x, int64_t stride, int ncomp) {
+  if (M->nproc == 0) return;
+  lf_context *ctx = M->ctx;
+  const Workspace &ws = M->ws;
+  if (M->p2pConnected) {
+    ctx->launch(LF_K_SUMPSI,
+                [&] { launch_push_x(ctx->stream, M->Lsum, M->md, x, stride, ncomp, ws, M->scratch); });
+    return;
+  }
+  for (int k = 0; k < ncomp; ++k) {
+    ctx->launch(LF_K_PACK, [&] { launch_pack_x(ctx->stream, M->nproc, ws.sendCell, x + k * stride, ws.sendBuf); });
+    halo_exchange(M, ws.sendBuf, ws.recvX + (size_t)k * M->nproc);
+  }
 }
 
 // gradS <- fvc::grad(x); lapSrc <- explicit non-orthogonal laplacian source
-// of that gradient (two gathers, stream-ordered).
+// of that gradient (two gathers, stream-ordered).  Across processor patches:
+// the halo of x before the gradient, the halo of the gradient before the
+// correction (the coupled faces interpolate with the neighbour rank's values).
 void correction_source(lf_mesh *M, const MeshDev &md, double DT, const double *x) {
   lf_context *ctx = M->ctx;
-  ctx->launch(LF_K_NONORTH, [&] { launch_grad(ctx->stream, M->Lasm, md, M->geo, x, M->gradS, nullptr); });
+  field_halo(M, x);
   ctx->launch(LF_K_NONORTH,
-              [&] { launch_lap_corr(ctx->stream, M->Lasm, md, M->geo, DT, M->gradS, M->lapSrc); });
+              [&] { launch_grad(ctx->stream, M->Lasm, md, M->geo, x, M->haloT(), M->gradS, nullptr); });
+  vector_halo(M, M->gradS, M->n, 3);
+  ctx->launch(LF_K_NONORTH, [&] {
+    launch_lap_corr(ctx->stream, M->Lasm, md, M->geo, DT, M->gradS, M->ws.recvX, M->nproc, M->lapSrc);
+  });
 }
 
 const MeshDev &mesh_for(const lf_mesh *M, const lf_laplacian_params *p) {

@@ -50,25 +50,42 @@ def local_mesh(mesh, part: np.ndarray, rank: int):
     inner = (po == rank) & (pn == rank)
     owner = loc[mesh.owner[inner]].astype(np.int32)
     neighbour = loc[mesh.neighbour[inner]].astype(np.int32)
+    geo = mesh.Sf is not None
     patches = []
     for p in mesh.patches:
         sel = part[p.face_cells] == rank
+        extra = {}
+        if geo and p.Sf is not None:
+            extra = dict(Sf=p.Sf[sel], Cf=None if p.Cf is None else p.Cf[sel])
         patches.append(dataclasses.replace(
             p, face_cells=loc[p.face_cells[sel]].astype(np.int32), mag_sf=p.mag_sf[sel],
-            delta=p.delta[sel], value=p.value[sel]))
+            delta=p.delta[sel], value=p.value[sel], **extra))
     cut = (po == rank) ^ (pn == rank)
     fidx = np.nonzero(cut)[0]
-    other = np.where(po[fidx] == rank, pn[fidx], po[fidx])
-    mine = np.where(po[fidx] == rank, mesh.owner[fidx], mesh.neighbour[fidx])
+    mine_is_owner = po[fidx] == rank
+    other = np.where(mine_is_owner, pn[fidx], po[fidx])
+    mine = np.where(mine_is_owner, mesh.owner[fidx], mesh.neighbour[fidx])
+    theirs = np.where(mine_is_owner, mesh.neighbour[fidx], mesh.owner[fidx])
     for s in np.unique(other):
         sel = other == s
         f = fidx[sel]                                   # ascending global face id
+        extra = {}
+        if geo:
+            # outward from this rank's cell; the coupled cell's centre (Cn)
+            sgn = np.where(mine_is_owner[sel], 1.0, -1.0)[:, None]
+            extra = dict(Sf=mesh.Sf[f] * sgn, Cf=mesh.Cf[f].copy(), Cn=mesh.C[theirs[sel]].copy())
         patches.append(meshgen.Patch(f"procBoundary{rank}to{int(s)}", "processor",
                                      loc[mine[sel]].astype(np.int32), mesh.mag_sf[f], mesh.delta[f],
-                                     np.zeros(f.shape[0]), neighb_rank=int(s), global_faces=f))
+                                     np.zeros(f.shape[0]), neighb_rank=int(s), global_faces=f, **extra))
+    gkw = {}
+    if geo:
+        gkw = dict(Sf=mesh.Sf[inner], Cf=mesh.Cf[inner], C=mesh.C[cells], affine=mesh.affine,
+                   grid_lines=mesh.grid_lines)
+    if mesh.DT_field is not None:
+        gkw["DT_field"] = mesh.DT_field[cells]
     sub = meshgen.Mesh(int(cells.shape[0]), owner, neighbour, mesh.mag_sf[inner], mesh.delta[inner],
                        mesh.V[cells], patches, dims=mesh.dims, extent=mesh.extent,
-                       cell_global=mesh.block_labels()[cells].astype(np.int64))
+                       cell_global=mesh.block_labels()[cells].astype(np.int64), **gkw)
     return sub, cells
 
 
@@ -79,12 +96,17 @@ def cut_mesh(mesh, face_mask: np.ndarray, rank: int = 0):
     keep = ~face_mask
     f = np.nonzero(face_mask)[0]
     patches = list(mesh.patches)
+    ga, gb, gkw = {}, {}, {}
+    if mesh.Sf is not None:  # geometry of the coupled faces (outward Sf, Cf, coupled cell centre)
+        ga = dict(Sf=mesh.Sf[f].copy(), Cf=mesh.Cf[f].copy(), Cn=mesh.C[mesh.neighbour[f]].copy())
+        gb = dict(Sf=-mesh.Sf[f], Cf=mesh.Cf[f].copy(), Cn=mesh.C[mesh.owner[f]].copy())
+        gkw = dict(Sf=mesh.Sf[keep], Cf=mesh.Cf[keep])
     patches.append(meshgen.Patch("procSelfA", "processor", mesh.owner[f].astype(np.int32), mesh.mag_sf[f],
-                                 mesh.delta[f], np.zeros(f.shape[0]), neighb_rank=rank, global_faces=f))
+                                 mesh.delta[f], np.zeros(f.shape[0]), neighb_rank=rank, global_faces=f, **ga))
     patches.append(meshgen.Patch("procSelfB", "processor", mesh.neighbour[f].astype(np.int32), mesh.mag_sf[f],
-                                 mesh.delta[f], np.zeros(f.shape[0]), neighb_rank=rank, global_faces=f))
+                                 mesh.delta[f], np.zeros(f.shape[0]), neighb_rank=rank, global_faces=f, **gb))
     return dataclasses.replace(mesh, owner=mesh.owner[keep], neighbour=mesh.neighbour[keep],
-                               mag_sf=mesh.mag_sf[keep], delta=mesh.delta[keep], patches=patches)
+                               mag_sf=mesh.mag_sf[keep], delta=mesh.delta[keep], patches=patches, **gkw)
 
 
 def z_plane_faces(mesh, k: int) -> np.ndarray:

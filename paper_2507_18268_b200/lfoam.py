@@ -42,7 +42,7 @@ class LfoamError(RuntimeError):
 class PatchDesc(C.Structure):
     _fields_ = [("type", C.c_int), ("n_faces", C.c_int32), ("face_cells", C.c_void_p),
                 ("mag_sf", C.c_void_p), ("delta_coeffs", C.c_void_p), ("value", C.c_void_p),
-                ("neighb_rank", C.c_int32), ("sf", C.c_void_p)]
+                ("neighb_rank", C.c_int32), ("sf", C.c_void_p), ("cf", C.c_void_p), ("cn", C.c_void_p)]
 
 
 class MeshDesc(C.Structure):
@@ -201,6 +201,7 @@ class Context:
     def p2p_init(self, nranks: int, rank: int):
         """Peer-memory transport (CUDA IPC); call before creating meshes."""
         _check(lib().lf_p2p_init(self.h, nranks, rank))
+        self._p2p = True
 
     def comm_info(self):
         n, r = C.c_int(), C.c_int()
@@ -266,9 +267,13 @@ class Mesh:
             fc = _host(p.face_cells, np.int32); pm = _host(p.mag_sf, np.float64)
             pd = _host(p.delta, np.float64); pv = _host(p.value, np.float64)
             psf = _vec3(getattr(p, "Sf", None)) if geometry else None
-            keep += [fc, pm, pd, pv, psf]
+            # processor patches of a geometry mesh: face centres and coupled cell centres
+            cpl = geometry and p.type == "processor" and getattr(p, "Cn", None) is not None
+            pcf = _vec3(p.Cf) if cpl else None
+            pcn = _vec3(p.Cn) if cpl else None
+            keep += [fc, pm, pd, pv, psf, pcf, pcn]
             pds[i] = PatchDesc(PATCH_TYPES[p.type], fc.shape[0], _ptr(fc), _ptr(pm), _ptr(pd), _ptr(pv),
-                               int(getattr(p, "neighb_rank", -1)), _ptr(psf))
+                               int(getattr(p, "neighb_rank", -1)), _ptr(psf), _ptr(pcf), _ptr(pcn))
             self.patch_sizes.append(int(fc.shape[0]))
             self.patch_types.append(p.type)
         g = [None, None, None]
@@ -286,8 +291,12 @@ class Mesh:
         self.n_bfaces = int(sum(self.patch_sizes))
         self.renumber = renumber
         self.variable_dt = False
+        self._pending_dt = None
         if getattr(m, "DT_field", None) is not None:
-            self.set_DT_field(m.DT_field)
+            if getattr(ctx, "_p2p", False) and any(p.type == "processor" for p in m.patches):
+                self._pending_dt = m.DT_field   # its halo needs the transport: set in p2p_connect
+            else:
+                self.set_DT_field(m.DT_field)
 
     def info(self):
         n, F, B, b = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int64()
@@ -326,6 +335,9 @@ class Mesh:
         blob = b"".join(bytes(h) for h in handles)
         buf = C.create_string_buffer(blob, len(blob))
         _check(lib().lf_p2p_connect(self.h, len(handles), rank, buf))
+        if self._pending_dt is not None:   # collective: every rank connects, then sets its DT
+            self.set_DT_field(self._pending_dt)
+            self._pending_dt = None
 
     def export_addressing(self):
         os_ = np.zeros(self.n_cells + 1, np.int32); lo = np.zeros(self.n_faces, np.int32)
