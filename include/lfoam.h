@@ -392,9 +392,15 @@ typedef enum {
  *                      so results are bitwise the same either way.  Measured
  *                      slower (200^3: 53.8 vs 40.5 ms/step: the decode adds
  *                      dependent integer work to every gather), hence off.
+ *   LF_OPT_OVERLAP_HALO (default 1) NCCL transport: the processor-patch halo
+ *                      of w runs on a second communicator (ncclCommSplit) and
+ *                      stream while the Amul phase of the cells WITHOUT
+ *                      processor faces runs; the cells with them follow once
+ *                      the halo has arrived (north_star: halos "overlapped with
+ *                      the interior Amul").  0 = the serial sequence.
  * Results are identical up to reduction grid size (all are deterministic). */
 typedef enum { LF_OPT_PERSISTENT = 0, LF_OPT_GRAPHS = 1, LF_OPT_SOLVE_VARIANT = 2,
-               LF_OPT_COMPRESSED_LABELS = 3 } lf_option;
+               LF_OPT_COMPRESSED_LABELS = 3, LF_OPT_OVERLAP_HALO = 4 } lf_option;
 LF_API lf_status lf_set_option(lf_context *ctx, lf_option opt, int value);
 
 /* enable != 0: bracket every launch of the hot kernels with CUDA events on

@@ -87,7 +87,12 @@ lf_context::~lf_context() {
     cudaEventDestroy(p.b);
   }
   for (auto e : evFree) cudaEventDestroy(e);
+  if (commStream) cudaStreamSynchronize(commStream);
+  if (commHalo) nccl_comm_destroy(commHalo);
   if (comm) nccl_comm_destroy(comm);
+  if (commStream) cudaStreamDestroy(commStream);
+  if (evPacked) cudaEventDestroy(evPacked);
+  if (evHalo) cudaEventDestroy(evHalo);
   if (ownStream && stream) cudaStreamDestroy(stream);
 }
 
@@ -150,6 +155,10 @@ lf_status lf_comm_init(lf_context *ctx, const void *uid, int nranks, int rank) {
     ctx->comm = nccl_comm_init(uid, nranks, rank, ctx->device);
     ctx->nranks = nranks;
     ctx->rank = rank;
+    ctx->commHalo = nccl_comm_split(ctx->comm, rank);
+    LF_CUDA(cudaStreamCreateWithFlags(&ctx->commStream, cudaStreamNonBlocking));
+    LF_CUDA(cudaEventCreateWithFlags(&ctx->evPacked, cudaEventDisableTiming));
+    LF_CUDA(cudaEventCreateWithFlags(&ctx->evHalo, cudaEventDisableTiming));
   });
 }
 
@@ -569,6 +578,8 @@ lf_status lf_set_option(lf_context *ctx, lf_option opt, int value) {
       ctx->solveVariant = value;
     } else if (opt == LF_OPT_COMPRESSED_LABELS)
       ctx->compressedLabels = value != 0;
+    else if (opt == LF_OPT_OVERLAP_HALO)
+      ctx->overlapHalo = value != 0;
     else
       throw Error{LF_ERR_INVALID_ARG, "unknown option"};
   });

@@ -22,6 +22,7 @@ struct Nccl {
   decltype(&ncclGroupEnd) groupEnd = nullptr;
   decltype(&ncclGetErrorString) errStr = nullptr;
   decltype(&ncclCommGetAsyncError) asyncErr = nullptr;
+  decltype(&ncclCommSplit) commSplit = nullptr;
 };
 
 static Nccl g_nccl;
@@ -44,6 +45,7 @@ Nccl *nccl_load() {
   LF_SYM(groupEnd, ncclGroupEnd)
   LF_SYM(errStr, ncclGetErrorString)
   LF_SYM(asyncErr, ncclCommGetAsyncError)
+  LF_SYM(commSplit, ncclCommSplit)
 #undef LF_SYM
   g_nccl.h = h;
   return &g_nccl;
@@ -71,6 +73,14 @@ void *nccl_comm_init(const void *uid128, int nranks, int rank, int device) {
   ncclComm_t comm = nullptr;
   LF_NCCL(n->commInitRank(&comm, nranks, id, rank));
   return comm;
+}
+
+// a second communicator over the same ranks (the processor-patch halos run
+// on it, on their own stream, concurrently with the reductions on the first)
+void *nccl_comm_split(void *comm, int rank) {
+  ncclComm_t out = nullptr;
+  LF_NCCL(g_nccl.commSplit(static_cast<ncclComm_t>(comm), 0, rank, &out, nullptr));
+  return out;
 }
 
 void nccl_comm_destroy(void *comm) {

@@ -16,6 +16,7 @@ Nccl *nccl_load();  // throws Error{LF_ERR_NCCL} if unavailable
 void nccl_unique_id(void *out128);
 void *nccl_comm_init(const void *uid128, int nranks, int rank, int device);
 void nccl_comm_destroy(void *comm);
+void *nccl_comm_split(void *comm, int rank);
 void nccl_allreduce_sum(void *comm, const double *send, double *recv, size_t count, cudaStream_t s);
 void nccl_group_start();
 void nccl_group_end();
@@ -30,7 +31,13 @@ struct lf_context {
   cudaStream_t stream = nullptr;
   bool ownStream = false;
   int nranks = 1, rank = 0;
-  void *comm = nullptr;  // ncclComm_t (transport NCCL)
+  void *comm = nullptr;  // ncclComm_t (transport NCCL): reductions, on `stream`
+  // NCCL halos overlapped with the interior Amul: a split communicator on its
+  // own stream; evPacked (compute -> comm) / evHalo (comm -> compute)
+  void *commHalo = nullptr;
+  cudaStream_t commStream = nullptr;
+  cudaEvent_t evPacked = nullptr, evHalo = nullptr;
+  bool overlapHalo = true;  // LF_OPT_OVERLAP_HALO
   bool p2p = false;      // transport: peer memory (lf_p2p_init)
   int smCount = 0;
   // instrumentation
@@ -101,6 +108,11 @@ struct lf_mesh {
   int persistentGrid = 0;     // co-resident grid of k_pcg_persistent
   bool l2Resident = false;    // an iteration's working set fits ~1.5x the L2 (mesh.cpp)
   bool stashOK = false;       // few enough trips per thread for the L2-resident variant
+  // NCCL transport, halo overlapped with the interior Amul: phase 1 split
+  // into the cells without processor faces (interior) and those with
+  int32_t *cellsInt = nullptr, *cellsBnd = nullptr;
+  int32_t nInt = 0, nBnd = 0;
+  bool haloPending = false;   // a w halo was started on the comm stream and not yet waited for
   int32_t ell16Escapes = -1;  // escaped compressed-label entries (-1: not built)
   unsigned *gridBar = nullptr;  // device {count, generation}
   // peer-memory transport: one IPC-exportable block [flags | vals | recvT | recvW]

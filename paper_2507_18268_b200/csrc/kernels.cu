@@ -51,7 +51,7 @@ namespace lf {
 
 constexpr int BS = LF_BS;
 constexpr unsigned FULL = 0xffffffffu;
-enum { T_SUM = 0, T_ASM = 1, T_SETUP = 2, T_P1 = 3, T_P2 = 4 };
+enum { T_SUM = 0, T_ASM = 1, T_SETUP = 2, T_P1 = 3, T_P2 = 4, T_P1I = 5 };
 constexpr int ELL_SHIFT = 29;  // slot kk <= 3 in bits 29-30: the packed label stays >= 0
 constexpr int ELL_MASK = (1 << ELL_SHIFT) - 1;
 
@@ -659,9 +659,9 @@ __device__ __forceinline__ double pval(const double *__restrict__ w, const doubl
 // ---------------------------------------------------------------- phase 1
 // Deferred psi += alpha_{k-1} p_{k-1}; stopping test on the previous
 // iteration's residual; p_k = w + beta p_{k-1}; q = A p_k; sum p.q, sum psi.
-template <int KE>
+template <int KE, int PART = 0>
 __global__ void __launch_bounds__(BS, LF_MINB_G)
-    k_phase1(MeshDev m, LduDev a, Workspace ws) {
+    k_phase1(MeshDev m, LduDev a, Workspace ws, const int32_t *__restrict__ cells = nullptr, int32_t count = 0) {
   const PcgCtl *ctl = ws.ctl;
   if (ctl->stop) return;
   const IterState s = derive_phase1(ws);
@@ -672,7 +672,9 @@ __global__ void __launch_bounds__(BS, LF_MINB_G)
   double *__restrict__ pnew = (s.k & 1) ? ws.p[1] : ws.p[0];
   const double *__restrict__ w = ws.w;
   double v[2] = {0.0, 0.0};
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < m.n; c += gridDim.x * blockDim.x) {
+  const int nIt = PART == 0 ? m.n : count;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nIt; t += gridDim.x * blockDim.x) {
+    const int c = PART == 0 ? t : cells[t];
 #if LF_PF > 0
     if (KE > 0 && s.cont && threadIdx.x < 4 + 3 * KE) {
       const int cb = c - threadIdx.x + LF_PF * gridDim.x * blockDim.x;
@@ -705,8 +707,16 @@ __global__ void __launch_bounds__(BS, LF_MINB_G)
       v[0] = fma(pc, q, v[0]);
     }
   }
+  if constexpr (PART == 1) {  // interior cells: partial sums only
+    reduce_grid<2>(v, ws.partials, ws.tickets + T_P1I, ws.lsum->p1x, ws.p2p);
+    return;
+  }
   if (reduce_grid<2>(v, ws.partials, ws.tickets + T_P1, ws.lsum->p1, ws.p2p) && threadIdx.x == 0) {
     PcgCtl *c = ws.ctl;
+    if (PART == 2) {  // + the interior cells' sums (fixed order: deterministic)
+      ws.lsum->p1[0] = v[0] + ws.lsum->p1x[0];
+      ws.lsum->p1[1] = v[1] + ws.lsum->p1x[1];
+    }
     if (first) {
       c->normFactor = s.nf;
       c->initRes = s.initRes;
@@ -723,6 +733,24 @@ __global__ void __launch_bounds__(BS, LF_MINB_G)
 void launch_phase1(cudaStream_t s, const Launch &L, const MeshDev &m, const LduDev &a,
                    const Workspace &ws) {
   LF_DISPATCH_KE(m, k_phase1, <<<L.grid, BS, 0, s>>>(m, a, ws));
+}
+
+template <int KE>
+static void phase1_part(cudaStream_t s, const Launch &L, const MeshDev &m, const LduDev &a, const Workspace &ws,
+                        int part, const int32_t *cells, int32_t count) {
+  if (part == 1)
+    k_phase1<KE, 1><<<L.grid, BS, 0, s>>>(m, a, ws, cells, count);
+  else
+    k_phase1<KE, 2><<<L.grid, BS, 0, s>>>(m, a, ws, cells, count);
+}
+
+void launch_phase1_part(cudaStream_t s, const Launch &L, const MeshDev &m, const LduDev &a, const Workspace &ws,
+                        int part, const int32_t *cells, int32_t count) {
+  if (!LF_NO_ELL && m.K > 0 && m.K <= 3) phase1_part<3>(s, L, m, a, ws, part, cells, count);
+  else if (!LF_NO_ELL && m.K == 4) phase1_part<4>(s, L, m, a, ws, part, cells, count);
+  else if (m.KS == 6) phase1_part<-6>(s, L, m, a, ws, part, cells, count);
+  else if (m.KS == 8) phase1_part<-8>(s, L, m, a, ws, part, cells, count);
+  else phase1_part<0>(s, L, m, a, ws, part, cells, count);
 }
 
 // ---------------------------------------------------------------- phase 2

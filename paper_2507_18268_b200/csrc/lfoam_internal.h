@@ -73,6 +73,7 @@ struct RedSlots {
   double setup[3];  // sum(|A psi - tmp| + |b - tmp|), sum|r|, sum w.r
   double p1[2];     // sum p.q, sum psi
   double p2[2];     // sum|r|, sum w.r
+  double p1x[2];    // phase 1 split (NCCL halo overlap): the interior cells' p.q, psi
 };
 
 // Read-only view of a mesh on the device (kernel argument, by value).
@@ -255,6 +256,11 @@ void launch_pcg_setup(cudaStream_t s, const Launch &L, const MeshDev &m, const L
                       const double *halo, const Workspace &ws);
 void launch_phase1(cudaStream_t s, const Launch &L, const MeshDev &m, const LduDev &a,
                    const Workspace &ws);
+// phase 1 over a cell list: part 1 = the cells without processor faces (sums
+// into p1x, no state commit), part 2 = the cells with them (sums + p1x into
+// p1, commits the state) — the halo-overlapped NCCL iteration
+void launch_phase1_part(cudaStream_t s, const Launch &L, const MeshDev &m, const LduDev &a, const Workspace &ws,
+                        int part, const int32_t *cells, int32_t count);
 void launch_phase2(cudaStream_t s, const Launch &L, const MeshDev &m, const LduDev &a,
                    const Workspace &ws);
 void launch_amul(cudaStream_t s, const Launch &L, const MeshDev &m, const LduDev &a,

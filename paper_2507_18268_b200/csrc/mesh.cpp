@@ -649,6 +649,22 @@ static void build_mesh(lf_context *ctx, const lf_mesh_desc *d, lf_mesh *M) {
   std::memset(&ws.p2p, 0, sizeof(ws.p2p));
   ws.sendCell = A.alloc<int32_t>(nproc);
   LF_CUDA(cudaMemcpyAsync(ws.sendCell, sendCells.data(), sizeof(int32_t) * nproc, cudaMemcpyHostToDevice, s));
+  if (nproc > 0) {
+    // cells without / with processor faces (the NCCL iteration overlaps the
+    // w halo with the first group's Amul)
+    std::vector<char> bnd(n, 0);
+    for (int32_t c : sendCells) bnd[c] = 1;
+    std::vector<int32_t> ci, cb;
+    for (int32_t c = 0; c < n; ++c) (bnd[c] ? cb : ci).push_back(c);
+    M->nInt = (int32_t)ci.size();
+    M->nBnd = (int32_t)cb.size();
+    M->cellsInt = A.alloc<int32_t>(ci.size());
+    M->cellsBnd = A.alloc<int32_t>(cb.size());
+    if (!ci.empty())
+      LF_CUDA(cudaMemcpyAsync(M->cellsInt, ci.data(), sizeof(int32_t) * ci.size(), cudaMemcpyHostToDevice, s));
+    LF_CUDA(cudaMemcpyAsync(M->cellsBnd, cb.data(), sizeof(int32_t) * cb.size(), cudaMemcpyHostToDevice, s));
+    LF_CUDA(cudaStreamSynchronize(s));  // the host vectors go out of scope
+  }
   M->T = A.alloc<double>(n);
   LF_CUDA(cudaMemsetAsync(M->T, 0, sizeof(double) * n, s));
   M->scratch = A.alloc<double>(n);

@@ -18,12 +18,17 @@ void allreduce(lf_mesh *M, const double *local, double *global, size_t count) {
   nccl_allreduce_sum(ctx->comm, local, global, count, ctx->stream);
 }
 
-// recv[seg] <- neighbour's send[seg'] for every processor patch.
+// recv[seg] <- neighbour's send[seg'] for every processor patch (on the
+// context's communicator and stream, or the given ones).
+static void halo_exchange_on(lf_mesh *M, const double *send, double *recv, void *comm, cudaStream_t s);
 void halo_exchange(lf_mesh *M, const double *send, double *recv) {
+  halo_exchange_on(M, send, recv, M->ctx->comm, M->ctx->stream);
+}
+
+static void halo_exchange_on(lf_mesh *M, const double *send, double *recv, void *comm, cudaStream_t s) {
   if (M->nproc == 0) return;
   lf_context *ctx = M->ctx;
-  cudaStream_t s = ctx->stream;
-  if (!ctx->comm) {
+  if (!comm) {
     for (const HaloSeg &g : M->segs) {
       if (g.partner < 0) throw Error{LF_ERR_STATE, "processor patch to another rank needs lf_comm_init"};
       const HaloSeg &p = M->segs[g.partner];
@@ -36,12 +41,39 @@ void halo_exchange(lf_mesh *M, const double *send, double *recv) {
   // patch each side in the same face order.  Self pairs (a,b): sends a,b;
   // recvs b,a so that recv[b] <- send[a] and recv[a] <- send[b].
   nccl_group_start();
-  for (const HaloSeg &g : M->segs) nccl_send(ctx->comm, send + g.offset, g.count, g.peer, s);
+  for (const HaloSeg &g : M->segs) nccl_send(comm, send + g.offset, g.count, g.peer, s);
   for (const HaloSeg &g : M->segs) {
     const HaloSeg &dst = g.partner >= 0 ? M->segs[g.partner] : g;
-    nccl_recv(ctx->comm, recv + dst.offset, dst.count, g.peer, s);
+    nccl_recv(comm, recv + dst.offset, dst.count, g.peer, s);
   }
   nccl_group_end();
+}
+
+// ------------------------------------- NCCL halo overlapped with the Amul
+// The w halo runs on the split communicator and the comm stream; phase 1 of
+// the cells without processor faces runs meanwhile, the rest after evHalo.
+static bool overlap_halo(const lf_mesh *M) {
+  return M->ctx->comm && M->ctx->commHalo && M->ctx->overlapHalo && M->nproc > 0 && M->cellsInt;
+}
+
+// the compute stream waits for the halo started last (if any)
+static void wait_w_halo(lf_mesh *M) {
+  if (!M->haloPending) return;
+  LF_CUDA(cudaStreamWaitEvent(M->ctx->stream, M->ctx->evHalo, 0));
+  M->haloPending = false;
+}
+
+// pack w at the send cells (compute stream), exchange on the comm stream
+static void start_w_halo(lf_mesh *M) {
+  lf_context *ctx = M->ctx;
+  const Workspace &ws = M->ws;
+  wait_w_halo(M);  // the previous exchange still reads sendBuf
+  ctx->launch(LF_K_PACK, [&] { launch_pack_x(ctx->stream, M->nproc, ws.sendCell, ws.w, ws.sendBuf); });
+  LF_CUDA(cudaEventRecord(ctx->evPacked, ctx->stream));
+  LF_CUDA(cudaStreamWaitEvent(ctx->commStream, ctx->evPacked, 0));
+  halo_exchange_on(M, ws.sendBuf, ws.recvW, ctx->commHalo, ctx->commStream);
+  LF_CUDA(cudaEventRecord(ctx->evHalo, ctx->commStream));
+  M->haloPending = true;
 }
 
 void upload_controls(lf_mesh *M, const lf_solver_controls *c, double *psi) {
@@ -102,6 +134,18 @@ static void iteration(lf_mesh *M) {
   lf_context *ctx = M->ctx;
   cudaStream_t s = ctx->stream;
   const Workspace &ws = M->ws;
+  if (overlap_halo(M)) {
+    // interior Amul while the w halo is in flight, then the cells with
+    // processor faces; the p2 allreduce overlaps the next halo
+    ctx->launch(LF_K_PHASE1, [&] { launch_phase1_part(s, M->Lp1, M->md, M->ld, ws, 1, M->cellsInt, M->nInt); });
+    wait_w_halo(M);
+    ctx->launch(LF_K_PHASE1, [&] { launch_phase1_part(s, M->Lp1, M->md, M->ld, ws, 2, M->cellsBnd, M->nBnd); });
+    allreduce(M, ws.lsum->p1, ws.gsum->p1, 2);
+    ctx->launch(LF_K_PHASE2, [&] { launch_phase2(s, M->Lp2, M->md, M->ld, ws); });
+    start_w_halo(M);
+    allreduce(M, ws.lsum->p2, ws.gsum->p2, 2);
+    return;
+  }
   ctx->launch(LF_K_PHASE1, [&] { launch_phase1(s, M->Lp1, M->md, M->ld, ws); });
   allreduce(M, ws.lsum->p1, ws.gsum->p1, 2);
   ctx->launch(LF_K_PHASE2, [&] { launch_phase2(s, M->Lp2, M->md, M->ld, ws); });
@@ -119,7 +163,10 @@ static void enqueue_iterations(lf_mesh *M, int count) {
     for (int i = 0; i < count; ++i) iteration(M);
     return;
   }
-  if (M->kernelsPerIteration == 0) M->kernelsPerIteration = host_halo(M) ? 3 : 2;
+  // graphs are self-contained: a halo started before them is waited for
+  // outside the capture, and every chunk joins its last halo
+  wait_w_halo(M);
+  if (M->kernelsPerIteration == 0) M->kernelsPerIteration = overlap_halo(M) ? 4 : host_halo(M) ? 3 : 2;
   for (int b = lf_mesh::kMaxGraphLog - 1; b >= 0 && count > 0;) {
     const int k = 1 << b;
     if (count < k) {
@@ -132,6 +179,7 @@ static void enqueue_iterations(lf_mesh *M, int count) {
       LF_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
       try {
         for (int i = 0; i < k; ++i) iteration(M);
+        wait_w_halo(M);  // join the comm stream back into the capture
       } catch (...) {
         cudaStreamEndCapture(s, &g);
         if (g) cudaGraphDestroy(g);
@@ -146,7 +194,7 @@ static void enqueue_iterations(lf_mesh *M, int count) {
     }
     LF_CUDA(cudaGraphLaunch(M->chunkGraph[b], s));
     ctx->launches += (int64_t)k * M->kernelsPerIteration;
-    ctx->kLaunches[LF_K_PHASE1] += k;
+    ctx->kLaunches[LF_K_PHASE1] += overlap_halo(M) ? 2 * k : k;
     ctx->kLaunches[LF_K_PHASE2] += k;
     if (host_halo(M)) ctx->kLaunches[LF_K_PACK] += k;
     count -= k;
@@ -205,6 +253,7 @@ static void run_iterations(lf_mesh *M, lf_solver_perf *out) {
     if (launched > bound) throw Error{LF_ERR_INTERNAL, "PCG loop did not stop within max_iter"};
     chunk = 8;
   }
+  wait_w_halo(M);  // no halo left in flight past the solve
   const PcgCtl *h = M->hctl;
   M->lastIters = h->it;
   if (out) {
@@ -293,7 +342,10 @@ void solve_loop(lf_mesh *M, const lf_solver_controls *c, double *psi, bool fromA
   } else {
     ctx->launch(LF_K_SETUP, [&] { launch_pcg_setup(s, M->Lsetup, M->md, M->ld, M->haloT(), ws); });
   }
-  if (host_halo(M)) exchange_field(M, ws.w, ws.recvW);  // w of the setup for iteration 0
+  if (overlap_halo(M))
+    start_w_halo(M);  // w of the setup for iteration 0, on the comm stream
+  else if (host_halo(M))
+    exchange_field(M, ws.w, ws.recvW);  // w of the setup for iteration 0
   allreduce(M, ws.lsum->setup, ws.gsum->setup, 3);
   run_iterations(M, out);
   // gsum->p1[1] now holds sum(psi) of the final psi (last phase-1 launch)

@@ -114,3 +114,32 @@ def test_unpaired_processor_patch_rejected(P):
         P.Mesh(ctx, c)
     assert e.value.status == 1
     ctx.close()
+
+
+@pytest.mark.parametrize("overlap,graphs", [(True, True), (True, False), (False, True)])
+def test_nccl_halo_overlap(P, overlap, graphs):
+    """NCCL transport (1-rank communicator, self pairs): the w halo on the
+    split communicator / comm stream, overlapped with the Amul phase of the
+    cells without processor faces (LF_OPT_OVERLAP_HALO), CUDA-graph chunks or
+    direct launches — against the undecomposed oracle, and the launch count
+    (two phase-1 launches per iteration when overlapped)."""
+    m, c = cut(12)
+    s = meshgen.multimode_field(m)
+    T_ref, _, p_ref = oracle.laplacian_foam(m, s, 4)
+    ctx = P.Context(0)
+    ctx.comm_init(P.Context.unique_id(), 1, 0)
+    ctx.set_option("overlap_halo", overlap)
+    ctx.set_option("graphs", graphs)
+    mesh = P.Mesh(ctx, c)
+    mesh.set_T(s)
+    ctx.set_instrumentation(not graphs)
+    pg = mesh.step(4)
+    T = mesh.get_T()
+    assert np.max(np.abs(T - T_ref)) <= 1e-8 * np.max(np.abs(T_ref))
+    assert all(abs(a["n_iterations"] - b["n_iterations"]) <= 1 for a, b in zip(pg, p_ref)), (pg, p_ref)
+    if not graphs:
+        n1, _ = ctx.kernel_stats("phase1")
+        n2, _ = ctx.kernel_stats("phase2")
+        assert (n1 >= 2 * n2) if overlap else (n1 < 2 * n2), (n1, n2)
+    mesh.close()
+    ctx.close()
