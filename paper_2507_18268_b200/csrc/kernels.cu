@@ -110,8 +110,12 @@ __device__ __forceinline__ double ld_relaxed_sys(const double *p) {
 __shared__ int lf_blockPushed;  // per block; may start as garbage (then one extra fence)
 // thread 0, after the block's bar.sync: make this block's peer stores
 // visible system-wide if it made any (and reset the note)
+#ifndef LF_PUSH_FENCE
+#define LF_PUSH_FENCE 1  // 0: no per-block system fence; the peer stores are ordered by the
+#endif                   // block's gpu-scope release at arrival and the last block's system-
+                         // scope fence + release.sys flag store in p2p_allreduce (cumulativity)
 __device__ __forceinline__ void fence_pushed() {
-  if (lf_blockPushed) {
+  if (LF_PUSH_FENCE && lf_blockPushed) {
     __threadfence_system();
     lf_blockPushed = 0;
   }
@@ -324,13 +328,17 @@ __device__ __forceinline__ double row_offdiag(const MeshDev &m, const LduDev &a,
   }
 }
 
+__device__ __forceinline__ bool has_proc(const MeshDev &m, int c) {
+  return m.hasProc && ((__ldg(m.procMask + (c >> 5)) >> (c & 31)) & 1u);
+}
+
 // Processor-interface term  sum_i bc_i * x_remote_i  (subtracted by callers);
 // sBc (optional) receives sum_i bc_i.
 __device__ __forceinline__ double row_proc(const MeshDev &m, const double *__restrict__ bBnd,
                                            const double *__restrict__ halo, int c,
                                            double *sBc = nullptr) {
   double s = 0.0, sb = 0.0;
-  if (m.hasProc) {
+  if (has_proc(m, c)) {
     const int k0 = m.pcStart[c], k1 = m.pcStart[c + 1];
     for (int k = k0; k < k1; ++k) {
       const int i = m.pcFace[k];
@@ -349,9 +357,9 @@ __device__ __forceinline__ double row_proc(const MeshDev &m, const double *__res
 // iteration (written by the thread that owns the face's cell).
 __device__ __forceinline__ double row_proc_p(const MeshDev &m, const double *__restrict__ bBnd,
                                              const Workspace &ws, bool first, double beta, int k,
-                                             int c) {
+                                             int c, int flag = -1 /* has_proc(m, c) if known */) {
   double s = 0.0;
-  if (m.hasProc) {
+  if (flag < 0 ? has_proc(m, c) : flag != 0) {
     const double *phOld = (k & 1) ? ws.pH[0] : ws.pH[1];
     double *phNew = (k & 1) ? ws.pH[1] : ws.pH[0];
     const int k0 = m.pcStart[c], k1 = m.pcStart[c + 1];
@@ -373,8 +381,8 @@ __device__ __forceinline__ double row_proc_p(const MeshDev &m, const double *__r
 // their arrival at the next reduction.
 enum { HALO_W = 0, HALO_T = 1 };
 template <int WHICH>
-__device__ __forceinline__ void push_halo(const MeshDev &m, const P2PDev &P, int c, double val) {
-  if (m.hasProc) {
+__device__ __forceinline__ void push_halo(const MeshDev &m, const P2PDev &P, int c, double val, int flag = -1) {
+  if (flag < 0 ? has_proc(m, c) : flag != 0) {
     const int k0 = m.pcStart[c], k1 = m.pcStart[c + 1];
     for (int kk = k0; kk < k1; ++kk) {
       const int sl = m.bSlot[m.pcFace[kk]];
@@ -1299,6 +1307,7 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
 #else
     for (int c = cstart; c < cend; c += cstep) {
 #endif
+      const int pflag = HALO ? (int)has_proc(m, c) : 0;  // issued with the cell's own loads
       if (idleF) {
         if (first) v1[1] += psi[c];
       } else if (psiPass) {
@@ -1331,7 +1340,7 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
           q = dc * pc;
           q = row_offdiag<KE, decltype(pnb), E16>(m, a, c, q, pnb);
         }
-        if (HALO) q -= row_proc_p(m, a.bBnd, ws, first, beta, k, c);
+        if (HALO) q -= row_proc_p(m, a.bBnd, ws, first, beta, k, c, pflag);
 #if LF_TAIL
         if (IDLE)
           lf_stash[i * BS + threadIdx.x] = make_double2(q, dc);
@@ -1378,10 +1387,12 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
       // U cells (c < 0: none): all loads first, then r, w and the sums
       auto p2cells = [&](const int (&cs)[U]) {
         double q[U], r[U], d[U];
+        int pf[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int c = cs[u];
           const bool ok = c >= 0;
+          pf[u] = (HALO && ok) ? (int)has_proc(m, c) : 0;
           q[u] = ok ? ws.q[c] : 0.0;
           r[u] = ok ? ws.r[c] : 0.0;
           d[u] = ok ? (w88 == 2 ? rDg[c] : a.diag[c]) : 1.0;
@@ -1394,7 +1405,7 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
             const double wc = (w88 == 2 ? d[u] : 1.0 / d[u]) * rn;
             ws.r[c] = rn;
             if (!w88) ws.w[c] = wc;
-            if (HALO && ws.p2p.P > 0) push_halo<HALO_W>(m, ws.p2p, c, wc);
+            if (HALO && ws.p2p.P > 0) push_halo<HALO_W>(m, ws.p2p, c, wc, pf[u]);
             v2[0] += fabs(rn);
             v2[1] = fma(wc, rn, v2[1]);
           }

@@ -89,6 +89,9 @@ struct MeshDev {
   // processor faces grouped per cell (Amul interface term); null if none
   const int32_t *pcStart, *pcFace;
   int32_t hasProc;
+  // bit c of procMask[c / 32]: cell c has processor faces (one broadcast
+  // word per warp instead of a pcStart pair per cell in the hot loops)
+  const unsigned *procMask;
   // ELL slices of the same addressing (K = max faces per side, 0 = none);
   // slot k of cell c at k*n + c.  See kernels.cu header.
   int32_t K, ldE;  // ldE: slab stride (n rounded up to 4: 16-byte aligned slabs)

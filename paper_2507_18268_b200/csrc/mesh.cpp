@@ -411,6 +411,16 @@ static void build_mesh(lf_context *ctx, const lf_mesh_desc *d, lf_mesh *M) {
   md.pcStart = pcStart;
   md.pcFace = pcFace;
   md.hasProc = nproc > 0;
+  md.procMask = nullptr;
+  if (nproc > 0) {
+    std::vector<uint32_t> mask(((size_t)n + 31) / 32, 0u);
+    for (int32_t fi = 0; fi < B; ++fi)
+      if (hType[fi] == LF_PATCH_PROCESSOR) mask[hCell[fi] >> 5] |= 1u << (hCell[fi] & 31);
+    unsigned *dm = A.alloc<unsigned>(mask.size());
+    LF_CUDA(cudaMemcpyAsync(dm, mask.data(), sizeof(uint32_t) * mask.size(), cudaMemcpyHostToDevice, s));
+    LF_CUDA(cudaStreamSynchronize(s));
+    md.procMask = dm;
+  }
 
   // -------------------------- full geometry (non-orthogonal correction path)
   // Internal face order and orientation: Sf is negated where the relabelled
