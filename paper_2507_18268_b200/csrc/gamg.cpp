@@ -231,6 +231,7 @@ void ensure_gamg(lf_mesh *M) {
       v.rowStart = upload(A, adj.start, s);
       v.rowCol = upload(A, col, s);
       v.rowFace = upload(A, adj.face, s);
+      v.rowU = A.alloc<double>(adj.face.size());
       v.D = A.alloc<double>(g.n);
       v.U = A.alloc<double>(g.nf());
       v.b = A.alloc<double>(g.n);

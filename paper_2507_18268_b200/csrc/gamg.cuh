@@ -110,7 +110,7 @@ __device__ __forceinline__ double gamg_rowc(const GamgLevelDev &L, int c, double
     double pr[B];
 #pragma unroll
     for (int k = 0; k < B; ++k)
-      pr[k] = e0 + k < e1 ? __dmul_rn(L.U[__ldg(L.rowFace + e0 + k)], xf(__ldg(L.rowCol + e0 + k))) : 0.0;
+      pr[k] = e0 + k < e1 ? __dmul_rn(L.rowU[e0 + k], xf(__ldg(L.rowCol + e0 + k))) : 0.0;
 #pragma unroll
     for (int k = 0; k < B; ++k)
       if (e0 + k < e1) y = __dadd_rn(y, pr[k]);
@@ -155,6 +155,12 @@ __device__ void gamg_galerkin(const GamgLevelDev *lv, int L, const GamgDev *g, c
       C.U[Fc] = s;
     });
     grid_barrier(bar);
+  }
+  // each coarse row entry's coefficient inline (the V-cycle rows read it
+  // contiguously instead of through the face index)
+  for (int l = 1; l <= L; ++l) {
+    const GamgLevelDev &C = lv[l];
+    gamg_range(2 * C.nf, false, [&](int e) { C.rowU[e] = C.U[__ldg(C.rowFace + e)]; });
   }
   if (blockIdx.x == 0) {
     // dense coarsest matrix, Cholesky by columns (every element's sum in the

@@ -145,6 +145,7 @@ constexpr int GAMG_MAXL = 30;
 struct GamgLevelDev {
   int32_t n, nf;
   const int32_t *rowStart, *rowCol, *rowFace;  // levels >= 1: [n+1], [2nf], [2nf]
+  double *rowU;                                // levels >= 1: [2nf] U of each row entry (per solve)
   const int32_t *faceL, *faceU;                // coarsest level only: [nf]
   double *D, *rD, *U;                          // [n], [n], [nf] (level 0: D, U alias the system)
   double *b, *x;                               // V-cycle right-hand side / correction (levels >= 1)
