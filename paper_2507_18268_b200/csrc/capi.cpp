@@ -392,6 +392,7 @@ lf_status laplacian_assemble(lf_mesh *M, const lf_laplacian_params *p, lf_ldu **
     }
     field_halo(M, M->T);
     ctx->launch(LF_K_ASSEMBLE, [&] {
+      M->upperStale = !M->ld.writeUpper;
       launch_assemble(s, M->Lasm, md, M->ld, p->DT, 1.0 / p->dt, M->T, M->haloT(), false, M->ws, nullptr,
                       lapSrc);
     });
@@ -421,6 +422,7 @@ lf_status lf_ldu_export(const lf_ldu *sys, double *diag, double *upper, double *
     if (upper && M->F > 0) {
       std::vector<double> tmp(M->F);
       std::vector<int32_t> perm(M->F);
+      ensure_upper(M);
       LF_CUDA(cudaMemcpyAsync(tmp.data(), M->ld.upper, sizeof(double) * M->F, cudaMemcpyDeviceToHost, s));
       LF_CUDA(cudaMemcpyAsync(perm.data(), M->facePerm, sizeof(int32_t) * M->F, cudaMemcpyDeviceToHost, s));
       LF_CUDA(cudaStreamSynchronize(s));

@@ -158,6 +158,8 @@ void require_gamg(const lf_mesh *M) {
 void ensure_gamg(lf_mesh *M) {
   require_gamg(M);
   build_rows(M);  // level-0 rows: the full-row ELL (neighbours ascending) + symU
+  M->ld.writeUpper = 1;  // the Galerkin set-up reads the face-order upper
+  ensure_upper(M);
   if (M->gamgBuilt) return;
   cudaStream_t s = M->ctx->stream;
   const int32_t n = M->n, F = M->F;

@@ -101,6 +101,7 @@ struct lf_mesh {
   int32_t lastIters = -1;
   bool broken = false;
   lf_ldu ldu;
+  bool upperStale = false;    // the last assembly wrote upperE only (LduDev.writeUpper == 0)
   // CUDA graphs of 2^i PCG iterations (captured once per mesh, replayed)
   static constexpr int kMaxGraphLog = 8;
   cudaGraphExec_t chunkGraph[kMaxGraphLog] = {};
@@ -173,6 +174,7 @@ void upload_controls(lf_mesh *M, const lf_solver_controls *c, double *psi);
 // precond.cpp
 void ensure_dic(lf_mesh *M);  // build the DIC levels / rows (once), fill symU if assembled
 void build_rows(lf_mesh *M);  // the same without the DIC transport check (mesh_create, K > 4)
+void ensure_upper(lf_mesh *M);  // rebuild ld.upper from upperE if the last assembly skipped it
 void require_dic(const lf_mesh *M);  // INVALID_ARG where the DIC kernels cannot run
 void precondition(lf_mesh *M, int precond, const double *r, double *w, double *rD);
 // gamg.cpp

@@ -48,6 +48,9 @@ namespace lf {
 #ifndef LF_NO_ELL
 #define LF_NO_ELL 0      // 1: force the CSR gather (ablation)
 #endif
+#ifndef LF_UNI
+#define LF_UNI 0         // 1: ELL gathers take the labels of uniform 32-cell groups from one
+#endif                   // descriptor per (slot, group) (MeshDev.uniE, k_build_uni)
 
 constexpr int BS = LF_BS;
 constexpr unsigned FULL = 0xffffffffu;
@@ -276,6 +279,17 @@ __device__ __forceinline__ double row_offdiag(const MeshDev &m, const LduDev &a,
         lo[k] = ldv == 0xFFFFu ? -1
                 : ldv == 0xFFFEu ? __ldg(m.loE + k * n + c)
                                  : (int)((ldv >> 14) << ELL_SHIFT) | (c - o.y - (int)(ldv & 0x3FFFu) + 0x2000);
+        uo[k] = a.upperE[k * n + c];
+      }
+    } else if (LF_UNI && m.uniE) {
+      // uniform groups: the labels follow from one broadcast descriptor per
+      // slot (no per-cell label bytes); other groups read them
+      const int g = c >> 5;
+#pragma unroll
+      for (int k = 0; k < KE; ++k) {
+        const int2 u = __ldg(m.uniE + k * m.ngE + g);
+        nb[k] = u.x > 0 ? c + u.x : (u.x == 0 ? -1 : __ldg(m.nbrE + k * n + c));
+        lo[k] = u.y > 0 ? ((u.y & ~ELL_MASK) | (c - (u.y & ELL_MASK))) : (u.y == 0 ? -1 : __ldg(m.loE + k * n + c));
         uo[k] = a.upperE[k * n + c];
       }
     } else {
@@ -511,7 +525,7 @@ __global__ void __launch_bounds__(BS, LF_MINB)
     const int o0 = m.ownerStart[c], o1 = m.ownerStart[c + 1];
     for (int i = o0; i < o1; ++i) {
       const double u = __dmul_rn(m.delta[i], __dmul_rn(m.gammaF ? m.gammaF[i] : DT, m.magSf[i]));
-      a.upper[i] = -u;
+      if (a.writeUpper) a.upper[i] = -u;
       if (m.K > 0) a.upperE[(i - o0) * m.ldE + c] = -u;
       if (a.symU) a.symU[((l1 - l0) + (i - o0)) * a.ldS + c] = -u;
       L = __dsub_rn(L, u);
@@ -1798,6 +1812,56 @@ __global__ void k_build_ell(MeshDev m, const int32_t *__restrict__ owner, int32_
 void launch_build_ell(cudaStream_t s, const MeshDev &m, const int32_t *owner, int32_t K, int32_t *nbrE,
                       int32_t *loE) {
   k_build_ell<<<grid_for(m.n), BS, 0, s>>>(m, owner, K, nbrE, loE);
+}
+
+// upper (face order) from the ELL copy: face ownerStart[c] + k is slot k of c
+__global__ void k_upper_from_ell(MeshDev m, LduDev a) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < m.n; c += gridDim.x * blockDim.x) {
+    const int o0 = m.ownerStart[c], o1 = m.ownerStart[c + 1];
+    for (int i = o0; i < o1; ++i) a.upper[i] = a.upperE[(i - o0) * m.ldE + c];
+  }
+}
+
+void launch_upper_from_ell(cudaStream_t s, const MeshDev &m, const LduDev &a) {
+  k_upper_from_ell<<<grid_for(m.n), BS, 0, s>>>(m, a);
+}
+
+// ------------------------------------------ uniform 32-cell label groups
+// One warp per (slot, group): if every cell of the group has the slot with
+// the same offset nbr - c (owner side: the same owner slot kk and c - owner)
+// the group's labels are implied by {offset}; all empty -> 0; else -1.
+__global__ void k_build_uni(MeshDev m, int2 *__restrict__ uniE) {
+  const int lane = threadIdx.x & 31, ld = m.ldE;
+  const long nw = (long)m.K * m.ngE;
+  for (long wi = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; wi < nw;
+       wi += ((long)gridDim.x * blockDim.x) >> 5) {
+    const int k = (int)(wi / m.ngE), g = (int)(wi % m.ngE), c = g * 32 + lane;
+    const bool in = c < m.n;
+    const int nb = in ? m.nbrE[k * ld + c] : 0, lo = in ? m.loE[k * ld + c] : 0;
+    const unsigned inMask = __ballot_sync(FULL, in);
+    // neighbour side
+    const int vn = nb >= 0 ? nb - c : -1;
+    const unsigned anyN = __ballot_sync(FULL, in && nb >= 0), allN = __ballot_sync(FULL, !in || nb >= 0);
+    const int v0n = __shfl_sync(FULL, vn, 0);
+    const bool sameN = __all_sync(FULL, !in || vn == v0n);
+    int x = -1;
+    if (anyN == 0) x = 0;
+    else if (allN == FULL && sameN && v0n > 0) x = v0n;
+    // owner side (packed kk << 29 | owner)
+    const int vl = lo >= 0 ? ((lo & ~ELL_MASK) | (c - (lo & ELL_MASK))) : -1;
+    const unsigned anyL = __ballot_sync(FULL, in && lo >= 0), allL = __ballot_sync(FULL, !in || lo >= 0);
+    const int v0l = __shfl_sync(FULL, vl, 0);
+    const bool sameL = __all_sync(FULL, !in || vl == v0l);
+    int y = -1;
+    if (anyL == 0) y = 0;
+    else if (allL == FULL && sameL && (v0l & ELL_MASK) > 0) y = v0l;
+    (void)inMask;
+    if (lane == 0) uniE[(long)k * m.ngE + g] = make_int2(x, y);
+  }
+}
+
+void launch_build_uni(cudaStream_t s, const MeshDev &m, int2 *uniE) {
+  k_build_uni<<<grid_for((int64_t)m.K * m.ngE * 32), BS, 0, s>>>(m, uniE);
 }
 
 // ------------------------------------------------ compressed ELL labels

@@ -103,6 +103,10 @@ struct MeshDev {
   const uint32_t *codeE;
   const int2 *offE;
   int32_t ngE;
+  // uniform 32-cell groups (LF_UNI): per (slot, group) {nbr - c, (kk << 29)
+  // | (c - owner)} when every cell of the group has it (> 0), 0 when none
+  // has the slot, -1: the labels differ -> read nbrE / loE.  null: not built
+  const int2 *uniE;
   // full-row ELL (the DIC rows, DicDev): used by the Amul gathers of meshes
   // with more than 4 faces on a side (K == 0) and at most 8 neighbours
   int32_t KS, ldS;
@@ -118,6 +122,10 @@ struct LduDev {
   double *bInt, *bBnd;  // per flat boundary face: internalCoeffs, boundaryCoeffs
   double *symU;    // [KS*ldS] full-row ELL coefficients (DIC meshes), or null
   int32_t ldS;     // its slab stride
+  // 0: the assembly writes the coefficients only to upperE (ELL meshes whose
+  // consumers all read the ELL copy); `upper` is rebuilt from upperE on
+  // demand (launch_upper_from_ell: export, full-row fill).  1: both.
+  int32_t writeUpper;
 };
 
 // DIC preconditioner (dic.cuh), built on first use.
@@ -318,6 +326,8 @@ void launch_build_ell(cudaStream_t s, const MeshDev &m, const int32_t *owner, in
 // compressed labels from nbrE/loE (md.K, md.ldE, md.nbrE, md.loE set);
 // *nEsc (device int, zeroed here) receives the number of escaped entries
 void launch_build_ell16(cudaStream_t s, const MeshDev &m, uint32_t *codeE, int2 *offE, int32_t *nEsc);
+void launch_build_uni(cudaStream_t s, const MeshDev &m, int2 *uniE);  // md.K, ldE, ngE, nbrE, loE set
+void launch_upper_from_ell(cudaStream_t s, const MeshDev &m, const LduDev &a);  // upper[f] <- upperE
 // CUB wrappers (kernels.cu): stable radix sort of (key, value) pairs.
 void sort_pairs_u64(cudaStream_t s, uint64_t *keys, int32_t *vals, int64_t m, int end_bit);
 void sort_pairs_i32(cudaStream_t s, int32_t *keys, int32_t *vals, int64_t m, int end_bit);

@@ -384,6 +384,7 @@ static void build_mesh(lf_context *ctx, const lf_mesh_desc *d, lf_mesh *M) {
   LduDev &L = M->ld;
   L.diag = A.alloc<double>(n);
   L.upper = A.alloc<double>(F);
+  L.writeUpper = 1;
   L.source = A.alloc<double>(n);
   L.bInt = A.alloc<double>(B);
   L.bBnd = A.alloc<double>(B);
@@ -532,6 +533,7 @@ static void build_mesh(lf_context *ctx, const lf_mesh_desc *d, lf_mesh *M) {
   md.K = 0;
   md.nbrE = md.loE = nullptr;
   md.codeE = nullptr;
+  md.uniE = nullptr;
   md.offE = nullptr;
   md.ngE = 0;
   L.upperE = nullptr;
@@ -553,9 +555,24 @@ static void build_mesh(lf_context *ctx, const lf_mesh_desc *d, lf_mesh *M) {
       LF_CUDA(cudaMemsetAsync(L.upperE, 0, sizeof(double) * KE * (size_t)ld, s));
       md.K = KE;
       md.ldE = ld;
+#if defined(LF_NO_ELL) && LF_NO_ELL
+      L.writeUpper = 1;
+#else
+      L.writeUpper = 0;  // the solve reads upperE; upper on demand (ensure_upper)
+#endif
       launch_build_ell(s, md, owner, KE, nbrE, loE);
       md.nbrE = nbrE;
       md.loE = loE;
+      md.uniE = nullptr;
+#if defined(LF_UNI) && LF_UNI
+      {
+        // uniform 32-cell label groups (kernels.cu, k_build_uni)
+        md.ngE = (n + 31) / 32;
+        int2 *uniE = A.alloc<int2>((size_t)KE * md.ngE);
+        launch_build_uni(s, md, uniE);
+        md.uniE = uniE;
+      }
+#endif
       if (ctx->compressedLabels) {
         // 16-bit label codes for the HBM-bound gathers (kernels.cu, k_build_ell16)
         md.ngE = (n + 31) / 32;

@@ -26,6 +26,12 @@ void ensure_dic(lf_mesh *M) {
   build_rows(M);
 }
 
+void ensure_upper(lf_mesh *M) {
+  if (!M->upperStale) return;
+  M->ctx->launch(LF_K_PRECOND, [&] { launch_upper_from_ell(M->ctx->stream, M->md, M->ld); });
+  M->upperStale = false;
+}
+
 void build_rows(lf_mesh *M) {
   cudaStream_t s = M->ctx->stream;
   if (!M->dicBuilt) {
@@ -106,8 +112,10 @@ void build_rows(lf_mesh *M) {
       md->symN = dSymN;
     }
     M->dicBuilt = true;
-    if (M->ldu.assembled)
+    if (M->ldu.assembled) {
+      ensure_upper(M);
       M->ctx->launch(LF_K_PRECOND, [&] { launch_sym_fill(s, M->Lamul, M->md, M->ld); });
+    }
   }
 }
 

@@ -336,6 +336,7 @@ void solve_loop(lf_mesh *M, const lf_solver_controls *c, double *psi, bool fromA
   if (host_halo(M)) exchange_field(M, psi, ws.recvT);
   if (fromAssembly) {
     ctx->launch(LF_K_ASSEMBLE, [&] {
+      M->upperStale = !M->ld.writeUpper;
       launch_assemble(s, M->Lasm, mesh_for(M, p), M->ld, p->DT, 1.0 / p->dt, psi, M->haloT(), true, ws, T0,
                       lapSrc);
     });
