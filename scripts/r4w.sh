@@ -1,0 +1,19 @@
+set -x
+mkdir -p gpurun_out
+summ() { python -c "
+import json,sys
+for l in open(sys.argv[1]):
+    if l.startswith('{'):
+        d=json.loads(l); r=d['roofline']; print(sys.argv[2], round(d['ms_per_step'],2), [round(v/1e6,1) for v in d['repeats']['values']], round(r['frac'],3), d['config']['pcg_iterations_per_step']['mean'], d['clocks']['sm_mhz'], d['clocks']['reasons'])
+" $1 "$2"; }
+for rep in 1 2 3; do
+for lib in liblfoam_base.so liblfoam.so; do
+  LFOAM_LIB=$lib timeout 300 python bench.py --steps 10 --warmup 3 --repeats 3 --no-cpu-baseline > gpurun_out/r4w_${lib}_$rep.json 2>&1
+  summ gpurun_out/r4w_${lib}_$rep.json $lib
+done
+done
+for lib in liblfoam_base.so liblfoam.so; do
+  LFOAM_LIB=$lib timeout 300 python bench.py --steps 20 --warmup 3 --repeats 2 --config 2 --no-cpu-baseline > gpurun_out/r4w_${lib}_c2.json 2>&1
+  summ gpurun_out/r4w_${lib}_c2.json "$lib cfg2"
+done
+timeout 900 python -m pytest tests/test_gpu_hbm.py tests/test_gpu_parity.py -q -x > gpurun_out/r4w_tests.log 2>&1; tail -2 gpurun_out/r4w_tests.log
