@@ -398,9 +398,20 @@ typedef enum {
  *                      processor faces runs; the cells with them follow once
  *                      the halo has arrived (north_star: halos "overlapped with
  *                      the interior Amul").  0 = the serial sequence.
+ *   LF_OPT_L2_PREFETCH (default 0 = chosen per mesh by mesh_create; 1 on, 2
+ *                      off; read at each solve) HBM-bound persistent diagonal
+ *                      solve: every warp prefetches into L2 the lines of its
+ *                      own-cell streams (labels, owner-side coefficients, w,
+ *                      diag, p_old, psi) one grid-stride trip ahead
+ *                      (prefetch.global.L2, lane-distributed), so a trip's
+ *                      first loads hit L2 instead of HBM.  On when the
+ *                      neighbour-reuse window plus two trips fits ~0.57 of the
+ *                      L2 (200^3: +6%; 400^3 would evict its reuse window: off).
+ *                      Pure prefetch: results are bitwise the same.
  * Results are identical up to reduction grid size (all are deterministic). */
 typedef enum { LF_OPT_PERSISTENT = 0, LF_OPT_GRAPHS = 1, LF_OPT_SOLVE_VARIANT = 2,
-               LF_OPT_COMPRESSED_LABELS = 3, LF_OPT_OVERLAP_HALO = 4 } lf_option;
+               LF_OPT_COMPRESSED_LABELS = 3, LF_OPT_OVERLAP_HALO = 4,
+               LF_OPT_L2_PREFETCH = 5 } lf_option;
 LF_API lf_status lf_set_option(lf_context *ctx, lf_option opt, int value);
 
 /* enable != 0: bracket every launch of the hot kernels with CUDA events on

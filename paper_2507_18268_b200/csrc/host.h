@@ -46,6 +46,7 @@ struct lf_context {
   bool useGraphs = true;   // replay iteration chunks as CUDA graphs
   bool persistent = true;  // single-rank, no processor patches: one cooperative launch per solve
   int solveVariant = 0;    // LF_OPT_SOLVE_VARIANT: 0 by mesh size, 1 L2-resident, 2 HBM-bound
+  int l2Prefetch = 0;      // LF_OPT_L2_PREFETCH: 0 by mesh (lf_mesh::pfFits), 1 on, 2 off
   bool compressedLabels = false;  // LF_OPT_COMPRESSED_LABELS (mesh_create; r4d: slower, off)
   struct Pending {
     int kind;
@@ -109,6 +110,8 @@ struct lf_mesh {
   int persistentGrid = 0;     // co-resident grid of k_pcg_persistent
   bool l2Resident = false;    // an iteration's working set fits ~1.5x the L2 (mesh.cpp)
   bool stashOK = false;       // few enough trips per thread for the L2-resident variant
+  bool pfFits = false;        // HBM-bound solve: next-trip L2 prefetch fits the L2 (mesh.cpp)
+  int64_t bandwidth = 0;      // max |neighbour - owner| over internal faces (internal numbering)
   // NCCL transport, halo overlapped with the interior Amul: phase 1 split
   // into the cells without processor faces (interior) and those with
   int32_t *cellsInt = nullptr, *cellsBnd = nullptr;

@@ -102,6 +102,20 @@ __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned *p) {
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned ld_relaxed_sys_u32(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// Spin-waits poll with RELAXED loads and acquire once after the flag moved
+// (LF_SPIN_RELAXED): an ld.acquire compiles to LDG.STRONG + CCTL.IVALL, so
+// polling with it invalidates the SM's L1 on every poll — under the block
+// that is still computing on the same SM (its neighbour gathers then miss
+// L1).  ncu r6c, 200^3: 39M polls per solve at the alpha barrier, 23% of the
+// warp samples waiting there.
+#ifndef LF_SPIN_RELAXED
+#define LF_SPIN_RELAXED 1
+#endif
 __device__ __forceinline__ double ld_relaxed_sys(const double *p) {
   double v;
   asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
@@ -162,10 +176,11 @@ __device__ void p2p_allreduce(const P2PDev &P, double (&tot)[NV] /* valid in thr
     const unsigned *mine = P.flags[P.rank] + par * LF_MAXP + q;
     const unsigned long long t0 = gtime_ns();
     unsigned tries = 0;
-    while ((int)(ld_acquire_sys(mine) - seq) < 0) {
+    while ((int)((LF_SPIN_RELAXED ? ld_relaxed_sys_u32(mine) : ld_acquire_sys(mine)) - seq) < 0) {
       __nanosleep(64);
       spin_check(t0, tries);
     }
+    if (LF_SPIN_RELAXED) (void)ld_acquire_sys(mine);  // synchronises with the peers' releases
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -864,10 +879,26 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 #ifndef LF_SPIN_NS
 #define LF_SPIN_NS 32  // grid-barrier poll back-off (ns)
 #endif
+// wait until the barrier generation moves past gen: relaxed polls, then one
+// acquire (orders the later loads; the single L1 invalidation they need)
+__device__ __forceinline__ void wait_generation(const unsigned *gp, unsigned gen) {
+  const unsigned long long t0 = gtime_ns();
+  unsigned tries = 0;
+  while ((LF_SPIN_RELAXED ? ld_relaxed(gp) : ld_acquire(gp)) == gen) {
+    if (LF_SPIN_NS > 0) __nanosleep(LF_SPIN_NS);
+    spin_check(t0, tries);
+  }
+  if (LF_SPIN_RELAXED) (void)ld_acquire(gp);
+}
 #ifndef LF_BAR_ACQREL
 #define LF_BAR_ACQREL 1  // grid barrier with acq_rel atomics instead of fence + atomic
 #endif
@@ -882,6 +913,7 @@ constexpr int LF_DBG_N = 64, LF_DBG_G = 1024;
 __device__ unsigned long long g_dbg_arr[LF_DBG_N][LF_DBG_G], g_dbg_wake[LF_DBG_N][LF_DBG_G];
 __device__ unsigned long long g_dbg_rel[LF_DBG_N];
 __device__ int g_dbg_last[LF_DBG_N];
+__device__ int g_dbg_smid[LF_DBG_G];
 __device__ int g_dbg_i_dummy;
 #define g_dbg_i dbg_i
 #endif
@@ -906,9 +938,14 @@ __device__ void grid_reduce_sync(double (&v)[NV], double *partials, unsigned *ba
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int k = 0; k < NV; ++k) partials[k * gridDim.x + blockIdx.x] = v[k];
-    gen = ld_acquire(bar + 1);  // read before arriving: cannot move until we arrive
+    gen = ld_relaxed(bar + 1);  // read before arriving (ordered by the release of the arrival)
 #if LF_TIMING
-    if (g_dbg_i < LF_DBG_N && blockIdx.x < LF_DBG_G) g_dbg_arr[g_dbg_i][blockIdx.x] = gtime_ns();
+    if (g_dbg_i < LF_DBG_N && blockIdx.x < LF_DBG_G) {
+      g_dbg_arr[g_dbg_i][blockIdx.x] = gtime_ns();
+      unsigned sm;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+      g_dbg_smid[blockIdx.x] = (int)sm;
+    }
 #endif
     unsigned t;
     if (PEER && P.P > 0) {
@@ -933,12 +970,7 @@ __device__ void grid_reduce_sync(double (&v)[NV], double *partials, unsigned *ba
     {
       // ld.acquire.gpu orders the later loads and invalidates this SM's L1
       // (SASS CCTL.IVALL), so cached loads of other blocks' data are coherent
-      const unsigned long long t0 = gtime_ns();
-      unsigned tries = 0;
-      while (ld_acquire(bar + 1) == gen) {
-        if (LF_SPIN_NS > 0) __nanosleep(LF_SPIN_NS);
-        spin_check(t0, tries);
-      }
+      wait_generation(bar + 1, gen);
 #if LF_TIMING
       if (g_dbg_i < LF_DBG_N && blockIdx.x < LF_DBG_G) g_dbg_wake[g_dbg_i][blockIdx.x] = gtime_ns();
 #endif
@@ -953,13 +985,15 @@ __device__ void grid_reduce_sync(double (&v)[NV], double *partials, unsigned *ba
 #pragma unroll
     for (int k = 0; k < NV; ++k) s[k] = 0.0;
     constexpr int U = 8;  // one L2 round trip for grids up to 8*blockDim
-    for (int b0 = threadIdx.x; b0 < (int)gridDim.x; b0 += blockDim.x * U) {
+    const int G = (int)gridDim.x;
+    for (int b0 = threadIdx.x; b0 < G; b0 += blockDim.x * U) {
       double t[U][NV];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int b = b0 + u * blockDim.x;
 #pragma unroll
-        for (int k = 0; k < NV; ++k) t[u][k] = b < (int)gridDim.x ? __ldcg(&partials[k * gridDim.x + b]) : 0.0;
+        for (int k = 0; k < NV; ++k)
+          t[u][k] = b < G ? __ldcg(&partials[k * G + b]) : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < U; ++u)
@@ -998,7 +1032,7 @@ __device__ __forceinline__ void grid_barrier(unsigned *bar) {
   __shared__ int amLastB;
   __syncthreads();
   if (threadIdx.x == 0) {
-    const unsigned gen = ld_acquire(bar + 1);
+    const unsigned gen = ld_relaxed(bar + 1);
     unsigned t;
     asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(t) : "l"(bar) : "memory");
     amLastB = (t == gridDim.x - 1);
@@ -1006,12 +1040,7 @@ __device__ __forceinline__ void grid_barrier(unsigned *bar) {
       bar[0] = 0u;
       asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar + 1) : "memory");
     } else {
-      const unsigned long long t0 = gtime_ns();
-      unsigned tries = 0;
-      while (ld_acquire(bar + 1) == gen) {
-        if (LF_SPIN_NS > 0) __nanosleep(LF_SPIN_NS);
-        spin_check(t0, tries);
-      }
+      wait_generation(bar + 1, gen);
     }
   }
   __syncthreads();
@@ -1114,6 +1143,27 @@ __device__ __forceinline__ double row_pre(const LduDev &a, int n, const int (&lo
 #define LF_QREC 0  // HBM-bound variant: q = A p by the recurrence q_k = A w_k + beta q_{k-1}
 #endif             // (p_k = w_k + beta p_{k-1}): ONE gather per neighbour (w) instead of two
                    // (w, p_old), for one more stream (q_{k-1}, 8n)
+#ifndef LF_LPF
+#define LF_LPF 1  // HBM-bound variant: each warp prefetches into L2 (prefetch.global.L2,
+#endif            // lane-distributed: one or two instructions per thread, no registers held)
+                  // the lines of its own-cell streams LF_LPF trips ahead in phase 1 when
+                  // ws.l2pf (chosen per mesh, mesh.cpp; r6b 200^3: 40.8 -> 38.5 ms/step)
+#ifndef LF_LPF_MASK
+#define LF_LPF_MASK 15  // streams prefetched: 1 labels, 2 owner-side coefficients, 4 w / diag / p_old,
+#endif                  // 8 psi / p_{k-2}
+#ifndef LF_LPF_BULK
+#define LF_LPF_BULK 0  // 1: the prefetch as one cp.async.bulk.prefetch.L2 per stream and block run
+#endif
+#ifndef LF_LPF2
+#define LF_LPF2 0  // the same for phase 2's streams (r, q, diag), trips ahead in its order
+#endif
+__device__ __forceinline__ void l2_pf_line(const void *p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+struct PfEnt {
+  const char *p;  // array base + byte offset of the point inside a warp's run
+  int sh;         // log2 element size
+};
 #ifndef LF_PSI2
 #define LF_PSI2 1  // HBM-bound variant: psi written every second iteration (two deferred
 #endif             // updates applied in sequence: bitwise the one-at-a-time psi), -4n/iteration
@@ -1314,16 +1364,74 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
       }
       cpa_wait_all();
     }
-    if (!piped)
-    for (int i = 0; i <= nFull; ++i) {
-      const int c = i < nFull ? cstart + i * cstep : tailC;
-      if (c < 0) break;
-#else
-    for (int c = cstart; c < cend; c += cstep) {
+#if LF_TAIL
+    constexpr bool lpf = LF_LPF > 0 && !IDLE && KE > 0 && !E16 && w88 == 0 && !qrec;
+    // lane-distributed L2 prefetch table: entry e = one point (first / middle
+    // / last byte) of one stream's 32-cell run; a warp covers every line of
+    // its run with one or two prefetch instructions per lane
+    __shared__ PfEnt pfTab[64];
+    __shared__ int pfN;
+    const int wbase = (int)blockIdx.x * BS + (int)(threadIdx.x & ~31u);
+    const int lane = threadIdx.x & 31;
+    auto pf_trip = [&](int ii, int ne) {
+#if LF_LPF_BULK
+      // one bulk L2 prefetch (TMA) per stream of the block's 512-cell run
+      if (ii < nFull && (int)threadIdx.x < ne) {
+        const PfEnt e = pfTab[threadIdx.x];
+        const long cb = (long)blockIdx.x * BS + (long)ii * cstep;
+        l2_prefetch(e.p + (cb << e.sh), (unsigned)BS << e.sh);
+      }
+      return;
 #endif
+      if (ii < nFull) {
+        const long cb = (long)wbase + (long)ii * cstep;
+        if (lane < ne) l2_pf_line(pfTab[lane].p + (cb << pfTab[lane].sh));
+        if (lane + 32 < ne) l2_pf_line(pfTab[lane + 32].p + (cb << pfTab[lane + 32].sh));
+      }
+    };
+    int pfn = 0;
+    if constexpr (lpf) {
+      if (cont && ws.l2pf && threadIdx.x == 0) {
+        int e = 0;
+        const long ld = m.ldE;
+        auto addI = [&](const int32_t *b) {
+          pfTab[e++] = {(const char *)b, 2};
+          if (!LF_LPF_BULK) pfTab[e++] = {(const char *)b + 124, 2};
+        };
+        auto addD = [&](const double *b) {
+          pfTab[e++] = {(const char *)b, 3};
+          if (!LF_LPF_BULK) pfTab[e++] = {(const char *)b + 128, 3};
+          if (!LF_LPF_BULK) pfTab[e++] = {(const char *)b + 248, 3};
+        };
+        for (int kk = 0; kk < KE; ++kk) {
+          if (LF_LPF_MASK & 1) addI(m.loE + kk * ld);
+          if (LF_LPF_MASK & 1) addI(m.nbrE + kk * ld);
+          if (LF_LPF_MASK & 2) addD(a.upperE + kk * ld);
+        }
+        if (LF_LPF_MASK & 4) addD(w);
+        if (LF_LPF_MASK & 4) addD(a.diag);
+        if ((LF_LPF_MASK & 4) && !first) addD(pold);
+        if ((LF_LPF_MASK & 8) && psiPass) addD(psi);
+        if ((LF_LPF_MASK & 8) && even2) addD(pnew);
+        pfN = e;
+        e = 48;  // phase 2's streams
+        addD(ws.q);
+        addD(ws.r);
+        addD(a.diag);
+      }
+      if (threadIdx.x == 0 && !(cont && ws.l2pf)) pfN = 0;
+      __syncthreads();
+      pfn = pfN;
+      if (cont)
+        for (int ii = 0; ii < LF_LPF; ++ii) pf_trip(ii, pfn);
+    }
+#endif
+#endif  // LF_TAIL (cp.async pipeline)
+    // one cell of phase 1 (i: its trip, the stash slot of the L2-resident variant)
+    auto cell1 = [&](const int c, const int i, double (&acc)[2]) {
       const int pflag = HALO ? (int)has_proc(m, c) : 0;  // issued with the cell's own loads
       if (idleF) {
-        if (first) v1[1] += psi[c];
+        if (first) acc[1] += psi[c];
       } else if (psiPass) {
         double ps = psi[c];
         if (even2) ps = fma(alphaPrev, pnew[c], ps);  // read before pnew[c] is overwritten below
@@ -1331,7 +1439,7 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
           ps = fma(alpha, pold[c], ps);
           psi[c] = ps;
         }
-        v1[1] += ps;
+        acc[1] += ps;
       }
       if (cont) {
 #if LF_TAIL
@@ -1361,9 +1469,20 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
         else
 #endif
           ws.q[c] = q;
-        v1[0] = fma(pc, q, v1[0]);
+        acc[0] = fma(pc, q, acc[0]);
       }
+    };
+#if LF_TAIL
+    if (!piped) {
+      for (int i = 0; i < nFull; ++i) {
+        if constexpr (lpf) if (pfn > 0) pf_trip(i + LF_LPF, pfn);
+        cell1(cstart + i * cstep, i, v1);
+      }
+      if (tailC >= 0) cell1(tailC, nFull, v1);
     }
+#else
+    for (int c = cstart; c < cend; c += cstep) cell1(c, 0, v1);
+#endif
     LF_TSTAMP(1);
     // idle-time prefetch (LF_IDLE_PF): r and diag of phase 2's first trips
     // (phase 2 walks the trips backwards, LF_REVERSE): this block's 512-cell
@@ -1460,6 +1579,16 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
             const int ii = LF_REVERSE ? nFull - (i0 + u) : i0 + u;
             cs[u] = (ii >= 0 && ii < nFull) ? cstart + ii * cstep : (ii == nFull ? tailC : -1);
           }
+          if constexpr (lpf && LF_LPF2 > 0 && LF_REVERSE) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const int ii = nFull - (i0 + u + U * LF_LPF2);
+              if (ii >= 0 && lane < 9 && pfn > 0) {
+                const long cb = (long)wbase + (long)ii * cstep;
+                l2_pf_line(pfTab[48 + lane].p + (cb << pfTab[48 + lane].sh));
+              }
+            }
+          }
           p2cells(cs);
         }
       }
@@ -1545,16 +1674,18 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
            blockIdx.x, k, tacc[0] / 1e3 / k, tacc[1] / 1e3 / k, tacc[2] / 1e3 / k, tacc[3] / 1e3 / k);
   if (threadIdx.x == 0 && blockIdx.x == 0 && k > 4) {
     const int G = min((int)gridDim.x, LF_DBG_G), NB = min(LF_DBG_N, 2 * k - 2);
-    double acc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+    double acc[2][5] = {{0, 0, 0, 0, 0}, {0, 0, 0, 0, 0}};
     int cnt[2] = {0, 0};
     for (int i = 2; i < NB; ++i) {
-      unsigned long long amin = ~0ull, amax = 0, wmax = 0, wsum = 0;
+      unsigned long long amin = ~0ull, amax = 0, wmax = 0, wsum = 0, asum = 0;
+      for (int b = 0; b < G; ++b) { const unsigned long long a = __ldcg(&g_dbg_arr[i][b]); amin = a < amin ? a : amin; }
       int nw = 0;
       const int last = __ldcg(&g_dbg_last[i]);
       for (int b = 0; b < G; ++b) {
         const unsigned long long a = __ldcg(&g_dbg_arr[i][b]);
         amin = a < amin ? a : amin;
         amax = a > amax ? a : amax;
+        asum += a - amin;
         if (b != last) {
           const unsigned long long w = __ldcg(&g_dbg_wake[i][b]);
           wmax = w > wmax ? w : wmax;
@@ -1568,13 +1699,25 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
       acc[j][1] += (double)(rel - amax);
       acc[j][2] += (double)(wmax - rel);
       acc[j][3] += nw ? (double)(wsum / nw - rel) : 0.0;
+      acc[j][4] += (double)(rel - amin) - (double)asum / G;
+      if (i == 20 || i == 21 || i == 40) {
+        if (i == 20) {
+          printf("LF_SMID:");
+          for (int b = 0; b < G; ++b) printf(" %d", __ldcg(&g_dbg_smid[b]));
+          printf("\n");
+        }
+        printf("LF_ARRIVALS %d:", i);
+        for (int b = 0; b < G; ++b) printf(" %.1f", (double)(__ldcg(&g_dbg_arr[i][b]) - amin) / 1e3);
+        printf("\n");
+      }
       ++cnt[j];
     }
     for (int j = 0; j < 2; ++j)
       if (cnt[j])
         printf("LF_BARRIER %d: arrival spread %.2f us, last-arrival->release %.2f us, "
-               "release->last wake %.2f us (mean wake %.2f us)\n", j + 1, acc[j][0] / 1e3 / cnt[j],
-               acc[j][1] / 1e3 / cnt[j], acc[j][2] / 1e3 / cnt[j], acc[j][3] / 1e3 / cnt[j]);
+               "release->last wake %.2f us (mean wake %.2f us), mean arrival->release %.2f us\n", j + 1,
+               acc[j][0] / 1e3 / cnt[j], acc[j][1] / 1e3 / cnt[j], acc[j][2] / 1e3 / cnt[j],
+               acc[j][3] / 1e3 / cnt[j], acc[j][4] / 1e3 / cnt[j]);
   }
 #endif
   if (blockIdx.x == 0 && threadIdx.x == 0) {

@@ -222,6 +222,7 @@ struct Workspace {
   int32_t *sendCell;    // [n_proc] local cell of each send slot
   int maxGrid;
   int idleFlush;        // persistent solve: psi flush in the beta-barrier wait (see mesh.cpp)
+  int l2pf;             // HBM-bound persistent solve: next-trip L2 prefetch (see mesh.cpp)
   P2PDev p2p;
 };
 

@@ -240,6 +240,7 @@ static void build_mesh(lf_context *ctx, const lf_mesh_desc *d, lf_mesh *M) {
   LF_CUDA(cudaMallocAsync(&keys, sizeof(uint64_t) * std::max(F, 1), s));
   {
     std::vector<int32_t> o = relabel(d->owner, F), nb = relabel(d->neighbour, F);
+    for (int32_t f = 0; f < F; ++f) M->bandwidth = std::max<int64_t>(M->bandwidth, std::abs((int64_t)o[f] - nb[f]));
     LF_CUDA(cudaMemcpyAsync(ownerU, o.data(), sizeof(int32_t) * F, cudaMemcpyHostToDevice, s));
     LF_CUDA(cudaMemcpyAsync(nbrU, nb.data(), sizeof(int32_t) * F, cudaMemcpyHostToDevice, s));
     launch_make_keys(s, ownerU, nbrU, F, keys);
@@ -636,6 +637,14 @@ static void build_mesh(lf_context *ctx, const lf_mesh_desc *d, lf_mesh *M) {
     M->l2Resident = bytesIter <= 1.5 * (double)l2;
     M->stashOK = persistent_tail() && (int64_t)n / ((int64_t)M->persistentGrid * BSZ) + 1 <= stash_trips();
     ws.idleFlush = (M->l2Resident && M->stashOK) ? 1 : 0;
+    // HBM-bound solve, next-trip L2 prefetch (LF_LPF): the L2 must hold the
+    // neighbour-reuse window (cells c - bw .. c + bw), the current trip and
+    // the prefetched one at the iteration's bytes per cell.  Measured
+    // crossover (r6b): 200^3 (55 MB by this count) +6%, 400^3 (90 MB) -5%.
+    const double trip = (double)M->persistentGrid * BSZ;
+    const double pfBytes = (2.0 * (double)M->bandwidth + 2.0 * trip) * bytesIter / std::max<double>(n, 1);
+    M->pfFits = !M->l2Resident && pfBytes <= 0.57 * (double)l2;
+    ws.l2pf = M->pfFits ? 1 : 0;
   }
   ws.r = A.alloc<double>(n);
   ws.w = A.alloc<double>(n);

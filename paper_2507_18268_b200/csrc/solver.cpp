@@ -213,6 +213,7 @@ static void run_iterations(lf_mesh *M, lf_solver_perf *out) {
   // persistent variant: L2-resident (idle psi flush) or HBM-bound (TMA)
   // (the L2-resident variant needs few enough trips per thread for its stash)
   M->ws.idleFlush = M->stashOK && (ctx->solveVariant == 0 ? M->l2Resident : ctx->solveVariant == 1) ? 1 : 0;
+  M->ws.l2pf = (ctx->l2Prefetch == 0 ? M->pfFits : ctx->l2Prefetch == 1) ? 1 : 0;
   if (M->hctl->precond == LF_PRECOND_GAMG) {
     // GAMG: one persistent launch (Galerkin set-up, V-cycles; single rank)
     ctx->launch(LF_K_PCG_GAMG, [&] {

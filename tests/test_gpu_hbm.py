@@ -30,10 +30,11 @@ def P_():
     return _P
 
 
-def context(variant=0, compressed=True):
+def context(variant=0, compressed=True, l2_prefetch=0):
     c = P.Context(0)
     c.set_option("variant", variant)
     c.set_option("compressed_labels", compressed)
+    c.set_option("l2_prefetch", l2_prefetch)
     return c
 
 
@@ -83,6 +84,35 @@ def test_compressed_labels_bitwise_and_oracle(P_, name):
         c.close()
     np.testing.assert_array_equal(out[True][0], out[False][0])
     assert out[True][1] == out[False][1]
+
+
+@pytest.mark.parametrize("name", ["box_3trips", "perm_rcm_3trips"])
+def test_l2_prefetch_bitwise_and_oracle(P_, name):
+    """Next-trip L2 prefetch (LF_OPT_L2_PREFETCH) in the HBM-bound variant on
+    meshes of 2+ full grid-stride trips and a ragged tail (~420K cells: the
+    prefetch runs, and stops before the tail trip): prefetch on and off give
+    BITWISE the same T and iteration counts (pure prefetch), both match the
+    oracle (4 steps, T 1e-8, iterations +-1)."""
+    m = meshgen.block_mesh(81, 67, 77, bc=mixed_bc())
+    if name == "perm_rcm_3trips":
+        m = meshgen.permute_mesh(m)
+    T0 = meshgen.multimode_field(m)
+    To, _, po = oracle.laplacian_foam(m, T0, 4)
+    out = {}
+    for pf in (1, 2):
+        c = context(variant=2, compressed=False, l2_prefetch=pf)
+        mesh = P.Mesh(c, m, renumber=1 if name == "perm_rcm_3trips" else 0)
+        assert mesh.layout()["ell_width"] in (3, 4)
+        mesh.set_T(T0)
+        pg = mesh.step(4)
+        out[pf] = (mesh.get_T(), [p["n_iterations"] for p in pg])
+        T = out[pf][0]
+        assert np.max(np.abs(T - To)) <= 1e-8 * np.max(np.abs(To))
+        assert all(abs(a["n_iterations"] - b["n_iterations"]) <= 1 for a, b in zip(pg, po)), (pg, po)
+        mesh.close()
+        c.close()
+    np.testing.assert_array_equal(out[1][0], out[2][0])
+    assert out[1][1] == out[2][1]
 
 
 @pytest.mark.parametrize("variant", [1, 2])
