@@ -64,6 +64,8 @@ def parse():
                     help="gather labels of ELL meshes: the int32 labels (default) or 16-bit codes")
     ap.add_argument("--variant", type=int, default=0,
                     help="persistent solve variant: 0 by mesh size, 1 L2-resident, 2 HBM-bound")
+    ap.add_argument("--dyn-pct", type=int, default=-1,
+                    help="HBM-bound solve: %% of phase-1 trips scheduled at run time (-1 library default)")
     ap.add_argument("--l2-prefetch", type=int, default=0,
                     help="HBM-bound solve: next-trip L2 prefetch, 0 by mesh (mesh.cpp), 1 on, 2 off")
     ap.add_argument("--mode", default="persistent", choices=["persistent", "graphs", "direct"],
@@ -349,6 +351,7 @@ def run_ours(args):
     ctx.set_option("graphs", args.mode != "direct")
     ctx.set_option("variant", args.variant)
     ctx.set_option("l2_prefetch", args.l2_prefetch)
+    ctx.set_option("dynamic_trips", args.dyn_pct)
     ctx.set_option("compressed_labels", args.labels == "compressed")
 
     cfg = args.config
@@ -550,7 +553,7 @@ def run_ours(args):
         "config": {"workload": wname, "n_cells": n_global, "steps_per_run": args.steps,
                    "global_batch": 1, "seq_len": 0, "parallelism": "1gpu" if ws == 1 else f"domain{ws}-{args.transport}",
                    "renumber": args.renumber, "mode": args.mode, "precond": args.precond,
-                   "variant": args.variant, "l2_prefetch": args.l2_prefetch, "labels": args.labels,
+                   "variant": args.variant, "l2_prefetch": args.l2_prefetch, "dyn_pct": args.dyn_pct, "labels": args.labels,
                    **({"gamg_levels": mesh.gamg_hierarchy()["n"]} if args.precond == "GAMG" else {}),
                    "l2": "flushed between timed steps (256 MiB write)", "tol": TOL,
                    "pcg_iterations_per_step": {"min": min(its), "max": max(its), "mean": sum(its) / len(its)}},

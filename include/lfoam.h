@@ -408,10 +408,21 @@ typedef enum {
  *                      neighbour-reuse window plus two trips fits ~0.57 of the
  *                      L2 (200^3: +6%; 400^3 would evict its reuse window: off).
  *                      Pure prefetch: results are bitwise the same.
+ *   LF_OPT_DYNAMIC_TRIPS (default -1 = 25; 0..100 forces the percentage; read
+ *                      at each solve) HBM-bound persistent diagonal solve, one
+ *                      rank: the last N% of phase 1's grid-stride trips are
+ *                      handed out at run time (a global counter, units of 2
+ *                      trips x one 512-cell block run in sweep order), so SMs
+ *                      that run slower take fewer.  Each unit's sums are
+ *                      reduced per warp, then over the unit's warps in warp
+ *                      order, and stored per unit; the barrier adds them in
+ *                      unit order — the totals do not depend on which block
+ *                      ran which unit (deterministic; the grouping differs
+ *                      from N = 0 at rounding level).
  * Results are identical up to reduction grid size (all are deterministic). */
 typedef enum { LF_OPT_PERSISTENT = 0, LF_OPT_GRAPHS = 1, LF_OPT_SOLVE_VARIANT = 2,
                LF_OPT_COMPRESSED_LABELS = 3, LF_OPT_OVERLAP_HALO = 4,
-               LF_OPT_L2_PREFETCH = 5 } lf_option;
+               LF_OPT_L2_PREFETCH = 5, LF_OPT_DYNAMIC_TRIPS = 6 } lf_option;
 LF_API lf_status lf_set_option(lf_context *ctx, lf_option opt, int value);
 
 /* enable != 0: bracket every launch of the hot kernels with CUDA events on

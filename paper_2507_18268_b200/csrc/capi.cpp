@@ -582,7 +582,10 @@ lf_status lf_set_option(lf_context *ctx, lf_option opt, int value) {
       ctx->compressedLabels = value != 0;
     else if (opt == LF_OPT_OVERLAP_HALO)
       ctx->overlapHalo = value != 0;
-    else if (opt == LF_OPT_L2_PREFETCH) {
+    else if (opt == LF_OPT_DYNAMIC_TRIPS) {
+      LF_REQUIRE(value >= -1 && value <= 100, "dynamic trips must be -1 (default) or a percentage 0..100");
+      ctx->dynPct = value;
+    } else if (opt == LF_OPT_L2_PREFETCH) {
       LF_REQUIRE(value >= 0 && value <= 2, "l2 prefetch must be 0 (by mesh), 1 (on) or 2 (off)");
       ctx->l2Prefetch = value;
     }

@@ -39,6 +39,11 @@
 #ifndef LF_DIC_STASH_DIAG
 #define LF_DIC_STASH_DIAG 0  // ... and diag (phase 1 reads it from the stash after iteration 0)
 #endif
+#ifndef LF_DIC_LPF
+#define LF_DIC_LPF 0  // HBM-bound variant (two contiguous levels): next-trip L2 prefetch of the
+#endif                // own-cell streams of the Amul phase and both sweeps when ws.l2pf.
+                      // Measured r6l (forced on): 200^3 37.9 -> 42.0 ms/step, 400^3 585 -> 721 ms
+                      // (the pair-mode passes' L2 working set cannot take another trip): off
 #ifndef LF_DIC_PAIR
 #define LF_DIC_PAIR 1    // phase 1 interleaves the two colours (thread t: cell t of each) in the
 #endif                   // HBM-bound variant (r1x: 200^3 39.2 vs 39.9 ms/step; 100^3 3.37 vs 3.13)
@@ -194,7 +199,7 @@ __device__ __forceinline__ void dic_apply(const MeshDev &m, const DicDev &d, con
                                           const double *q, double *w, bool upd, double alpha, unsigned *bar,
                                           double *partials, double *out, const P2PDev &pp,
                                           Idle idle = Idle(), bool odd = false, const double2 *stash = nullptr,
-                                          int n = 0) {
+                                          int n = 0, const PfSet *pfs = nullptr) {
   const int L = d.L;
   double v[2] = {0.0, 0.0};
   if (stash) {
@@ -226,8 +231,15 @@ __device__ __forceinline__ void dic_apply(const MeshDev &m, const DicDev &d, con
     grid_reduce_sync<2, HALO>(v, partials, bar, out, pp LF_DBG_ARG(0), idle);
     return;
   }
+  const int S = gridDim.x * blockDim.x, lane = threadIdx.x & 31;
   for (int l = 1; l < L; ++l) {
+    const int t0 = __ldg(d.lvlStart + l), t1 = __ldg(d.lvlStart + l + 1);
+    const bool rev = LF_DIC_REVERSE && L == 2 && !odd;
     auto fwd = [&](int t) {
+      if (pfs) {  // the warp's run of the next trip (contiguous levels)
+        const int nb = t - lane + (rev ? -S : S);
+        if (nb >= t0 && nb < t1) pf_run(*pfs, nb);
+      }
       const int c = level_cell(d, t);
       double wc;
       const double rc = dic_forward_cell<KS>(d, a, c, r, q, w, upd, alpha, wc);
@@ -240,14 +252,20 @@ __device__ __forceinline__ void dic_apply(const MeshDev &m, const DicDev &d, con
     // two levels (LF_DIC_REVERSE): every pass starts where the previous one
     // ended — even iterations: Amul forwards, this pass backwards, the
     // backward pass forwards; odd iterations the mirror image
-    if (LF_DIC_REVERSE && L == 2 && !odd)
-      grid_range_rev(__ldg(d.lvlStart + l), __ldg(d.lvlStart + l + 1), fwd);
+    if (rev)
+      grid_range_rev(t0, t1, fwd);
     else
-      grid_range(__ldg(d.lvlStart + l), __ldg(d.lvlStart + l + 1), fwd);
+      grid_range(t0, t1, fwd);
     grid_barrier(bar);
   }
   for (int l = L >= 2 ? L - 2 : 0; l >= 0; --l) {
+    const int t0 = __ldg(d.lvlStart + l), t1 = __ldg(d.lvlStart + l + 1);
+    const bool rev = LF_DIC_REVERSE == 2 && L == 2 && odd;
     auto bwd = [&](int t) {
+      if (pfs) {
+        const int nb = t - lane + (rev ? -S : S);
+        if (nb >= t0 && nb < t1) pf_run(*pfs, nb);
+      }
       const int c = level_cell(d, t);
       double wc;
       const double rc = dic_backward_cell<KS>(d, a, c, l == 0, r, q, w, upd, alpha, wc);
@@ -255,10 +273,10 @@ __device__ __forceinline__ void dic_apply(const MeshDev &m, const DicDev &d, con
       v[1] = fma(wc, rc, v[1]);
       if (HALO && pp.P > 0) push_halo<HALO_W>(m, pp, c, wc);
     };
-    if (LF_DIC_REVERSE == 2 && L == 2 && odd)
-      grid_range_rev(__ldg(d.lvlStart + l), __ldg(d.lvlStart + l + 1), bwd);
+    if (rev)
+      grid_range_rev(t0, t1, bwd);
     else
-      grid_range(__ldg(d.lvlStart + l), __ldg(d.lvlStart + l + 1), bwd);
+      grid_range(t0, t1, bwd);
     if (l > 0) grid_barrier(bar);
   }
   grid_reduce_sync<2, HALO>(v, partials, bar, out, pp LF_DBG_ARG(0), idle);
@@ -352,6 +370,17 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
   const int nTrips = (m.n + stride - 1) / stride;
   const bool stash = LF_DIC_STASH && IDLE && d.contig && L == 2 && nTrips <= LF_STASH_TRIPS;
   const int n0s = stash ? __ldg(d.lvlStart + 1) : 0;
+  // next-trip L2 prefetch (HBM-bound variant, two contiguous levels)
+  const bool dpf = LF_DIC_LPF && pair && ws.l2pf;
+  __shared__ PfSet pfA, pfS;  // Amul phase (rebuilt per iteration: p_old), sweeps
+  if (dpf && threadIdx.x == 0) {
+    pfS.clear();
+    for (int kk = 0; kk < KS; ++kk) pfS.addI(d.symN + kk * d.ldS);
+    for (int kk = 0; kk < KS; ++kk) pfS.addD(a.symU + kk * d.ldS);
+    pfS.addD(r);
+    pfS.addD(q);
+    pfS.addD(d.rD);
+  }
 
   if (threadIdx.x == 0) {
     st.k = ctl->it;
@@ -415,6 +444,15 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
         st.beta = wn / st.wArA;
         st.wArA = wn;
       }
+      if (dpf) {
+        pfA.clear();
+        for (int kk = 0; kk < KS; ++kk) pfA.addI(d.symN + kk * d.ldS);
+        for (int kk = 0; kk < KS; ++kk) pfA.addD(a.symU + kk * d.ldS);
+        pfA.addD(psi);
+        pfA.addD(w);
+        pfA.addD(a.diag);
+        if (st.k > 0) pfA.addD((st.k & 1) ? ws.p[0] : ws.p[1]);  // p_old
+      }
     }
     __syncthreads();
     const int k = st.k;
@@ -441,7 +479,14 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
       if (odd)
         grid_range_rev(0, nt, two);
       else
-        for (int t = gtid; t < nt; t += stride) two(t);
+        for (int t = gtid; t < nt; t += stride) {
+          if (dpf) {  // both colours' runs of the next trip
+            const int nb = t - (int)(threadIdx.x & 31) + stride;
+            if (nb < n0) pf_run(pfA, nb);
+            if (nb < n1) pf_run(pfA, n0 + nb);
+          }
+          two(t);
+        }
     } else if (stash) {
       for (int i = 0; i < nTrips; ++i) {
         const int c = gtid + i * stride;
@@ -485,7 +530,8 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
       });
     };
     dic_apply<KS, HALO>(m, d, a, r, q, w, true, alphaK, bar, ws.partials, ws.gsum->p2, pp, flush,
-                        LF_DIC_REVERSE == 2 && L == 2 && (st.k & 1), stash ? lf_dstash : nullptr, m.n);
+                        LF_DIC_REVERSE == 2 && L == 2 && (st.k & 1), stash ? lf_dstash : nullptr, m.n,
+                        dpf ? &pfS : nullptr);
     if (threadIdx.x == 0) ++st.k;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {

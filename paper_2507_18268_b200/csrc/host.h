@@ -46,6 +46,7 @@ struct lf_context {
   bool useGraphs = true;   // replay iteration chunks as CUDA graphs
   bool persistent = true;  // single-rank, no processor patches: one cooperative launch per solve
   int solveVariant = 0;    // LF_OPT_SOLVE_VARIANT: 0 by mesh size, 1 L2-resident, 2 HBM-bound
+  int dynPct = -1;         // LF_OPT_DYNAMIC_TRIPS: % of phase-1 trips scheduled at run time (-1 default)
   int l2Prefetch = 0;      // LF_OPT_L2_PREFETCH: 0 by mesh (lf_mesh::pfFits), 1 on, 2 off
   bool compressedLabels = false;  // LF_OPT_COMPRESSED_LABELS (mesh_create; r4d: slower, off)
   struct Pending {

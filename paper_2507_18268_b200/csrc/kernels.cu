@@ -54,7 +54,7 @@ namespace lf {
 
 constexpr int BS = LF_BS;
 constexpr unsigned FULL = 0xffffffffu;
-enum { T_SUM = 0, T_ASM = 1, T_SETUP = 2, T_P1 = 3, T_P2 = 4, T_P1I = 5 };
+enum { T_SUM = 0, T_ASM = 1, T_SETUP = 2, T_P1 = 3, T_P2 = 4, T_P1I = 5, T_DYN = 8 };
 constexpr int ELL_SHIFT = 29;  // slot kk <= 3 in bits 29-30: the packed label stays >= 0
 constexpr int ELL_MASK = (1 << ELL_SHIFT) - 1;
 
@@ -930,7 +930,12 @@ __device__ void grid_reduce_sync(double (&v)[NV], double *partials, unsigned *ba
 #if LF_TIMING
                                  , int dbg_i
 #endif
-                                 , Idle idle = Idle()) {
+                                 , Idle idle = Idle(), const double *xtra = nullptr, int nx = 0,
+                                 unsigned *rst = nullptr) {
+  // xtra (nx > 0): per-unit sums of run-time scheduled work (xtra[k * nx +
+  // u]), added after the gridDim.x block partials in index order: the totals
+  // do not depend on which block ran a unit; rst: a counter the last block
+  // zeroes before releasing
   __shared__ double sm[NV][32];
   __shared__ int amLast;
   block_sum<NV>(v, sm);
@@ -985,15 +990,15 @@ __device__ void grid_reduce_sync(double (&v)[NV], double *partials, unsigned *ba
 #pragma unroll
     for (int k = 0; k < NV; ++k) s[k] = 0.0;
     constexpr int U = 8;  // one L2 round trip for grids up to 8*blockDim
-    const int G = (int)gridDim.x;
-    for (int b0 = threadIdx.x; b0 < G; b0 += blockDim.x * U) {
+    const int G = (int)gridDim.x, NT = G + nx;
+    for (int b0 = threadIdx.x; b0 < NT; b0 += blockDim.x * U) {
       double t[U][NV];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int b = b0 + u * blockDim.x;
 #pragma unroll
         for (int k = 0; k < NV; ++k)
-          t[u][k] = b < G ? __ldcg(&partials[k * G + b]) : 0.0;
+          t[u][k] = b < G ? __ldcg(&partials[k * G + b]) : (b < NT ? __ldcg(&xtra[(long)k * nx + (b - G)]) : 0.0);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u)
@@ -1005,6 +1010,7 @@ __device__ void grid_reduce_sync(double (&v)[NV], double *partials, unsigned *ba
     if (threadIdx.x == 0) {
 #pragma unroll
       for (int k = 0; k < NV; ++k) out[k] = s[k];
+      if (rst) *rst = 0u;
       bar[0] = 0u;
 #if LF_TIMING
       if (g_dbg_i < LF_DBG_N) {
@@ -1053,6 +1059,18 @@ __device__ __forceinline__ void grid_barrier(unsigned *bar) {
 #ifndef LF_TIMING
 #define LF_TIMING 0  // 1: per-phase / per-barrier times printed by the persistent kernel
 #endif
+// default share (%) of phase-1 trips scheduled at run time (HBM-bound
+// variant; r6n/r6o: 200^3 on a box with slow SMs 44.4 -> 40.3 ms/step,
+// elsewhere within +-1%; 400^3 658 -> 636 ms)
+#ifndef LF_DYN_PCT
+#define LF_DYN_PCT 25
+#endif
+#ifndef LF_DYN_UT
+#define LF_DYN_UT 2  // grid-stride trips per run-time scheduled unit (UT x one 512-cell block run)
+#endif
+#ifndef LF_DYN_MAXU
+#define LF_DYN_MAXU 32  // run-time units a block may take per phase (shared-memory slots)
+#endif
 #ifndef LF_CHUNKED
 #define LF_CHUNKED 0  // persistent kernel: contiguous cell chunk per block (vs grid stride).
 #endif                // r1n: chunks raise the phase-1 arrival spread 6 -> 28 us at 100^3 -> off
@@ -1074,6 +1092,7 @@ bool persistent_chunked() { return LF_CHUNKED != 0; }
 #endif
 bool persistent_tail() { return LF_TAIL != 0; }
 int stash_trips() { return LF_TAIL ? LF_STASH_TRIPS : 0; }
+int dynamic_trips_pct() { return LF_DYN_PCT; }
 static size_t stash_bytes() { return (size_t)LF_STASH_TRIPS * BS * sizeof(double2); }
 #ifndef LF_STASH_FIT
 #define LF_STASH_FIT 1  // launch with only the stash slots the mesh's trips use (more L1 left)
@@ -1185,6 +1204,12 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
     int k, cont, singular;
   };
   __shared__ St st;
+  // run-time trips (phase 1, see below): claimed unit per slot (-1: not yet)
+  // and each warp's sums per slot
+  constexpr bool dyn = LF_TAIL && !IDLE && !HALO && !qrec && w88 == 0 && !cpa;
+  __shared__ int dynU[dyn ? LF_DYN_MAXU : 1];
+  __shared__ double dynP[dyn ? LF_DYN_MAXU : 1][BS / 32][2];
+  if (dyn && (int)threadIdx.x < LF_DYN_MAXU) dynU[threadIdx.x] = -1;
   if (threadIdx.x == 0) {
     st.k = ctl->it;
     st.nf = ctl->normFactor;
@@ -1373,6 +1398,11 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
     __shared__ int pfN;
     const int wbase = (int)blockIdx.x * BS + (int)(threadIdx.x & ~31u);
     const int lane = threadIdx.x & 31;
+    // lane-distributed prefetch of the warp's 32-cell run starting at cell cb
+    auto pf_cb = [&](long cb, int ne) {
+      if (lane < ne) l2_pf_line(pfTab[lane].p + (cb << pfTab[lane].sh));
+      if (lane + 32 < ne) l2_pf_line(pfTab[lane + 32].p + (cb << pfTab[lane + 32].sh));
+    };
     auto pf_trip = [&](int ii, int ne) {
 #if LF_LPF_BULK
       // one bulk L2 prefetch (TMA) per stream of the block's 512-cell run
@@ -1473,10 +1503,90 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
       }
     };
 #if LF_TAIL
+    // Run-time trips (HBM-bound variant, one rank; ws.dynTrips > 0): the
+    // last trips are handed out by a global counter in units of LF_DYN_UT
+    // trips x one block run (unit u: trip row u / G, block slot u % G — sweep
+    // order), so SMs that run slower take fewer.  No block-wide barrier per
+    // unit: thread 0 claims units two ahead into shared-memory slots the
+    // warps poll; each warp stores its unit sums per slot, and after the
+    // phase the block adds a unit's 16 warp sums in warp order and stores
+    // them per unit -> totals independent of which block ran which unit.
+    constexpr int UT = LF_DYN_UT, MAXU = LF_DYN_MAXU;
+    auto n_dyn = [&]() { return dyn ? min(ws.dynTrips, nFull) : 0; };
+    auto n_units = [&]() { return ((n_dyn() + UT - 1) / UT) * (int)gridDim.x; };
     if (!piped) {
-      for (int i = 0; i < nFull; ++i) {
-        if constexpr (lpf) if (pfn > 0) pf_trip(i + LF_LPF, pfn);
-        cell1(cstart + i * cstep, i, v1);
+      if constexpr (dyn) if (n_dyn() > 0 && threadIdx.x == 0) {
+        dynU[0] = (int)atomicAdd(ws.tickets + T_DYN, 1u);
+        dynU[1] = (int)atomicAdd(ws.tickets + T_DYN, 1u);
+      }
+      {
+        const int nStat = nFull - n_dyn();
+        for (int i = 0; i < nStat; ++i) {
+          if constexpr (lpf) if (pfn > 0 && i + LF_LPF < nStat) pf_trip(i + LF_LPF, pfn);
+          cell1(cstart + i * cstep, i, v1);
+        }
+      }
+      if constexpr (dyn) if (n_dyn() > 0) {
+        const int G = gridDim.x, nStat = nFull - n_dyn(), UD = n_units(), wid = threadIdx.x >> 5;
+        constexpr int ut = UT;
+        volatile int *vU = dynU;
+        for (;;) {  // rounds of up to MAXU units (slots flushed between rounds)
+          int J = 0;
+          bool done = false;
+          for (; J < MAXU; ++J) {
+            int u;
+            while ((u = vU[J]) < 0) __nanosleep(32);  // thread 0 has not claimed slot J yet
+            if (u >= UD) {
+              done = true;
+              break;
+            }
+            int nxt = 0;
+            if (threadIdx.x == 0 && J + 2 < MAXU) nxt = (int)atomicAdd(ws.tickets + T_DYN, 1u);
+            if constexpr (lpf) if (pfn > 0 && J + 1 < MAXU) {
+              const int un = vU[J + 1];  // the next unit, if claimed: its lines into L2 now
+              if (un >= 0 && un < UD) {
+                const int rn = un / G, sn = un - rn * G;
+#pragma unroll
+                for (int jj = 0; jj < ut; ++jj) {
+                  const int ii = nStat + rn * ut + jj;
+                  if (ii < nFull) pf_cb((long)ii * cstep + (long)sn * BS + (long)(threadIdx.x & ~31u), pfn);
+                }
+              }
+            }
+            const int row = u / G, sl = u - row * G;
+            double vu[2] = {0.0, 0.0};
+#pragma unroll
+            for (int jj = 0; jj < ut; ++jj) {
+              const int ii = nStat + row * ut + jj;
+              if (ii < nFull) cell1(ii * cstep + sl * BS + (int)threadIdx.x, ii, vu);
+            }
+            warp_sum<2>(vu);
+            if (lane == 0) {
+              dynP[J][wid][0] = vu[0];
+              dynP[J][wid][1] = vu[1];
+            }
+            if (threadIdx.x == 0 && J + 2 < MAXU) vU[J + 2] = nxt;
+          }
+          __syncthreads();  // every warp is past its last slot read; dynP complete
+          if ((int)threadIdx.x < J) {
+            const int j = threadIdx.x, u = dynU[j];
+            double s0 = 0.0, s1 = 0.0;
+            for (int wv = 0; wv < BS / 32; ++wv) {  // warp order: deterministic
+              s0 += dynP[j][wv][0];
+              s1 += dynP[j][wv][1];
+            }
+            ws.partialsD[u] = s0;
+            ws.partialsD[UD + u] = s1;
+          }
+          __syncthreads();  // slots read
+          if ((int)threadIdx.x < MAXU) dynU[threadIdx.x] = -1;
+          if (done) break;  // (the next phase's claims follow a grid barrier)
+          __syncthreads();  // reset visible before the next round's claims
+          if (threadIdx.x == 0) {
+            vU[0] = (int)atomicAdd(ws.tickets + T_DYN, 1u);
+            vU[1] = (int)atomicAdd(ws.tickets + T_DYN, 1u);
+          }
+        }
       }
       if (tailC >= 0) cell1(tailC, nFull, v1);
     }
@@ -1499,7 +1609,15 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
         }
       }
     };
+#if LF_TAIL
+    {
+      const bool dy = n_dyn() > 0;
+      grid_reduce_sync<2, HALO>(v1, ws.partials, bar, ws.gsum->p1, ws.p2p LF_DBG_ARG(2 * k), pf1,
+                                dy ? ws.partialsD : nullptr, dy ? n_units() : 0, dy ? ws.tickets + T_DYN : nullptr);
+    }
+#else
     grid_reduce_sync<2, HALO>(v1, ws.partials, bar, ws.gsum->p1, ws.p2p LF_DBG_ARG(2 * k), pf1);
+#endif
     LF_TSTAMP(2);
     if (!cont) break;
     // ---- phase 2: singularity, alpha, r -= alpha q, w = r/diag, sums
@@ -2097,6 +2215,33 @@ void sort_pairs_u64(cudaStream_t s, uint64_t *keys, int32_t *vals, int64_t m, in
 }
 void sort_pairs_i32(cudaStream_t s, int32_t *keys, int32_t *vals, int64_t m, int end_bit) {
   sort_pairs<int32_t>(s, keys, vals, m, end_bit);
+}
+
+// ------------------------------------- lane-distributed L2 prefetch sets
+// A list of (array, point) entries — first / last byte of an int array's
+// 32-cell run, first / middle / last byte of a double array's — so that one
+// warp covers every line of its run with one or two prefetch instructions
+// per lane (the L2 prefetch of k_pcg_persistent, for the other solves).
+struct PfSet {
+  PfEnt e[48];
+  int n;
+  __device__ void clear() { n = 0; }
+  __device__ void addI(const int32_t *b) {
+    e[n++] = {(const char *)b, 2};
+    e[n++] = {(const char *)b + 124, 2};
+  }
+  __device__ void addD(const double *b) {
+    e[n++] = {(const char *)b, 3};
+    e[n++] = {(const char *)b + 128, 3};
+    e[n++] = {(const char *)b + 248, 3};
+  }
+};
+// prefetch the warp's run of 32 cells starting at cb (every lane passes the
+// same cb)
+__device__ __forceinline__ void pf_run(const PfSet &s, long cb) {
+  const int lane = threadIdx.x & 31, n = s.n;
+  if (lane < n) l2_pf_line(s.e[lane].p + (cb << s.e[lane].sh));
+  if (lane + 32 < n) l2_pf_line(s.e[lane + 32].p + (cb << s.e[lane + 32].sh));
 }
 
 // ----------------------------------------------------- DIC preconditioner

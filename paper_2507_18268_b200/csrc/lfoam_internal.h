@@ -210,6 +210,9 @@ struct Workspace {
   double *r, *w, *q, *p[2];
   double *rDiag;        // 1/diag of the current solve (LF_W88 == 2 variant only)
   double *partials;     // [4 * maxGrid]
+  double *partialsD;    // [2 * dynCap] per-unit sums of the run-time scheduled phase-1 trips
+  int dynCap;           // capacity of partialsD per sum
+  int dynTrips;         // HBM-bound persistent solve: phase-1 trips scheduled at run time (solver.cpp)
   unsigned *tickets;    // [16]
   PcgCtl *ctl;
   RedSlots *gsum;       // global sums
@@ -281,6 +284,7 @@ void launch_amul(cudaStream_t s, const Launch &L, const MeshDev &m, const LduDev
 int persistent_grid(int device, int K);
 bool persistent_tail();  // LF_TAIL: SM-uniform grid, evenly spread tail trip
 int stash_trips();       // max grid-stride trips of the L2-resident variant (0: none)
+int dynamic_trips_pct();  // default % of phase-1 trips scheduled at run time (HBM-bound variant)
 bool persistent_chunked();
 void launch_pcg_persistent(cudaStream_t s, int grid, const MeshDev &m, const LduDev &a,
                            const Workspace &ws, unsigned *bar);

@@ -655,6 +655,8 @@ static void build_mesh(lf_context *ctx, const lf_mesh_desc *d, lf_mesh *M) {
   ws.p[0] = A.alloc<double>(n);
   ws.p[1] = A.alloc<double>(n);
   ws.partials = A.alloc<double>(4 * (size_t)maxGrid);
+  ws.dynCap = (int)(n / BSZ) + 2 * maxGrid + 2;
+  ws.partialsD = A.alloc<double>(2 * (size_t)ws.dynCap);
   ws.tickets = A.alloc<unsigned>(16);
   LF_CUDA(cudaMemsetAsync(ws.tickets, 0, 16 * sizeof(unsigned), s));
   ws.ctl = A.alloc<PcgCtl>(1);

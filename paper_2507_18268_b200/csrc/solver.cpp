@@ -214,6 +214,13 @@ static void run_iterations(lf_mesh *M, lf_solver_perf *out) {
   // (the L2-resident variant needs few enough trips per thread for its stash)
   M->ws.idleFlush = M->stashOK && (ctx->solveVariant == 0 ? M->l2Resident : ctx->solveVariant == 1) ? 1 : 0;
   M->ws.l2pf = (ctx->l2Prefetch == 0 ? M->pfFits : ctx->l2Prefetch == 1) ? 1 : 0;
+  {
+    // HBM-bound solve, one rank: the last trips of phase 1 are handed out at
+    // run time (kernels.cu "run-time trips")
+    const int64_t nFull = M->n / ((int64_t)M->persistentGrid * kernel_block_size());
+    const int pct = ctx->dynPct >= 0 ? ctx->dynPct : dynamic_trips_pct();
+    M->ws.dynTrips = M->ws.idleFlush ? 0 : (int)(nFull * pct / 100);
+  }
   if (M->hctl->precond == LF_PRECOND_GAMG) {
     // GAMG: one persistent launch (Galerkin set-up, V-cycles; single rank)
     ctx->launch(LF_K_PCG_GAMG, [&] {

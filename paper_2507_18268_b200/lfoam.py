@@ -30,7 +30,7 @@ PRECONDITIONERS = {"diagonal": 0, "DIC": 1, "DILU": 2, "GAMG": 3}
 GAMG_MAXL = 30
 # lf_mesh_desc.renumber
 RENUMBER = {False: 0, True: 1, 0: 0, 1: 1, 2: 2, "none": 0, "rcm": 1, "colour": 2}
-OPTIONS = {"persistent": 0, "graphs": 1, "variant": 2, "compressed_labels": 3, "overlap_halo": 4, "l2_prefetch": 5}
+OPTIONS = {"persistent": 0, "graphs": 1, "variant": 2, "compressed_labels": 3, "overlap_halo": 4, "l2_prefetch": 5, "dynamic_trips": 6}
 
 
 class LfoamError(RuntimeError):

@@ -105,6 +105,27 @@ def test_config4_closed_form(P):
     ctx.close()
 
 
+def test_config4_runtime_trips_closed_form(P):
+    """400^3 with 40% of phase 1's trips scheduled at run time (~168 trips,
+    ~84 units per block: several rounds of the shared-memory claim slots):
+    3 steps vs the exact decay, every solve converged in the diagonal run's
+    iteration range."""
+    m = meshgen.block_mesh(400)
+    s = meshgen.canonical_field(m)
+    ctx = P.Context(0)
+    ctx.set_option("dynamic_trips", 40)
+    mesh = P.Mesh(ctx, m)
+    mesh.set_T(s)
+    perfs = mesh.step(3)
+    T = mesh.get_T()
+    g, _ = g_factor(400)
+    ref = g ** 3 * s
+    assert np.max(np.abs(T - ref)) <= 1e-8 * np.max(np.abs(ref))
+    its = [p["n_iterations"] for p in perfs]
+    assert all(p["converged"] for p in perfs) and max(its) <= 450, its
+    ctx.close()
+
+
 @pytest.mark.parametrize("renumber", [False, True])
 def test_config5_permuted_closed_form(P, renumber):
     """Permuted 200^3 (BASELINE config 5): raw gather stress and RCM."""

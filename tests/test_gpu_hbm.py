@@ -115,6 +115,32 @@ def test_l2_prefetch_bitwise_and_oracle(P_, name):
     assert out[1][1] == out[2][1]
 
 
+@pytest.mark.parametrize("pct", [25, 100])
+def test_runtime_trips_deterministic_and_oracle(P_, pct):
+    """Run-time scheduled phase-1 trips (LF_OPT_DYNAMIC_TRIPS) on a mesh of
+    several grid-stride trips with a ragged tail (~420K cells, mixed
+    patches): T matches the oracle (4 steps, T 1e-8, iterations +-1) and a
+    second run is BITWISE identical (per-unit sums, added in unit order)."""
+    m = meshgen.block_mesh(81, 67, 77, bc=mixed_bc())
+    T0 = meshgen.multimode_field(m)
+    To, _, po = oracle.laplacian_foam(m, T0, 4)
+    res = []
+    for rep in range(2):
+        c = context(variant=2, compressed=False, l2_prefetch=1)
+        c.set_option("dynamic_trips", pct)
+        mesh = P.Mesh(c, m)
+        mesh.set_T(T0)
+        pg = mesh.step(4)
+        T = mesh.get_T()
+        assert np.max(np.abs(T - To)) <= 1e-8 * np.max(np.abs(To))
+        assert all(abs(a["n_iterations"] - b["n_iterations"]) <= 1 for a, b in zip(pg, po)), (pg, po)
+        res.append((T, [p["n_iterations"] for p in pg]))
+        mesh.close()
+        c.close()
+    np.testing.assert_array_equal(res[0][0], res[1][0])
+    assert res[0][1] == res[1][1]
+
+
 @pytest.mark.parametrize("variant", [1, 2])
 @pytest.mark.parametrize("kw", [dict(max_iter=1), dict(max_iter=2), dict(max_iter=5), dict(max_iter=6),
                                 dict(min_iter=41), dict(min_iter=42), dict(tol=0.0, rel_tol=1e-3)])
