@@ -1060,10 +1060,12 @@ __device__ __forceinline__ void grid_barrier(unsigned *bar) {
 #define LF_TIMING 0  // 1: per-phase / per-barrier times printed by the persistent kernel
 #endif
 // default share (%) of phase-1 trips scheduled at run time (HBM-bound
-// variant; r6n/r6o: 200^3 on a box with slow SMs 44.4 -> 40.3 ms/step,
-// elsewhere within +-1%; 400^3 658 -> 636 ms)
+// variant).  200^3 on boxes with slow SMs (r6n/r6r/r6s): 43.4-44.4 ->
+// 41.2-41.5 ms/step at 25-40% (best 33%); on the others 38.9-39.3 at 0%,
+// -1% at 25%, -2% at 40% (r6o/r6q); 400^3 658 -> 636 ms; permuted 200^3
+// 199 -> 191 ms
 #ifndef LF_DYN_PCT
-#define LF_DYN_PCT 25
+#define LF_DYN_PCT 30
 #endif
 #ifndef LF_DYN_UT
 #define LF_DYN_UT 2  // grid-stride trips per run-time scheduled unit (UT x one 512-cell block run)
@@ -1522,7 +1524,22 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
       {
         const int nStat = nFull - n_dyn();
         for (int i = 0; i < nStat; ++i) {
-          if constexpr (lpf) if (pfn > 0 && i + LF_LPF < nStat) pf_trip(i + LF_LPF, pfn);
+          if constexpr (lpf) if (pfn > 0) {
+            if (i + LF_LPF < nStat) {
+              pf_trip(i + LF_LPF, pfn);
+            } else if constexpr (dyn) {
+              // last static trip: the block's first claimed unit instead
+              const int u0 = ((volatile int *)dynU)[0], G = gridDim.x, UD = n_units();
+              if (u0 >= 0 && u0 < UD) {
+                const int r0 = u0 / G, s0 = u0 - r0 * G;
+#pragma unroll
+                for (int jj = 0; jj < UT; ++jj) {
+                  const int ii = nStat + r0 * UT + jj;
+                  if (ii < nFull) pf_cb((long)ii * cstep + (long)s0 * BS + (long)(threadIdx.x & ~31u), pfn);
+                }
+              }
+            }
+          }
           cell1(cstart + i * cstep, i, v1);
         }
       }
