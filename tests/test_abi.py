@@ -101,3 +101,14 @@ def test_product_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "liboracle" not in txt and "lfoam_oracle" not in txt, f
+
+
+def test_binding_option_ids_match_header():
+    """lfoam.py's option names map to the lf_option values include/lfoam.h
+    declares (LF_OPT_<NAME> = id), one for one."""
+    import paper_2507_18268_b200.lfoam as L
+    src = open(HEADER).read()
+    body = re.search(r"typedef enum \{([^}]*)\} lf_option;", src).group(1)
+    ids = {m.group(1).lower(): int(m.group(2)) for m in re.finditer(r"LF_OPT_(\w+)\s*=\s*(\d+)", body)}
+    alias = {"solve_variant": "variant"}
+    assert {alias.get(k, k): v for k, v in ids.items()} == L.OPTIONS
