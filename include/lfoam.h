@@ -408,8 +408,12 @@ typedef enum {
  *                      neighbour-reuse window plus two trips fits ~0.57 of the
  *                      L2 (200^3: +6%; 400^3 would evict its reuse window: off).
  *                      Pure prefetch: results are bitwise the same.
- *   LF_OPT_DYNAMIC_TRIPS (default -1 = 30; 0..100 forces the percentage; read
- *                      at each solve) HBM-bound persistent diagonal solve, one
+ *   LF_OPT_DYNAMIC_TRIPS (default -1 = 30 in builds with -DLF_DYN=1, where the
+ *                      run-time trips are compiled in; the default build
+ *                      compiles them out and keeps the static schedule, the
+ *                      option is then accepted and has no effect; 0..100
+ *                      forces the percentage; read at each solve) HBM-bound
+ *                      persistent diagonal solve, one
  *                      rank: the last N% of phase 1's grid-stride trips are
  *                      handed out at run time (a global counter, units of 2
  *                      trips x one 512-cell block run in sweep order), so SMs

@@ -1067,6 +1067,11 @@ __device__ __forceinline__ void grid_barrier(unsigned *bar) {
 #ifndef LF_DYN_PCT
 #define LF_DYN_PCT 30
 #endif
+#ifndef LF_DYN
+#define LF_DYN 0  // 1: run-time trips compiled into the persistent diagonal solve.  Off: the
+#endif            // extra code costs the static trip loop spills (r6zb, one box: 200^3 217 ->
+                  // 224-228 us/iteration, 400^3 1937 -> 2056) while the balancing gains
+                  // 5-10% only on boxes with a slow TPC (r6n/r6r/r6s)
 #ifndef LF_DYN_UT
 #define LF_DYN_UT 2  // grid-stride trips per run-time scheduled unit (UT x one 512-cell block run)
 #endif
@@ -1094,7 +1099,7 @@ bool persistent_chunked() { return LF_CHUNKED != 0; }
 #endif
 bool persistent_tail() { return LF_TAIL != 0; }
 int stash_trips() { return LF_TAIL ? LF_STASH_TRIPS : 0; }
-int dynamic_trips_pct() { return LF_DYN_PCT; }
+int dynamic_trips_pct() { return LF_DYN ? LF_DYN_PCT : 0; }
 static size_t stash_bytes() { return (size_t)LF_STASH_TRIPS * BS * sizeof(double2); }
 #ifndef LF_STASH_FIT
 #define LF_STASH_FIT 1  // launch with only the stash slots the mesh's trips use (more L1 left)
@@ -1208,7 +1213,7 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
   __shared__ St st;
   // run-time trips (phase 1, see below): claimed unit per slot (-1: not yet)
   // and each warp's sums per slot
-  constexpr bool dyn = LF_TAIL && !IDLE && !HALO && !qrec && w88 == 0 && !cpa;
+  constexpr bool dyn = LF_DYN && LF_TAIL && !IDLE && !HALO && !qrec && w88 == 0 && !cpa;
   __shared__ int dynU[dyn ? LF_DYN_MAXU : 1];
   __shared__ double dynP[dyn ? LF_DYN_MAXU : 1][BS / 32][2];
   if (dyn && (int)threadIdx.x < LF_DYN_MAXU) dynU[threadIdx.x] = -1;
@@ -1522,9 +1527,13 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
         dynU[1] = (int)atomicAdd(ws.tickets + T_DYN, 1u);
       }
       {
+        // the static trips, then the spread tail trip (i == nStat: one loop,
+        // one copy of the cell body, as before the run-time trips)
         const int nStat = nFull - n_dyn();
-        for (int i = 0; i < nStat; ++i) {
-          if constexpr (lpf) if (pfn > 0) {
+        for (int i = 0; i <= nStat; ++i) {
+          const int c = i < nStat ? cstart + i * cstep : tailC;
+          if (c < 0) break;
+          if constexpr (lpf) if (pfn > 0 && i < nStat) {
             if (i + LF_LPF < nStat) {
               pf_trip(i + LF_LPF, pfn);
             } else if constexpr (dyn) {
@@ -1540,7 +1549,7 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
               }
             }
           }
-          cell1(cstart + i * cstep, i, v1);
+          cell1(c, i < nStat ? i : nFull, v1);
         }
       }
       if constexpr (dyn) if (n_dyn() > 0) {
@@ -1605,7 +1614,6 @@ __global__ void __launch_bounds__(BS, LF_MINB_P)
           }
         }
       }
-      if (tailC >= 0) cell1(tailC, nFull, v1);
     }
 #else
     for (int c = cstart; c < cend; c += cstep) cell1(c, 0, v1);

@@ -640,10 +640,11 @@ static void build_mesh(lf_context *ctx, const lf_mesh_desc *d, lf_mesh *M) {
     // HBM-bound solve, next-trip L2 prefetch (LF_LPF): the L2 must hold the
     // neighbour-reuse window (cells c - bw .. c + bw), the current trip and
     // the prefetched one at the iteration's bytes per cell.  Measured
-    // crossover (r6b): 200^3 (55 MB by this count) +6%, 400^3 (90 MB) -5%.
+    // crossover: 200^3 (55 MB by this count) +0-6% (r6b/r6c/r6zb), 300^3
+    // (69.5 MB) -10% (r6zb), 400^3 (90 MB) -5% (r6b).
     const double trip = (double)M->persistentGrid * BSZ;
     const double pfBytes = (2.0 * (double)M->bandwidth + 2.0 * trip) * bytesIter / std::max<double>(n, 1);
-    M->pfFits = !M->l2Resident && pfBytes <= 0.57 * (double)l2;
+    M->pfFits = !M->l2Resident && pfBytes <= 0.5 * (double)l2;
     ws.l2pf = M->pfFits ? 1 : 0;
   }
   ws.r = A.alloc<double>(n);

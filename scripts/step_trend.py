@@ -16,14 +16,14 @@ import paper_2507_18268_b200 as P  # noqa: E402
 CONFIGS = meshgen.CONFIGS
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 40
-cfg = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+cfg = sys.argv[2] if len(sys.argv) > 2 else "3"  # config number, or N<edge> for an N^3 cube
 opts = dict(a.split("=") for a in sys.argv[3:])
 stream = torch.cuda.Stream()
 torch.cuda.set_stream(stream)
 ctx = P.Context(0, stream=stream)
 for k, v in opts.items():
     ctx.set_option(k, int(v))
-m = meshgen.block_mesh(CONFIGS[cfg]["N"])
+m = meshgen.block_mesh(int(cfg[1:]) if cfg.startswith("N") else CONFIGS[int(cfg)]["N"])
 mesh = P.Mesh(ctx, m)
 mesh.set_T(meshgen.canonical_field(m))
 flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")

@@ -106,7 +106,8 @@ def test_config4_closed_form(P):
 
 
 def test_config4_runtime_trips_closed_form(P):
-    """400^3 with 40% of phase 1's trips scheduled at run time (~168 trips,
+    """400^3 with 40% of phase 1's trips scheduled at run time (builds with
+    -DLF_DYN=1; static in the default build) (~168 trips,
     ~84 units per block: several rounds of the shared-memory claim slots):
     3 steps vs the exact decay, every solve converged in the diagonal run's
     iteration range."""

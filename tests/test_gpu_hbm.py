@@ -117,7 +117,8 @@ def test_l2_prefetch_bitwise_and_oracle(P_, name):
 
 @pytest.mark.parametrize("pct", [25, 100])
 def test_runtime_trips_deterministic_and_oracle(P_, pct):
-    """Run-time scheduled phase-1 trips (LF_OPT_DYNAMIC_TRIPS) on a mesh of
+    """Run-time scheduled phase-1 trips (LF_OPT_DYNAMIC_TRIPS; in builds with
+    -DLF_DYN=1 — the default build keeps the static schedule) on a mesh of
     several grid-stride trips with a ragged tail (~420K cells, mixed
     patches): T matches the oracle (4 steps, T 1e-8, iterations +-1) and a
     second run is BITWISE identical (per-unit sums, added in unit order)."""
